@@ -1,0 +1,596 @@
+/*
+ * hip_oracle.c — CPU ORACLE for HiP (Hierarchically Pruned Attention, arXiv 2406.09827).
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the plain, slow, obviously-correct reference that the
+ * CUDA path is checked against.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it.  It shares NO code, header, table or constant with the CUDA
+ * path (paper_2406_09827_b200/csrc); neither includes the other.
+ *
+ * Citation key: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n; G<n> = reading n in
+ * DESIGN.md §"Readings of the paper" (the same numbering as SURVEY.md §8c).
+ *
+ * What it computes (per batch b, query head h, query block q; kv head = h*Hkv/Hq):
+ *   - oracle_mask             Alg. 1 with block approximation, step by step:
+ *                             initial n = k/b_k nodes (G1), half-up rounding (G3), split into two
+ *                             branches, representative = FIRST block of each branch
+ *                             (G4), branch score = max of the b_q x b_k tile
+ *                             (P:178-180), keep the top-n branches with
+ *                             ties toward the smaller block (G10), until every node is one block
+ *                             (G5, G6).  Causal reading G7/G8.
+ *   - oracle_sparse_attention Eq. 2-3: softmax over the selected tokens only, fp64.
+ *   - oracle_dense_attention  S = QK^T, P = softmax(S), O = PV, fp64, causal optional.
+ *   - oracle_exact_block_topn top-n of the exact block-max scores (the textbook top-k of P:116 at
+ *                             block granularity) — used for pins and recall.
+ *   - *_paged                 the same on a paged KV cache (decode): token s of
+ *                             sequence b lives at page block_table[b][s / page_size], slot
+ *                             s % page_size; gathered with plain loops.
+ *
+ * Arithmetic.  Inputs are float32 arrays (bf16 inputs are widened exactly by the caller).  Mask
+ * scores come in two modes: ORC_F32C — `acc = fmaf(q[c], k[c], acc)` for c = 0..d-1 (the canonical
+ * fp32 order, reading G9), and ORC_F64 — the dot product in double.  Attention is fp64 throughout.
+ * Compile with -ffp-contract=off and without -ffast-math so that the written order is the order run.
+ *
+ * Pins (tests/test_oracle_pins.py): PIN-1 k >= T => dense causal attention (vs torch SDPA fp64);
+ * PIN-2 n < B_q <= 2n => exact top-n of block maxima (brute-force sort); PIN-3 monotone scores;
+ * PIN-4 worked examples; PIN-5 invariants;
+ * PIN-6 scale invariance; PIN-7 complexity counter; PIN-8 attention special cases.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_EINVAL 1
+#define ORC_ENOMEM 2
+#define ORC_ERANGE 3
+
+#define ORC_F32C 0
+#define ORC_F64 1
+
+typedef struct {
+    int64_t f, l; /* first / last key-block index of the range, inclusive */
+    double s;     /* score of the representative (= first) block         */
+} orc_node;
+
+static int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+/* Validation shared by every entry point. */
+static int check_dims(int B, int Hq, int Hkv, int Tq, int Tk, int d, int k, int bq, int bk, int causal)
+{
+    if (B < 1 || Hq < 1 || Hkv < 1 || Tq < 1 || Tk < 1 || d < 1) return ORC_EINVAL;
+    if (Hq % Hkv != 0) return ORC_EINVAL;
+    if (bq < 1 || bk < 1 || k < bk || k % bk != 0) return ORC_EINVAL; /* G12 */
+    if (causal && Tq > Tk) return ORC_EINVAL;                          /* G7  */
+    return ORC_OK;
+}
+
+/* Number of visible key blocks B_q of query block q (a1; causal reading G7:
+ * query row t sits at key position t + Tk - Tq, a block is visible if it starts at or before the
+ * position of the block's last row). */
+static int64_t visible_blocks(int64_t q, int bq, int bk, int Tq, int Tk, int causal)
+{
+    int64_t nkb = ((int64_t)Tk + bk - 1) / bk;
+    if (!causal) return nkb;
+    int64_t tlast = imin64((q + 1) * (int64_t)bq, Tq) - 1;
+    int64_t v = (tlast + (Tk - Tq)) / bk + 1;
+    return imin64(v, nkb);
+}
+
+/* Branch score: max over the b_q x b_k tile of q_t . k_s for the representative
+ * block j, restricted to valid pairs (s < Tk; causal: s <= t + Tk - Tq, reading G8).  No softmax
+ * scale (G11).  `emax` (optional) receives max over the pairs of sum_c |q_c k_c|, used
+ * to bound the rounding error of any fp32 evaluation order. */
+static double block_score(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
+                          int Tq, int Tk, int d, int causal, int mode, double *emax)
+{
+    int64_t delta = (int64_t)Tk - Tq;
+    int64_t s0 = j * bk, s1 = imin64((j + 1) * (int64_t)bk, Tk);
+    double best = -INFINITY, e_best = 0.0;
+    for (int64_t t = t0; t < t1; ++t) {
+        const float *q = Qh + t * d;
+        for (int64_t s = s0; s < s1; ++s) {
+            if (causal && s > t + delta) continue;
+            const float *kk = Kh + s * d;
+            double v, e = 0.0;
+            if (mode == ORC_F32C) {
+                float acc = 0.0f;
+                for (int c = 0; c < d; ++c) acc = fmaf(q[c], kk[c], acc);
+                v = (double)acc;
+                for (int c = 0; c < d; ++c) e += fabs((double)q[c] * (double)kk[c]);
+            } else {
+                double acc = 0.0;
+                for (int c = 0; c < d; ++c) {
+                    double p = (double)q[c] * (double)kk[c]; /* exact: 24+24 bit mantissas */
+                    acc += p;
+                    e += fabs(p);
+                }
+                v = acc;
+            }
+            if (v > best) best = v;
+            if (e > e_best) e_best = e;
+        }
+    }
+    if (emax) *emax = e_best;
+    return best;
+}
+
+/* Ranking of branches: larger score first; equal scores -> smaller first block (G10). */
+static int node_cmp(const void *pa, const void *pb)
+{
+    const orc_node *a = (const orc_node *)pa, *b = (const orc_node *)pb;
+    if (a->s > b->s) return -1;
+    if (a->s < b->s) return 1;
+    if (a->f < b->f) return -1;
+    if (a->f > b->f) return 1;
+    return 0;
+}
+
+static int i64_cmp(const void *pa, const void *pb)
+{
+    int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
+    return (a > b) - (a < b);
+}
+
+/* Per-unit diagnostics (all optional). */
+typedef struct {
+    double margin_min;   /* min over iterations of score(C[n-1]) - score(C[n]) (selection gap)   */
+    double emax;         /* max over all scored pairs of sum_c |q_c k_c|                          */
+    int64_t n_scored;    /* distinct representative blocks scored (PIN-7 counter)                 */
+    int32_t n_iter;      /* iterations run                                                        */
+} orc_diag;
+
+/*
+ * Alg. 1 for ONE query block, followed exactly:
+ *   line 4   initial nodes: n = k/b_k equal ranges over the visible blocks [0, B_q) (G1, G2),
+ *            f_j = round_half_up(j*B_q/n) = floor((2 j B_q + n) / (2n)) (G3), l_j = f_{j+1} - 1;
+ *   line 7-8 split every node at m = round_half_up((f+l)/2) = floor((f+l+1)/2) into (f, m-1) and
+ *            (m, l); a one-block node passes through unchanged (G5);
+ *   line 10-13 score each branch by its first block (G4) with the tile max;
+ *   line 14-15 keep the n best branches (G10 tie rule);
+ *   repeat until every node is a single block (G6); line 17: I = first blocks, ascending.
+ * Exact case (G1): B_q <= n selects every visible block.
+ * trace_nodes (optional) receives the node ranges after every iteration: [max_trace+1][n][2]
+ * (row 0 = initial partition); trace_scores [max_trace][n] the kept scores.
+ */
+static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t q, int n, int bq,
+                     int bk, int causal, int mode, int32_t *out_idx, int32_t *out_cnt, orc_diag *diag,
+                     int32_t *trace_nodes, double *trace_scores, int max_trace)
+{
+    int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
+    int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
+    orc_diag dg = {INFINITY, 0.0, 0, 0};
+
+    if (Bq <= n) { /* exact case */
+        for (int64_t j = 0; j < n; ++j) out_idx[j] = j < Bq ? (int32_t)j : -1;
+        *out_cnt = (int32_t)Bq;
+        if (diag) *diag = dg;
+        return ORC_OK;
+    }
+
+    double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
+    orc_node *nodes = (orc_node *)malloc(sizeof(orc_node) * (size_t)n);
+    orc_node *cand = (orc_node *)malloc(sizeof(orc_node) * 2 * (size_t)n);
+    int64_t *firsts = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    if (!memo || !nodes || !cand || !firsts) {
+        free(memo); free(nodes); free(cand); free(firsts);
+        return ORC_ENOMEM;
+    }
+    for (int64_t j = 0; j < Bq; ++j) memo[j] = NAN;
+
+    for (int j = 0; j < n; ++j) {
+        int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
+        int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
+        nodes[j].f = fj;
+        nodes[j].l = fj1 - 1;
+        nodes[j].s = NAN;
+    }
+    if (trace_nodes)
+        for (int j = 0; j < n; ++j) {
+            trace_nodes[2 * j] = (int32_t)nodes[j].f;
+            trace_nodes[2 * j + 1] = (int32_t)nodes[j].l;
+        }
+
+    for (;;) {
+        int any_split = 0;
+        for (int j = 0; j < n; ++j) any_split |= nodes[j].l > nodes[j].f;
+        if (!any_split) break;
+
+        int nc = 0;
+        for (int j = 0; j < n; ++j) {
+            int64_t f = nodes[j].f, l = nodes[j].l;
+            if (l == f) {
+                cand[nc].f = f; cand[nc].l = f; ++nc;
+            } else {
+                int64_t m = (f + l + 1) / 2;
+                cand[nc].f = f; cand[nc].l = m - 1; ++nc;
+                cand[nc].f = m; cand[nc].l = l; ++nc;
+            }
+        }
+        for (int c = 0; c < nc; ++c) {
+            int64_t r = cand[c].f; /* representative = first block of the branch */
+            if (isnan(memo[r])) {
+                double e = 0.0;
+                memo[r] = block_score(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, &e);
+                if (e > dg.emax) dg.emax = e;
+                dg.n_scored++;
+            }
+            cand[c].s = memo[r];
+        }
+        qsort(cand, (size_t)nc, sizeof(orc_node), node_cmp);
+        if (nc > n) {
+            double gap = cand[n - 1].s - cand[n].s;
+            if (gap < dg.margin_min) dg.margin_min = gap;
+        }
+        memcpy(nodes, cand, sizeof(orc_node) * (size_t)n);
+        if (trace_nodes && dg.n_iter < max_trace) {
+            int32_t *tn = trace_nodes + (size_t)(dg.n_iter + 1) * 2 * n;
+            for (int j = 0; j < n; ++j) {
+                tn[2 * j] = (int32_t)nodes[j].f;
+                tn[2 * j + 1] = (int32_t)nodes[j].l;
+                if (trace_scores) trace_scores[(size_t)dg.n_iter * n + j] = nodes[j].s;
+            }
+        }
+        dg.n_iter++;
+    }
+
+    for (int j = 0; j < n; ++j) firsts[j] = nodes[j].f;
+    qsort(firsts, (size_t)n, sizeof(int64_t), i64_cmp);
+    for (int j = 0; j < n; ++j) out_idx[j] = (int32_t)firsts[j];
+    *out_cnt = n;
+    if (diag) *diag = dg;
+    free(memo); free(nodes); free(cand); free(firsts);
+    return ORC_OK;
+}
+
+/* -------------------------------------------------------------------------------------------- */
+/* Contiguous layout: Q [B, Hq, Tq, d], K/V [B, Hkv, Tk, d], all row-major float32.               */
+/* idx [B, Hq, Nqb, n] int32 ascending, -1 padded; cnt [B, Hq, Nqb].                              */
+/* Optional per-unit outputs (NULL to skip): margin_min, emax (double), n_scored (int64), n_iter. */
+/* -------------------------------------------------------------------------------------------- */
+int oracle_mask(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
+                int bq, int bk, int causal, int mode, int32_t *idx, int32_t *cnt, double *margin_min,
+                double *emax, int64_t *n_scored, int32_t *n_iter)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    int n = k / bk;
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int64_t units = (int64_t)B * Hq * nqb;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t u = 0; u < units; ++u) {
+        int64_t q = u % nqb, bh = u / nqb;
+        int64_t b = bh / Hq, h = bh % Hq, hk = h / (Hq / Hkv);
+        const float *Qh = Q + ((b * Hq + h) * (int64_t)Tq) * d;
+        const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
+        orc_diag dg;
+        int r = mask_unit(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, idx + u * n, cnt + u, &dg, NULL,
+                          NULL, 0);
+        if (r) {
+#pragma omp critical
+            err = r;
+        }
+        if (margin_min) margin_min[u] = dg.margin_min;
+        if (emax) emax[u] = dg.emax;
+        if (n_scored) n_scored[u] = dg.n_scored;
+        if (n_iter) n_iter[u] = dg.n_iter;
+    }
+    return err;
+}
+
+/* Node trace of one unit (for the invariant pins, PIN-5).  trace_nodes: [(max_trace+1) * n * 2],
+ * trace_scores: [max_trace * n]; *n_iter receives the iteration count. */
+int oracle_mask_trace(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
+                      int bq, int bk, int causal, int mode, int b, int h, int q, int32_t *idx_out,
+                      int32_t *cnt_out, int32_t *trace_nodes, double *trace_scores, int max_trace,
+                      int32_t *n_iter, int64_t *n_scored)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    int hk = h / (Hq / Hkv);
+    const float *Qh = Q + (((int64_t)b * Hq + h) * (int64_t)Tq) * d;
+    const float *Kh = K + (((int64_t)b * Hkv + hk) * (int64_t)Tk) * d;
+    orc_diag dg;
+    rc = mask_unit(Qh, Kh, Tq, Tk, d, q, k / bk, bq, bk, causal, mode, idx_out, cnt_out, &dg, trace_nodes,
+                   trace_scores, max_trace);
+    if (n_iter) *n_iter = dg.n_iter;
+    if (n_scored) *n_scored = dg.n_scored;
+    return rc;
+}
+
+/* Exact block-level top-n (textbook top-k, at key-block granularity with the same tile
+ * score and tie rule): used by PIN-2 and for mask recall. */
+int oracle_exact_block_topn(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d,
+                            int k, int bq, int bk, int causal, int mode, int32_t *idx, int32_t *cnt)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    int n = k / bk;
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int64_t units = (int64_t)B * Hq * nqb;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t u = 0; u < units; ++u) {
+        int64_t q = u % nqb, bh = u / nqb;
+        int64_t b = bh / Hq, h = bh % Hq, hk = h / (Hq / Hkv);
+        const float *Qh = Q + ((b * Hq + h) * (int64_t)Tq) * d;
+        const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
+        int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
+        int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
+        orc_node *all = (orc_node *)malloc(sizeof(orc_node) * (size_t)Bq);
+        int64_t *firsts = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+        if (!all || !firsts) {
+            free(all); free(firsts);
+#pragma omp critical
+            err = ORC_ENOMEM;
+            continue;
+        }
+        for (int64_t j = 0; j < Bq; ++j) {
+            all[j].f = all[j].l = j;
+            all[j].s = block_score(Qh, Kh, t0, t1, j, bk, Tq, Tk, d, causal, mode, NULL);
+        }
+        qsort(all, (size_t)Bq, sizeof(orc_node), node_cmp);
+        int64_t m = imin64(Bq, n);
+        for (int64_t j = 0; j < m; ++j) firsts[j] = all[j].f;
+        qsort(firsts, (size_t)m, sizeof(int64_t), i64_cmp);
+        for (int64_t j = 0; j < n; ++j) idx[u * n + j] = j < m ? (int32_t)firsts[j] : -1;
+        cnt[u] = (int32_t)m;
+        free(all); free(firsts);
+    }
+    return err;
+}
+
+/* Representative-block scores for a list of (b, h, q, j) tuples (certification of near-ties):
+ * scores[i] = tile max (mode), emax[i] = max_pairs sum_c |q_c k_c|. */
+int oracle_block_scores(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d,
+                        int bq, int bk, int causal, int mode, const int32_t *tuples, int64_t m,
+                        double *scores, double *emax)
+{
+    if (check_dims(B, Hq, Hkv, Tq, Tk, d, bk, bq, bk, causal)) return ORC_EINVAL;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+        int64_t b = tuples[4 * i], h = tuples[4 * i + 1], q = tuples[4 * i + 2], j = tuples[4 * i + 3];
+        int64_t nkb = ((int64_t)Tk + bk - 1) / bk, nqb = ((int64_t)Tq + bq - 1) / bq;
+        if (b < 0 || b >= B || h < 0 || h >= Hq || q < 0 || q >= nqb || j < 0 || j >= nkb) {
+#pragma omp critical
+            err = ORC_ERANGE;
+            continue;
+        }
+        int64_t hk = h / (Hq / Hkv);
+        const float *Qh = Q + ((b * Hq + h) * (int64_t)Tq) * d;
+        const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
+        int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
+        double e = 0.0;
+        scores[i] = block_score(Qh, Kh, t0, t1, j, bk, Tq, Tk, d, causal, mode, &e);
+        if (emax) emax[i] = e;
+    }
+    return err;
+}
+
+/* -------------------------------------------------------------------------------------------- */
+/* Attention (Eq. 2-3), fp64.  Row t of query block q attends to the tokens of the     */
+/* selected key blocks that are < Tk and (causal) <= t + Tk - Tq, visited in ascending order.     */
+/* Softmax scale sm_scale (G11; <= 0 means 1/sqrt(d)).  Empty row: O = 0, lse = -inf (G13).       */
+/* O [B, Hq, Tq, d] double, lse [B, Hq, Tq] double (optional).                                    */
+/* -------------------------------------------------------------------------------------------- */
+static void attend_row(const float *q, const float *Kh, const float *Vh, int Tk, int d, const int64_t *tok,
+                       int64_t ntok, double sm_scale, double *o, double *lse)
+{
+    if (ntok == 0) {
+        for (int c = 0; c < d; ++c) o[c] = 0.0;
+        if (lse) *lse = -INFINITY;
+        return;
+    }
+    double *x = (double *)malloc(sizeof(double) * (size_t)ntok);
+    double M = -INFINITY;
+    for (int64_t i = 0; i < ntok; ++i) {
+        const float *kk = Kh + tok[i] * d;
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c) acc += (double)q[c] * (double)kk[c];
+        x[i] = sm_scale * acc;
+        if (x[i] > M) M = x[i];
+    }
+    double Z = 0.0;
+    for (int c = 0; c < d; ++c) o[c] = 0.0;
+    for (int64_t i = 0; i < ntok; ++i) {
+        double p = exp(x[i] - M);
+        Z += p;
+        const float *vv = Vh + tok[i] * d;
+        for (int c = 0; c < d; ++c) o[c] += p * (double)vv[c];
+    }
+    for (int c = 0; c < d; ++c) o[c] /= Z;
+    if (lse) *lse = M + log(Z);
+    (void)Tk;
+    free(x);
+}
+
+/* Shared driver: dense = 1 attends to every visible key; else the idx/cnt selection. */
+static int attention_impl(const float *Q, const float *K, const float *V, int B, int Hq, int Hkv, int Tq,
+                          int Tk, int d, int n, int bq, int bk, int causal, double sm_scale,
+                          const int32_t *idx, const int32_t *cnt, int dense, double *O, double *lse)
+{
+    if (sm_scale <= 0.0) sm_scale = 1.0 / sqrt((double)d);
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int64_t nkb = ((int64_t)Tk + bk - 1) / bk;
+    int64_t delta = (int64_t)Tk - Tq;
+    int64_t rows = (int64_t)B * Hq * Tq;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < rows; ++r) {
+        int64_t t = r % Tq, bh = r / Tq;
+        int64_t b = bh / Hq, h = bh % Hq, hk = h / (Hq / Hkv);
+        int64_t q = t / bq, u = bh * nqb + q;
+        const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
+        const float *Vh = V + ((b * Hkv + hk) * (int64_t)Tk) * d;
+        int64_t cap = dense ? (int64_t)Tk : (int64_t)n * bk;
+        int64_t *tok = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cap > 0 ? cap : 1));
+        int64_t ntok = 0;
+        int bad = 0;
+        if (dense) {
+            for (int64_t s = 0; s < Tk; ++s)
+                if (!causal || s <= t + delta) tok[ntok++] = s;
+        } else {
+            int32_t c = cnt[u];
+            if (c < 0 || c > n) bad = 1;
+            int64_t prev = -1;
+            for (int32_t i = 0; !bad && i < c; ++i) {
+                int64_t j = idx[u * n + i];
+                if (j < 0 || j >= nkb || j <= prev) { bad = 1; break; } /* S:309 index out of range */
+                prev = j;
+                for (int64_t s = j * bk; s < imin64((j + 1) * (int64_t)bk, Tk); ++s)
+                    if (!causal || s <= t + delta) tok[ntok++] = s;
+            }
+        }
+        if (bad) {
+#pragma omp critical
+            err = ORC_ERANGE;
+        } else {
+            attend_row(Q + r * d, Kh, Vh, Tk, d, tok, ntok, sm_scale, O + r * d, lse ? lse + r : NULL);
+        }
+        free(tok);
+    }
+    return err;
+}
+
+int oracle_sparse_attention(const float *Q, const float *K, const float *V, int B, int Hq, int Hkv, int Tq,
+                            int Tk, int d, int k, int bq, int bk, int causal, double sm_scale,
+                            const int32_t *idx, const int32_t *cnt, double *O, double *lse)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, k / bk, bq, bk, causal, sm_scale, idx, cnt, 0, O,
+                          lse);
+}
+
+int oracle_dense_attention(const float *Q, const float *K, const float *V, int B, int Hq, int Hkv, int Tq,
+                           int Tk, int d, int causal, double sm_scale, double *O, double *lse)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, 1, 1, 1, causal);
+    if (rc) return rc;
+    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, 1, 1, 1, causal, sm_scale, NULL, NULL, 1, O, lse);
+}
+
+/* -------------------------------------------------------------------------------------------- */
+/* Paged KV cache (decode).  pages: [num_pages, Hkv, page_size, d] float32 row-major.       */
+/* Sequence b has Tk = seq_lens[b] tokens; token s is at page block_table[b*max_pages + s/ps],     */
+/* slot s % ps.  Q [B, Hq, Tq, d] with the same Tq for every sequence (Tq = 1 for plain decode).   */
+/* The oracle gathers each (b, kv-head) into a contiguous [Tk, d] buffer with plain loops and runs  */
+/* the contiguous routines on it.                                                                  */
+/* -------------------------------------------------------------------------------------------- */
+static float *gather_paged(const float *pages, int num_pages, int Hkv, int ps, int d,
+                           const int32_t *block_table, int max_pages, int b, int hk, int Tk, int *err)
+{
+    float *out = (float *)malloc(sizeof(float) * (size_t)Tk * d);
+    if (!out) { *err = ORC_ENOMEM; return NULL; }
+    for (int64_t s = 0; s < Tk; ++s) {
+        int64_t pi = s / ps;
+        if (pi >= max_pages) { *err = ORC_ERANGE; free(out); return NULL; }
+        int64_t page = block_table[(int64_t)b * max_pages + pi];
+        if (page < 0 || page >= num_pages) { *err = ORC_ERANGE; free(out); return NULL; }
+        const float *src = pages + (((page * Hkv + hk) * (int64_t)ps) + s % ps) * d;
+        memcpy(out + s * d, src, sizeof(float) * (size_t)d);
+    }
+    return out;
+}
+
+int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int page_size,
+                      const int32_t *block_table, int max_pages, const int32_t *seq_lens, int B, int Hq,
+                      int Hkv, int Tq, int d, int k, int bq, int bk, int causal, int mode, int32_t *idx,
+                      int32_t *cnt, double *margin_min, double *emax, int64_t *n_scored, int32_t *n_iter)
+{
+    if (page_size < 1 || page_size % bk != 0 || num_pages < 1) return ORC_EINVAL;
+    int n = k / bk;
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int err = ORC_OK;
+    for (int b = 0; b < B && !err; ++b) {
+        int Tk = seq_lens[b];
+        int rc = check_dims(1, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+        if (rc) return rc;
+        for (int hk = 0; hk < Hkv && !err; ++hk) {
+            float *Kh = gather_paged(Kpages, num_pages, Hkv, page_size, d, block_table, max_pages, b, hk, Tk,
+                                     &err);
+            if (!Kh) break;
+            int g = Hq / Hkv;
+#pragma omp parallel for schedule(dynamic, 1)
+            for (int64_t w = 0; w < (int64_t)g * nqb; ++w) {
+                int64_t h = (int64_t)hk * g + w / nqb, q = w % nqb;
+                int64_t u = ((int64_t)b * Hq + h) * nqb + q;
+                const float *Qh = Q + (((int64_t)b * Hq + h) * (int64_t)Tq) * d;
+                orc_diag dg;
+                int r = mask_unit(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, idx + u * n, cnt + u, &dg,
+                                  NULL, NULL, 0);
+                if (r) {
+#pragma omp critical
+                    err = r;
+                }
+                if (margin_min) margin_min[u] = dg.margin_min;
+                if (emax) emax[u] = dg.emax;
+                if (n_scored) n_scored[u] = dg.n_scored;
+                if (n_iter) n_iter[u] = dg.n_iter;
+            }
+            free(Kh);
+        }
+    }
+    return err;
+}
+
+int oracle_sparse_attention_paged(const float *Q, const float *Kpages, const float *Vpages, int num_pages,
+                                  int page_size, const int32_t *block_table, int max_pages,
+                                  const int32_t *seq_lens, int B, int Hq, int Hkv, int Tq, int d, int k, int bq,
+                                  int bk, int causal, double sm_scale, const int32_t *idx, const int32_t *cnt,
+                                  double *O, double *lse)
+{
+    if (page_size < 1 || page_size % bk != 0 || num_pages < 1) return ORC_EINVAL;
+    int n = k / bk;
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int err = ORC_OK;
+    for (int b = 0; b < B && !err; ++b) {
+        int Tk = seq_lens[b];
+        int rc = check_dims(1, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+        if (rc) return rc;
+        for (int hk = 0; hk < Hkv && !err; ++hk) {
+            float *Kh = gather_paged(Kpages, num_pages, Hkv, page_size, d, block_table, max_pages, b, hk, Tk,
+                                     &err);
+            if (!Kh) break;
+            float *Vh = gather_paged(Vpages, num_pages, Hkv, page_size, d, block_table, max_pages, b, hk, Tk,
+                                     &err);
+            if (!Vh) { free(Kh); break; }
+            int g = Hq / Hkv;
+            for (int hh = 0; hh < g && !err; ++hh) {
+                int64_t h = (int64_t)hk * g + hh;
+                int64_t off = ((int64_t)b * Hq + h);
+                /* one (b, h) slice as a B=Hq=Hkv=1 problem */
+                rc = attention_impl(Q + off * Tq * d, Kh, Vh, 1, 1, 1, Tq, Tk, d, n, bq, bk, causal, sm_scale,
+                                    idx + off * nqb * n, cnt + off * nqb, 0, O + off * Tq * d,
+                                    lse ? lse + off * Tq : NULL);
+                if (rc) err = rc;
+            }
+            free(Kh);
+            free(Vh);
+        }
+    }
+    return err;
+}
+
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void oracle_set_num_threads(int t)
+{
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}

@@ -1,0 +1,237 @@
+"""ctypes front-end of the CPU oracle (oracle/hip_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs may import this module; the product package never does.
+
+Every function takes numpy arrays (or anything numpy can view) and widens them to float32 exactly
+(bf16 -> fp32 is exact); the arithmetic happens in C (see the header of hip_oracle.c for the
+citations of each step).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hip_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+F32C = 0  # canonical fp32: acc = fmaf(q[c], k[c], acc), c = 0..d-1 (reading G9)
+F64 = 1   # fp64 dot products
+
+_ERR = {1: "invalid value", 2: "out of memory", 3: "index out of range"}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C99 + OpenMP, no fast-math, no FP contraction).
+
+    HIP_ORACLE_LIB overrides the library path (used by tests/mutants.py to check that the pins
+    kill deliberately broken oracles)."""
+    if os.environ.get("HIP_ORACLE_LIB"):
+        return os.environ["HIP_ORACLE_LIB"]
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c99", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        i32, i64, f64 = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        P = ctypes.c_void_p
+        _lib.oracle_mask.argtypes = [P, P] + [i32] * 11 + [P] * 6
+        _lib.oracle_mask_trace.argtypes = [P, P] + [i32] * 11 + [i32] * 3 + [P, P, P, P, i32, P, P]
+        _lib.oracle_exact_block_topn.argtypes = [P, P] + [i32] * 11 + [P, P]
+        _lib.oracle_block_scores.argtypes = [P, P] + [i32] * 10 + [P, i64, P, P]
+        _lib.oracle_sparse_attention.argtypes = [P, P, P] + [i32] * 10 + [f64, P, P, P, P]
+        _lib.oracle_dense_attention.argtypes = [P, P, P] + [i32] * 7 + [f64, P, P]
+        _lib.oracle_mask_paged.argtypes = [P, P, i32, i32, P, i32, P] + [i32] * 9 + [P] * 6
+        _lib.oracle_sparse_attention_paged.argtypes = ([P, P, P, i32, i32, P, i32, P] + [i32] * 9
+                                                       + [f64, P, P, P, P])
+        _lib.oracle_num_threads.restype = i32
+        _lib.oracle_set_num_threads.argtypes = [i32]
+        for name in ("oracle_mask", "oracle_mask_trace", "oracle_exact_block_topn", "oracle_block_scores",
+                     "oracle_sparse_attention", "oracle_dense_attention", "oracle_mask_paged",
+                     "oracle_sparse_attention_paged"):
+            getattr(_lib, name).restype = i32
+    return _lib
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+def set_num_threads(t: int) -> None:
+    lib().oracle_set_num_threads(int(t))
+
+
+def _f32(a) -> np.ndarray:
+    if hasattr(a, "detach"):  # torch tensor: widen exactly on the host
+        a = a.detach().cpu().float().numpy()
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _i32(a) -> np.ndarray:
+    if hasattr(a, "detach"):
+        a = a.detach().cpu().numpy()
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise ValueError(f"{what}: {_ERR.get(rc, rc)}")
+
+
+def n_blocks(k: int, bk: int) -> int:
+    return k // bk
+
+
+def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: bool = False):
+    """Alg. 1 mask. Q [B,Hq,Tq,d], K [B,Hkv,Tk,d] -> idx [B,Hq,Nqb,n] (asc, -1 pad), cnt [B,Hq,Nqb].
+
+    diag=True also returns dict(margin_min, emax, n_scored, n_iter) per unit."""
+    Q, K = _f32(Q), _f32(K)
+    B, Hq, Tq, d = Q.shape
+    _, Hkv, Tk, _ = K.shape
+    n = k // bk if bk > 0 else 0
+    nqb = -(-Tq // bq) if bq > 0 else 0
+    idx = np.empty((B, Hq, nqb, max(n, 1)), np.int32)
+    cnt = np.empty((B, Hq, nqb), np.int32)
+    mg = np.empty((B, Hq, nqb), np.float64)
+    em = np.empty((B, Hq, nqb), np.float64)
+    ns = np.empty((B, Hq, nqb), np.int64)
+    ni = np.empty((B, Hq, nqb), np.int32)
+    rc = lib().oracle_mask(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, _p(idx), _p(cnt),
+                           _p(mg), _p(em), _p(ns), _p(ni))
+    _check(rc, "oracle_mask")
+    if diag:
+        return idx, cnt, dict(margin_min=mg, emax=em, n_scored=ns, n_iter=ni)
+    return idx, cnt
+
+
+def mask_trace(Q, K, k: int, bq: int, bk: int, causal: bool, b: int, h: int, q: int, mode: int = F32C,
+               max_trace: int = 64):
+    """Node ranges after every iteration of one unit: list of [n,2] arrays (entry 0 = initial)."""
+    Q, K = _f32(Q), _f32(K)
+    B, Hq, Tq, d = Q.shape
+    _, Hkv, Tk, _ = K.shape
+    n = k // bk
+    idx = np.empty(n, np.int32)
+    cnt = np.empty(1, np.int32)
+    tn = np.full(((max_trace + 1), n, 2), -7, np.int32)
+    ts = np.full((max_trace, n), np.nan, np.float64)
+    nit = np.zeros(1, np.int32)
+    nsc = np.zeros(1, np.int64)
+    rc = lib().oracle_mask_trace(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, b, h, q,
+                                 _p(idx), _p(cnt), _p(tn), _p(ts), max_trace, _p(nit), _p(nsc))
+    _check(rc, "oracle_mask_trace")
+    it = int(nit[0])
+    return dict(idx=idx, cnt=int(cnt[0]), nodes=[tn[i] for i in range(it + 1)] if it else [],
+                scores=[ts[i] for i in range(it)], n_iter=it, n_scored=int(nsc[0]))
+
+
+def exact_block_topn(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C):
+    Q, K = _f32(Q), _f32(K)
+    B, Hq, Tq, d = Q.shape
+    _, Hkv, Tk, _ = K.shape
+    n = k // bk
+    nqb = -(-Tq // bq)
+    idx = np.empty((B, Hq, nqb, n), np.int32)
+    cnt = np.empty((B, Hq, nqb), np.int32)
+    rc = lib().oracle_exact_block_topn(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode,
+                                       _p(idx), _p(cnt))
+    _check(rc, "oracle_exact_block_topn")
+    return idx, cnt
+
+
+def block_scores(Q, K, bq: int, bk: int, causal: bool, tuples, mode: int = F64):
+    """Tile-max scores for (b, h, q, j) tuples -> (scores, emax)."""
+    Q, K = _f32(Q), _f32(K)
+    B, Hq, Tq, d = Q.shape
+    _, Hkv, Tk, _ = K.shape
+    t = np.ascontiguousarray(np.asarray(tuples, np.int32).reshape(-1, 4))
+    sc = np.empty(len(t), np.float64)
+    em = np.empty(len(t), np.float64)
+    rc = lib().oracle_block_scores(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, bq, bk, int(causal), mode, _p(t),
+                                   len(t), _p(sc), _p(em))
+    _check(rc, "oracle_block_scores")
+    return sc, em
+
+
+def sparse_attention(Q, K, V, k: int, bq: int, bk: int, causal: bool, idx, cnt, sm_scale: float = 0.0):
+    """Eq. 2-3 in fp64 over the selection idx/cnt -> (O [B,Hq,Tq,d] f64, lse [B,Hq,Tq] f64)."""
+    Q, K, V = _f32(Q), _f32(K), _f32(V)
+    idx, cnt = _i32(idx), _i32(cnt)
+    B, Hq, Tq, d = Q.shape
+    _, Hkv, Tk, _ = K.shape
+    O = np.empty((B, Hq, Tq, d), np.float64)
+    lse = np.empty((B, Hq, Tq), np.float64)
+    rc = lib().oracle_sparse_attention(_p(Q), _p(K), _p(V), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal),
+                                       float(sm_scale), _p(idx), _p(cnt), _p(O), _p(lse))
+    _check(rc, "oracle_sparse_attention")
+    return O, lse
+
+
+def dense_attention(Q, K, V, causal: bool, sm_scale: float = 0.0):
+    Q, K, V = _f32(Q), _f32(K), _f32(V)
+    B, Hq, Tq, d = Q.shape
+    _, Hkv, Tk, _ = K.shape
+    O = np.empty((B, Hq, Tq, d), np.float64)
+    lse = np.empty((B, Hq, Tq), np.float64)
+    rc = lib().oracle_dense_attention(_p(Q), _p(K), _p(V), B, Hq, Hkv, Tq, Tk, d, int(causal),
+                                      float(sm_scale), _p(O), _p(lse))
+    _check(rc, "oracle_dense_attention")
+    return O, lse
+
+
+def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causal: bool, mode: int = F32C,
+               diag: bool = False):
+    """Mask on a paged cache. Kpages [num_pages, Hkv, page_size, d]; block_table [B, max_pages]."""
+    Q, Kp = _f32(Q), _f32(Kpages)
+    bt, sl = _i32(block_table), _i32(seq_lens)
+    B, Hq, Tq, d = Q.shape
+    num_pages, Hkv, ps, _ = Kp.shape
+    n = k // bk
+    nqb = -(-Tq // bq)
+    idx = np.empty((B, Hq, nqb, n), np.int32)
+    cnt = np.empty((B, Hq, nqb), np.int32)
+    mg = np.empty((B, Hq, nqb), np.float64)
+    em = np.empty((B, Hq, nqb), np.float64)
+    ns = np.empty((B, Hq, nqb), np.int64)
+    ni = np.empty((B, Hq, nqb), np.int32)
+    rc = lib().oracle_mask_paged(_p(Q), _p(Kp), num_pages, ps, _p(bt), bt.shape[1], _p(sl), B, Hq, Hkv, Tq, d,
+                                 k, bq, bk, int(causal), mode, _p(idx), _p(cnt), _p(mg), _p(em), _p(ns), _p(ni))
+    _check(rc, "oracle_mask_paged")
+    if diag:
+        return idx, cnt, dict(margin_min=mg, emax=em, n_scored=ns, n_iter=ni)
+    return idx, cnt
+
+
+def sparse_attention_paged(Q, Kpages, Vpages, block_table, seq_lens, k: int, bq: int, bk: int, causal: bool,
+                           idx, cnt, sm_scale: float = 0.0):
+    Q, Kp, Vp = _f32(Q), _f32(Kpages), _f32(Vpages)
+    bt, sl = _i32(block_table), _i32(seq_lens)
+    idx, cnt = _i32(idx), _i32(cnt)
+    B, Hq, Tq, d = Q.shape
+    num_pages, Hkv, ps, _ = Kp.shape
+    O = np.empty((B, Hq, Tq, d), np.float64)
+    lse = np.empty((B, Hq, Tq), np.float64)
+    rc = lib().oracle_sparse_attention_paged(_p(Q), _p(Kp), _p(Vp), num_pages, ps, _p(bt), bt.shape[1], _p(sl),
+                                             B, Hq, Hkv, Tq, d, k, bq, bk, int(causal), float(sm_scale),
+                                             _p(idx), _p(cnt), _p(O), _p(lse))
+    _check(rc, "oracle_sparse_attention_paged")
+    return O, lse

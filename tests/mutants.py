@@ -1,0 +1,57 @@
+"""Mutation check of the oracle pins (run by hand: python tests/mutants.py).
+
+Each mutant is a plausible mistake in oracle/hip_oracle.c (a dropped term, a wrong index, a flipped
+rule).  The pin suite (tests/test_oracle_pins.py) must fail on every one of them."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "oracle", "hip_oracle.c")
+
+MUTANTS = {
+    "representative = last block of the branch": ("int64_t r = cand[c].f;", "int64_t r = cand[c].l;"),
+    "tie-break toward larger block": ("if (a->f < b->f) return -1;\n    if (a->f > b->f) return 1;",
+                                      "if (a->f > b->f) return -1;\n    if (a->f < b->f) return 1;"),
+    "no causal mask inside the tile": ("if (causal && s > t + delta) continue;\n            const float *kk",
+                                       "const float *kk"),
+    "tile max over the first query row only": ("for (int64_t t = t0; t < t1; ++t) {\n        const float *q = Qh",
+                                               "for (int64_t t = t0; t < t0 + 1; ++t) {\n        const float *q = Qh"),
+    "causal bound off by one block": ("int64_t v = (tlast + (Tk - Tq)) / bk + 1;", "int64_t v = (tlast + (Tk - Tq)) / bk;"),
+    "initial partition rounds down": ("int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);",
+                                      "int64_t fj = (2 * (int64_t)j * Bq) / (2 * (int64_t)n);"),
+    "keep bottom-n": ("if (a->s > b->s) return -1;\n    if (a->s < b->s) return 1;",
+                      "if (a->s < b->s) return -1;\n    if (a->s > b->s) return 1;"),
+    "attention drops the max subtraction": ("double p = exp(x[i] - M);", "double p = exp(x[i]);"),
+    "attention forgets the softmax scale": ("x[i] = sm_scale * acc;", "x[i] = acc;"),
+    # (Bq < n instead of Bq <= n is an EQUIVALENT mutant: with B_q == n every initial node is one
+    #  block, the loop never splits and the output is again 0..n-1.)
+    "exact case up to 2n": ("if (Bq <= n) { /* exact case */", "if (Bq <= 2 * n) { /* exact case */"),
+    "split rounds half down": ("int64_t m = (f + l + 1) / 2;", "int64_t m = (f + l) / 2;"),
+    "paged slot uses page index": ("+ s % ps) * d;", "+ s / ps % ps) * d;"),
+}
+
+
+def main():
+    src = open(SRC).read()
+    survived = []
+    for name, (a, b) in MUTANTS.items():
+        assert a in src, name
+        path = f"/tmp/mut/{abs(hash(name))}.c"
+        open(path, "w").write(src.replace(a, b, 1))
+        lib = path[:-2] + ".so"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-o", lib, path, "-lm"])
+        env = dict(os.environ, HIP_ORACLE_LIB=lib)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                           env=env, capture_output=True, text=True, cwd=ROOT)
+        killed = r.returncode != 0
+        print(f"{'KILLED ' if killed else 'SURVIVED'}  {name}")
+        if not killed:
+            survived.append(name)
+    print("survivors:", survived)
+    return 1 if survived else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,436 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (no GPU).
+
+Each test names the pin and the passage it follows.  Library routines used as
+independent references: torch SDPA (fp64) for dense attention, numpy matmul + sort for brute-force
+top-n.  Integer-valued inputs make every score exact, so ties and tie-breaks are tested bit-exactly.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2406_09827_b200 import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")
+
+
+def _qk_from_scores(scores):
+    """q = (1, 0), key s = (score_s, 0): q . k_s = score_s exactly."""
+    T = len(scores)
+    Q = np.zeros((1, 1, 1, 2), np.float32)
+    Q[..., 0] = 1.0
+    K = np.zeros((1, 1, T, 2), np.float32)
+    K[0, 0, :, 0] = np.asarray(scores, np.float32)
+    return Q, K
+
+
+def _brute_block_scores(Q, K, bq, bk, causal):
+    """[B,Hq,Nqb,Nkb] tile maxima by full matmul (library primitive) + masking; -inf = invisible."""
+    Q = np.asarray(Q, np.float64)
+    K = np.asarray(K, np.float64)
+    B, Hq, Tq, d = Q.shape
+    Hkv, Tk = K.shape[1], K.shape[2]
+    g = Hq // Hkv
+    nqb, nkb = -(-Tq // bq), -(-Tk // bk)
+    out = np.full((B, Hq, nqb, nkb), -np.inf)
+    t = np.arange(Tq)[:, None]
+    s = np.arange(Tk)[None, :]
+    valid = (s <= t + (Tk - Tq)) if causal else np.ones((Tq, Tk), bool)
+    for b in range(B):
+        for h in range(Hq):
+            S = Q[b, h] @ K[b, h // g].T
+            S = np.where(valid, S, -np.inf)
+            for q in range(nqb):
+                rows = S[q * bq:(q + 1) * bq]
+                for j in range(nkb):
+                    out[b, h, q, j] = rows[:, j * bk:(j + 1) * bk].max()
+    return out
+
+
+def _visible(q, bq, bk, Tq, Tk, causal):
+    nkb = -(-Tk // bk)
+    if not causal:
+        return nkb
+    tlast = min((q + 1) * bq, Tq) - 1
+    return min((tlast + Tk - Tq) // bk + 1, nkb)
+
+
+def _topn_sorted(scores_row, n):
+    """Exact top-n of a score vector, ties -> smaller index (np.lexsort), returned ascending."""
+    idx = np.arange(len(scores_row))
+    order = np.lexsort((idx, -scores_row))
+    return np.sort(order[:n])
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-4: worked examples (paper P:902-904)
+# --------------------------------------------------------------------------------------------
+def test_pin4_token_traces(orc):
+    gold = json.load(open(GOLD))
+    for case in gold["token_traces"]:
+        Q, K = _qk_from_scores(case["scores"])
+        idx, cnt = orc.mask(Q, K, case["k"], case["b_q"], case["b_k"], case["causal"], mode=orc.F32C)
+        got = idx[0, 0, 0, : cnt[0, 0, 0]].tolist()
+        assert got == case["expect"], case["name"]
+        idx64, _ = orc.mask(Q, K, case["k"], case["b_q"], case["b_k"], case["causal"], mode=orc.F64)
+        assert idx64[0, 0, 0, : cnt[0, 0, 0]].tolist() == case["expect"]
+        if "exact_top" in case:  # the greedy miss really is a miss
+            ex, ecnt = orc.exact_block_topn(Q, K, case["k"], case["b_q"], case["b_k"], case["causal"])
+            assert ex[0, 0, 0, : ecnt[0, 0, 0]].tolist() == case["exact_top"]
+
+
+def test_pin4_block_trace(orc):
+    gold = json.load(open(GOLD))
+    for case in gold["block_traces"]:
+        T, bq, bk = case["T"], case["b_q"], case["b_k"]
+        Q = np.zeros((1, 1, T, 2), np.float32)
+        Q[..., 0] = 1.0
+        K = np.zeros((1, 1, T, 2), np.float32)
+        for j, m in enumerate(case["block_max"]):
+            K[0, 0, j * bk, 0] = m
+            K[0, 0, j * bk + 1, 0] = m - 0.5
+        idx, cnt = orc.mask(Q, K, case["k"], bq, bk, case["causal"])
+        for q in range(T // bq):
+            assert idx[0, 0, q, : cnt[0, 0, q]].tolist() == case["expect"], case["name"]
+
+
+def _split_observed(orc, node, favour_right):
+    """Observe the branches of a node through the first iteration of a unit whose single node is
+    `node` (n = 1) or, for the pass-through case, n = 2 over 3 blocks."""
+    f, l = node
+    if f == l:
+        nblocks, k = 3, 2
+    else:
+        assert f == 0
+        nblocks, k = l + 1, 1
+    scores = np.full(nblocks, 0.0, np.float32)
+    if f == l:
+        scores[l] = 9.0
+    else:
+        m = (f + l + 1) // 2 if favour_right else f
+        scores[m if favour_right else f] = 9.0
+    Q, K = _qk_from_scores(scores)
+    tr = orc.mask_trace(Q, K, k, 1, 1, False, 0, 0, 0)
+    return [tuple(r) for r in tr["nodes"][1].tolist()]
+
+
+def test_pin4_splits(orc):
+    gold = json.load(open(GOLD))
+    for case in gold["splits"]:
+        node, br = case["node"], [tuple(b) for b in case["branches"]]
+        if len(br) == 1:
+            kept = _split_observed(orc, node, True)
+            assert br[0] in kept, case["name"]
+        else:
+            assert _split_observed(orc, node, True) == [br[1]], case["name"]
+            assert _split_observed(orc, node, False) == [br[0]], case["name"]
+            # both branches non-empty and equal-sized up to one block
+            (a0, a1), (b0, b1) = br
+            assert a0 <= a1 and b0 <= b1 and abs((a1 - a0) - (b1 - b0)) <= 1
+
+
+def test_pin4_paper_configuration(orc):
+    """T=4k, k=512, b_q=32, b_k=2 -> initial groups of 8 blocks, final mask at iteration 3."""
+    cfg = json.load(open(GOLD))["paper_configuration"]
+    T = cfg["T"]
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, 128, "iid", seed=3, dtype=torch.float32, make_v=False)
+    last = T // cfg["b_q"] - 1
+    tr = orc.mask_trace(Q, K, cfg["k"], cfg["b_q"], cfg["b_k"], cfg["causal"], 0, 0, last)
+    sizes = tr["nodes"][0][:, 1] - tr["nodes"][0][:, 0] + 1
+    assert (sizes == cfg["initial_node_blocks"]).all()
+    assert tr["n_iter"] == cfg["last_query_block_iterations"]
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-1: k >= T  =>  HiP == dense (causal) attention (Eq. 1-3 with M = all ones)
+# --------------------------------------------------------------------------------------------
+def _sdpa64(Q, K, V, causal, scale):
+    Q, K, V = (torch.as_tensor(np.asarray(x, np.float32)).double() for x in (Q, K, V))
+    Tq, Tk = Q.shape[2], K.shape[2]
+    g = Q.shape[1] // K.shape[1]
+    K = K.repeat_interleave(g, dim=1)
+    V = V.repeat_interleave(g, dim=1)
+    mask = None
+    if causal:
+        mask = torch.ones(Tq, Tk, dtype=torch.bool).tril(diagonal=Tk - Tq)
+    return torch.nn.functional.scaled_dot_product_attention(Q, K, V, attn_mask=mask, scale=scale).numpy()
+
+
+@pytest.mark.parametrize("Tq,Tk,Hq,Hkv,causal", [(256, 256, 2, 2, True), (96, 300, 4, 2, True),
+                                                 (200, 200, 1, 1, False), (1, 333, 2, 1, True)])
+def test_pin1_exact_case_is_dense(orc, Tq, Tk, Hq, Hkv, causal):
+    d, k, bq, bk = 64, 512, 32, 2
+    Q, K, V = synth.gen_qkv(1, Hq, Hkv, Tq, Tk, d, "iid", seed=11, dtype=torch.float32)
+    idx, cnt = orc.mask(Q, K, k, bq, bk, causal)
+    nqb = idx.shape[2]
+    for q in range(nqb):
+        vis = _visible(q, bq, bk, Tq, Tk, causal)
+        assert (cnt[:, :, q] == vis).all()
+        assert (idx[:, :, q, :vis] == np.arange(vis)).all() and (idx[:, :, q, vis:] == -1).all()
+    O, lse = orc.sparse_attention(Q, K, V, k, bq, bk, causal, idx, cnt)
+    Od, lsed = orc.dense_attention(Q, K, V, causal)
+    assert np.array_equal(O, Od) and np.array_equal(lse, lsed)  # shared loop: bit-identical
+    ref = _sdpa64(Q, K, V, causal, 1.0 / math.sqrt(d))
+    assert np.abs(O - ref).max() < 1e-12
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-2: n < B_q <= 2n  =>  one iteration, every visible block is a candidate once => the mask is
+# the exact top-n of the block maxima (P:150-153 with the tile score of P:178-180).
+# --------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dist,mode", [("int", 0), ("int", 1), ("iid", 1)])
+def test_pin2_one_level_is_exact_topn(orc, dist, mode):
+    T, d, k, bq, bk = 1024, 32, 128, 16, 2  # n = 64; causal blocks with 64 < B_q <= 128: q in [8, 16)
+    Q, K, _ = synth.gen_qkv(1, 2, 1, T, T, d, dist, seed=5, dtype=torch.float32, make_v=False)
+    n = k // bk
+    idx, cnt = orc.mask(Q, K, k, bq, bk, True, mode=mode)
+    bs = _brute_block_scores(Q, K, bq, bk, True)
+    checked = 0
+    for h in range(2):
+        for q in range(idx.shape[2]):
+            vis = _visible(q, bq, bk, T, T, True)
+            if not (n < vis <= 2 * n):
+                continue
+            want = _topn_sorted(bs[0, h, q, :vis], n)
+            assert cnt[0, h, q] == n
+            assert np.array_equal(idx[0, h, q], want), (h, q)
+            checked += 1
+    assert checked == 16
+    # non-causal with N_kb in (n, 2n]
+    Tk = 200
+    Q2, K2, _ = synth.gen_qkv(1, 1, 1, 40, Tk, d, dist, seed=6, dtype=torch.float32, make_v=False)
+    idx2, _ = orc.mask(Q2, K2, k, bq, bk, False, mode=mode)
+    bs2 = _brute_block_scores(Q2, K2, bq, bk, False)
+    for q in range(idx2.shape[2]):
+        assert np.array_equal(idx2[0, 0, q], _topn_sorted(bs2[0, 0, q], n))
+
+
+def test_pin2_exact_topn_routine(orc):
+    """oracle_exact_block_topn (used for recall) against the brute-force sort at every query block."""
+    T, d, k, bq, bk = 512, 16, 64, 8, 4
+    Q, K, _ = synth.gen_qkv(1, 2, 2, T, T, d, "int", seed=9, dtype=torch.float32, make_v=False)
+    idx, cnt = orc.exact_block_topn(Q, K, k, bq, bk, True)
+    bs = _brute_block_scores(Q, K, bq, bk, True)
+    n = k // bk
+    for h in range(2):
+        for q in range(idx.shape[2]):
+            vis = _visible(q, bq, bk, T, T, True)
+            want = _topn_sorted(bs[0, h, q, :vis], n)
+            assert cnt[0, h, q] == len(want)
+            assert np.array_equal(idx[0, h, q, : len(want)], want)
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-3: strictly monotone block scores => greedy = exact top-n (last n / first n visible blocks)
+# --------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("T,k,bq,bk", [(2048, 128, 32, 2), (1000, 64, 8, 1), (3000, 96, 16, 4), (777, 40, 4, 8)])
+@pytest.mark.parametrize("sign", [1, -1])
+def test_pin3_monotone(orc, T, k, bq, bk, sign):
+    Q = np.zeros((1, 1, T, 4), np.float32)
+    Q[..., 0] = 1.0
+    K = np.zeros((1, 1, T, 4), np.float32)
+    K[0, 0, :, 0] = sign * (np.arange(T, dtype=np.float32) / np.float32(T))
+    n = k // bk
+    for causal in (True, False):
+        idx, cnt = orc.mask(Q, K, k, bq, bk, causal)
+        for q in range(idx.shape[2]):
+            vis = _visible(q, bq, bk, T, T, causal)
+            m = min(n, vis)
+            want = np.arange(vis - m, vis) if sign > 0 else np.arange(m)
+            assert cnt[0, 0, q] == m
+            assert np.array_equal(idx[0, 0, q, :m], want), (q, vis)
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-5: invariants: per iteration n disjoint non-empty nodes nested in the previous
+# ones and inside [0, B_q); final: min(n, B_q) distinct ascending blocks; leaf exactness.
+# --------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dist", ["iid", "int", "llm"])
+def test_pin5_invariants(orc, dist):
+    T, d, k, bq, bk = 3000, 32, 96, 16, 2
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, dist, seed=21, dtype=torch.float32, make_v=False)
+    n = k // bk
+    nqb = -(-T // bq)
+    for q in [0, 2, 3, 5, 6, 7, 50, 101, 150, nqb - 1]:
+        vis = _visible(q, bq, bk, T, T, True)
+        tr = orc.mask_trace(Q, K, k, bq, bk, True, 0, 0, q)
+        final = tr["idx"][: tr["cnt"]]
+        assert tr["cnt"] == min(n, vis)
+        assert np.all(np.diff(final) > 0) and final.min() >= 0 and final.max() < vis
+        if vis <= n:
+            assert tr["n_iter"] == 0
+            continue
+        assert tr["n_iter"] == math.ceil(math.log2(math.ceil(vis / n))) or tr["n_iter"] < math.ceil(
+            math.log2(math.ceil(vis / n))) + 1
+        prev = None
+        for it, nodes in enumerate(tr["nodes"]):
+            f, l = nodes[:, 0], nodes[:, 1]
+            assert len(nodes) == n and (f <= l).all() and f.min() >= 0 and l.max() < vis
+            o = np.argsort(f)
+            assert (f[o][1:] > l[o][:-1]).all()  # disjoint
+            if it == 0:
+                assert f[o][0] == 0 and l[o][-1] == vis - 1  # initial partition covers [0, B_q)
+                sz = l - f + 1
+                assert sz.max() - sz.min() <= 1          # "k equal-sized ranges"
+            else:
+                pf, pl = prev[:, 0], prev[:, 1]
+                for a, b in zip(f, l):                   # nesting
+                    assert ((pf <= a) & (b <= pl)).any()
+            prev = nodes
+        assert (tr["nodes"][-1][:, 0] == tr["nodes"][-1][:, 1]).all()  # leaves are single blocks
+        # leaf exactness: the kept scores of the last iteration are the exact tile maxima
+        last = tr["nodes"][-1]
+        tuples = [(0, 0, q, int(j)) for j in last[:, 0]]
+        sc, _ = orc.block_scores(Q, K, bq, bk, True, tuples, mode=orc.F32C)
+        assert np.array_equal(sc, tr["scores"][-1])
+
+
+def test_pin5_causal_budget(orc):
+    """Row t_last of an aligned query block keeps exactly min(k, visible) tokens."""
+    T, d, k, bq, bk = 2048, 16, 128, 32, 2
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=4, dtype=torch.float32, make_v=False)
+    idx, cnt = orc.mask(Q, K, k, bq, bk, True)
+    for q in range(idx.shape[2]):
+        tlast = (q + 1) * bq - 1
+        toks = [s for j in idx[0, 0, q, : cnt[0, 0, q]] for s in range(j * bk, (j + 1) * bk) if s <= tlast]
+        assert len(toks) == min(k, tlast + 1)
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-6: scale / permutation invariance
+# --------------------------------------------------------------------------------------------
+def test_pin6_power_of_two_scaling(orc):
+    T, d = 1500, 64
+    Q, K, _ = synth.gen_qkv(1, 2, 2, T, T, d, "llm", seed=8, dtype=torch.float32, make_v=False)
+    base = orc.mask(Q, K, 64, 16, 2, True)[0]
+    for j in (-3, 1, 5):
+        Qs = Q * (2.0 ** j)
+        for mode in (orc.F32C, orc.F64):
+            assert np.array_equal(orc.mask(Qs, K, 64, 16, 2, True, mode=mode)[0],
+                                  orc.mask(Q, K, 64, 16, 2, True, mode=mode)[0])
+    assert base.shape[-1] == 32
+
+
+def test_pin6_row_permutation_integer(orc):
+    T, d, bq = 1024, 32, 16
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "int", seed=12, dtype=torch.float32, make_v=False)
+    Qn = Q.numpy().copy()
+    rng = np.random.default_rng(0)
+    for q in range(T // bq):
+        rows = np.arange(q * bq, (q + 1) * bq)
+        Qn[0, 0, rows] = Qn[0, 0, rng.permutation(rows)]
+    a = orc.mask(Q, K, 64, bq, 2, False)[0]
+    b = orc.mask(Qn, K, 64, bq, 2, False)[0]
+    assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-7: complexity counter: distinct representative blocks scored per query block
+# = 2n + (n_it - 1) n when every node has the same power-of-two size, <= that bound otherwise.
+# --------------------------------------------------------------------------------------------
+def test_pin7_counter(orc):
+    T, d, k, bq, bk = 8192, 16, 64, 16, 2
+    n = k // bk
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=2, dtype=torch.float32, make_v=False)
+    _, _, dg = orc.mask(Q, K, k, bq, bk, True, diag=True)
+    exact = 0
+    for q in range(T // bq):
+        vis = _visible(q, bq, bk, T, T, True)
+        ns, nit = int(dg["n_scored"][0, 0, q]), int(dg["n_iter"][0, 0, q])
+        if vis <= n:
+            assert ns == 0 and nit == 0
+            continue
+        full_it = math.ceil(math.log2(math.ceil(vis / n)))
+        bound = 2 * n + (full_it - 1) * n
+        ratio = vis / n
+        if ratio == int(ratio) and (int(ratio) & (int(ratio) - 1)) == 0:
+            assert nit == full_it and ns == bound
+            exact += 1
+        else:
+            assert ns <= bound and nit <= full_it
+    assert exact >= 5
+
+
+# --------------------------------------------------------------------------------------------
+# PIN-8: attention special cases
+# --------------------------------------------------------------------------------------------
+def test_pin8_attention_special_cases(orc):
+    T, d, k, bq, bk = 64, 8, 16, 4, 2
+    Q, K, V = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=1, dtype=torch.float32)
+    nqb, n = T // bq, k // bk
+    # a single selected block whose first token is the only visible one for row 0 -> O = V[0]
+    idx = np.full((1, 1, nqb, n), -1, np.int32)
+    cnt = np.zeros((1, 1, nqb), np.int32)
+    idx[0, 0, 0, 0] = 0
+    cnt[0, 0, 0] = 1
+    O, lse = orc.sparse_attention(Q, K, V, k, bq, bk, True, idx, cnt)
+    assert np.array_equal(O[0, 0, 0], V[0, 0, 0].double().numpy())
+    assert np.isfinite(lse[0, 0, 0])
+    # empty rows -> zeros, -inf (G13)
+    assert (O[0, 0, bq:] == 0).all() and np.isneginf(lse[0, 0, bq:]).all()
+    # convexity: each output coordinate within [min, max] of the selected (visible) V rows
+    rng = np.random.default_rng(3)
+    for q in range(nqb):
+        c = rng.integers(1, n + 1)
+        sel = np.sort(rng.choice(nqb * bq // bk, size=c, replace=False))
+        idx[0, 0, q] = -1
+        idx[0, 0, q, :c] = sel
+        cnt[0, 0, q] = c
+    O, lse = orc.sparse_attention(Q, K, V, k, bq, bk, False, idx, cnt)
+    Vn = V[0, 0].double().numpy()
+    for t in range(T):
+        q = t // bq
+        toks = [s for j in idx[0, 0, q, : cnt[0, 0, q]] for s in range(j * bk, (j + 1) * bk)]
+        lo, hi = Vn[toks].min(0), Vn[toks].max(0)
+        assert (O[0, 0, t] >= lo - 1e-12).all() and (O[0, 0, t] <= hi + 1e-12).all()
+    # out-of-range index is an error
+    idx[0, 0, 0, 0] = 10_000
+    with pytest.raises(ValueError):
+        orc.sparse_attention(Q, K, V, k, bq, bk, False, idx, cnt)
+
+
+def test_pin8_dense_vs_sdpa_gqa(orc):
+    Q, K, V = synth.gen_qkv(2, 4, 2, 50, 70, 16, "llm", seed=7, dtype=torch.float32)
+    for causal in (True, False):
+        O, _ = orc.dense_attention(Q, K, V, causal, sm_scale=0.3)
+        ref = _sdpa64(Q, K, V, causal, 0.3)
+        assert np.abs(O - ref).max() < 1e-12
+
+
+# --------------------------------------------------------------------------------------------
+# Decode / paged: the paged routines see exactly the contiguous problem (reading G16)
+# --------------------------------------------------------------------------------------------
+def test_paged_equals_contiguous_and_bq_irrelevant(orc):
+    B, Hq, Hkv, d, ps = 3, 4, 2, 32, 8
+    seq = [700, 64, 1031]
+    Tmax = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=1, dtype=torch.float32)
+    _, K, V = synth.gen_qkv(B, Hkv, Hkv, 1, Tmax, d, "iid", seed=2, dtype=torch.float32)
+    kp, vp, bt, sl = synth.to_paged(K, V, seq, ps, seed=2)
+    k, bk = 128, 2
+    idx_p, cnt_p = orc.mask_paged(Q, kp, bt, sl, k, 32, bk, True)
+    idx_p1, _ = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True)
+    assert np.array_equal(idx_p, idx_p1)
+    O_p, lse_p = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, idx_p, cnt_p)
+    for b in range(B):
+        Tk = seq[b]
+        idx_c, cnt_c = orc.mask(Q[b:b + 1], K[b:b + 1, :, :Tk], k, 1, bk, True)
+        assert np.array_equal(idx_c, idx_p[b:b + 1]) and np.array_equal(cnt_c, cnt_p[b:b + 1])
+        O_c, lse_c = orc.sparse_attention(Q[b:b + 1], K[b:b + 1, :, :Tk], V[b:b + 1, :, :Tk], k, 1, bk, True,
+                                          idx_c, cnt_c)
+        assert np.array_equal(O_c, O_p[b:b + 1]) and np.array_equal(lse_c, lse_p[b:b + 1])
+
+
+def test_iteration_count_reading_g6(orc):
+    """Any number of extra iterations is a no-op (G5/G6): the loop stops when all nodes are single
+    blocks, and the mask of a query block whose nodes are already singletons never changes."""
+    T, d = 4096, 32
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=31, dtype=torch.float32, make_v=False)
+    _, _, dg = orc.mask(Q, K, 512, 32, 2, True, diag=True)
+    vis = np.array([_visible(q, 32, 2, T, T, True) for q in range(T // 32)])
+    need = np.array([0 if v <= 256 else math.ceil(math.log2(math.ceil(v / 256))) for v in vis])
+    assert (dg["n_iter"][0, 0] <= need).all()
+    assert (dg["n_iter"][0, 0][vis > 256] >= 1).all()
