@@ -1,0 +1,228 @@
+// common.cuh — device helpers shared by the HiP kernels (sm_100a only).
+//
+// PTX wrappers for cp.async (LDGSTS), mbarrier, tcgen05 (TMEM alloc / MMA / commit / ld) and the
+// UMMA shared-memory + instruction descriptors, plus the problem descriptors passed to kernels.
+// Nothing here is shared with the CPU oracle (oracle/), by design.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef __CUDACC__
+#error "CUDA only"
+#endif
+
+namespace hip {
+
+// ----------------------------------------------------------------------------------------------
+// Problem descriptors
+// ----------------------------------------------------------------------------------------------
+// Where key (or value) row s of (batch b, kv head hk) lives: contiguous [B,Hkv,T,d] or paged
+// [num_pages, Hkv, page_size, d] through a block table.  Strides are in elements.
+struct RowSrc {
+  const char* base;          // bytes
+  int64_t sb, sh, st;        // contiguous strides (elements); paged: sh, st used + sp
+  int64_t sp;                // paged: page stride (elements)
+  const int32_t* block_table;
+  int32_t page_size, max_pages;
+  int32_t paged;
+  int32_t esize;             // bytes per element
+};
+
+__device__ __forceinline__ const char* row_ptr(const RowSrc& r, int b, int hk, int64_t s) {
+  if (!r.paged) return r.base + (b * r.sb + hk * r.sh + s * r.st) * r.esize;
+  int64_t pi = s / r.page_size;
+  int64_t page = __ldg(r.block_table + (int64_t)b * r.max_pages + pi);
+  return r.base + (page * r.sp + hk * r.sh + (s - pi * r.page_size) * r.st) * r.esize;
+}
+
+struct QSrc {
+  const char* base;
+  int64_t sb, sh, st;
+  int32_t esize;
+};
+
+__device__ __forceinline__ const char* q_ptr(const QSrc& q, int b, int h, int64_t t) {
+  return q.base + (b * q.sb + h * q.sh + t * q.st) * q.esize;
+}
+
+// Shape of one launch.  Tk is uniform unless seq_lens != nullptr (paged decode).
+struct Shape {
+  int B, Hq, Hkv, Tq, Tk, d;
+  int n, bq, bk, causal;
+  int nqb;
+  const int32_t* seq_lens;
+};
+
+__device__ __forceinline__ int seq_len(const Shape& sh, int b) {
+  return sh.seq_lens ? __ldg(sh.seq_lens + b) : sh.Tk;
+}
+
+// Unit u -> (b, h, q): head-major (all query blocks of one head adjacent, so K of that head stays
+// in L2 while they run); within a head the heavier (later) query blocks first.
+__device__ __forceinline__ void unit_coords(const Shape& sh, int64_t u, int& b, int& h, int& q) {
+  int64_t bh = u / sh.nqb;
+  q = sh.nqb - 1 - (int)(u - bh * sh.nqb);
+  b = (int)(bh / sh.Hq);
+  h = (int)(bh - (int64_t)b * sh.Hq);
+}
+
+// Visible key blocks of query block q (a1; reading G7): all blocks if not causal, else the blocks
+// that start at or before the key position of the block's last row.
+__device__ __forceinline__ int visible_blocks(const Shape& sh, int q, int Tk) {
+  int nkb = (Tk + sh.bk - 1) / sh.bk;
+  if (!sh.causal) return nkb;
+  int64_t tlast = min((int64_t)(q + 1) * sh.bq, (int64_t)sh.Tq) - 1;
+  int64_t v = (tlast + (Tk - sh.Tq)) / sh.bk + 1;
+  return (int)min(v, (int64_t)nkb);
+}
+
+// ----------------------------------------------------------------------------------------------
+// Small utilities
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Key order of the branch ranking (reading G10): larger score first, equal scores ->
+// smaller first block.  Comparison is on float values, so +0 == -0.
+__device__ __forceinline__ bool key_greater(float sa, int fa, float sb, int fb) {
+  return sa > sb || (sa == sb && fa < fb);
+}
+
+// ----------------------------------------------------------------------------------------------
+// cp.async (LDGSTS): 16-byte global -> shared copy; src_bytes < 16 zero-fills the remainder.
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// Make generic-proxy shared-memory writes (cp.async / st.shared) visible to the async proxy
+// (tcgen05.mma operand reads).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// ----------------------------------------------------------------------------------------------
+// mbarrier
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
+// ----------------------------------------------------------------------------------------------
+// tcgen05: TMEM allocation, MMA, commit, loads
+// ----------------------------------------------------------------------------------------------
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // the same warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(kCols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem], kind::f16 (bf16 inputs, fp32 accumulate), issued by ONE thread.
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive on an mbarrier once all previously issued tcgen05.mma of this thread have completed
+// (implies tcgen05.fence::before_thread_sync).
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns: thread i of the warp gets lane (base + i), columns
+// [col, col + 32).  The warp must be the one allowed to access that lane quadrant (warp % 4).
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ----------------------------------------------------------------------------------------------
+// UMMA descriptors (sm_100 tcgen05)
+// ----------------------------------------------------------------------------------------------
+// Shared-memory matrix descriptor: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 at
+// [46,48), base offset 0, layout type at [61,64) (0 none/interleave, 2 = 128B swizzle,
+// 4 = 64B swizzle, 6 = 32B swizzle).
+enum : uint32_t { kLayoutNone = 0, kLayoutSw128 = 2, kLayoutSw64 = 4, kLayoutSw32 = 6 };
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7) << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A bf16 (7-9 = 1), B bf16 (10-12 = 1),
+// A major (15), B major (16) (0 = K-major, 1 = MN-major), N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn_major, uint32_t b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn_major << 15) | (b_mn_major << 16) | ((N >> 3) << 17) |
+         ((M >> 4) << 24);
+}
+
+// Byte offset of 16-byte chunk `c` (0..7) of row `r` inside a K-major / MN-major 128-byte-swizzled
+// region whose rows are 128 bytes (8-row atoms of 1024 bytes; chunk XOR (row % 8)).
+__device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t c) {
+  return (r >> 3) * 1024u + (r & 7u) * 128u + ((c ^ (r & 7u)) << 4);
+}
+
+}  // namespace hip

@@ -1,0 +1,180 @@
+// mask_cc.cu — HiP mask estimation with CUDA-core scoring (Alg. 1; block approximation
+// P:172-186).  Every dot product is the canonical sequential chain acc = fmaf(q[c], k[c], acc),
+// c = 0..d-1, in fp32 (reading G9), so the selected blocks are bit-identical to the oracle's F32C
+// mode on any input.  Used for fp32 inputs (BASELINE config C1), for bf16 with
+// HIP_FLAG_EXACT_SCORES, for shapes the tcgen05 kernel does not cover, and for decode (T_q rows
+// against a paged KV cache), where scoring is a GEMV and the kernel is HBM-bound.
+//
+// One CTA (256 threads) per (b, h, query block) at a time, persistent over units.  Per iteration the
+// representative key blocks are gathered with coalesced 16-byte cp.async into a padded shared
+// stage (double-buffered chunks), each thread computes whole dot products for (query row, key row)
+// pairs, and one thread per block takes the tile max over the valid (causal) pairs.
+#include "kernels.h"
+#include "select.cuh"
+
+namespace hip {
+
+constexpr int kCCThreads = 256;
+
+template <typename T>
+struct CCScorer {
+  const float* qs;   // [rows_q][qpitch] fp32
+  int qpitch;        // floats
+  char* stage[2];    // staged key rows
+  int kpitch;        // bytes
+  float* pairs;      // [rows_per_chunk][rows_q]
+  RowSrc ks;
+  int b, hk, Tk, d, bk, causal, rows_q, ch;  // ch = key blocks per chunk
+  int64_t tpos0;     // key position of query row 0 of the block: q*bq + Tk - Tq
+
+  __device__ void issue(const int* rep, int n_rep, int c) {
+    const int blk0 = c * ch, nblk = min(ch, n_rep - blk0);
+    const int rows = nblk * bk, pieces = (d * (int)sizeof(T)) / 16;
+    const uint32_t dst0 = smem_u32(stage[c & 1]);
+    for (int p = threadIdx.x; p < rows * pieces; p += kCCThreads) {
+      int r = p / pieces, c16 = p - r * pieces;
+      int64_t s = (int64_t)rep[blk0 + r / bk] * bk + (r % bk);
+      bool ok = s < Tk;
+      const char* src = row_ptr(ks, b, hk, ok ? s : 0) + c16 * 16;
+      cp_async16(dst0 + r * kpitch + c16 * 16, src, ok ? 16u : 0u);
+    }
+  }
+
+  __device__ void score(const int* rep, int n_rep, float* out) {
+    const int nch = (n_rep + ch - 1) / ch;
+    issue(rep, n_rep, 0);
+    cp_async_commit();
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) issue(rep, n_rep, c + 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const int blk0 = c * ch, nblk = min(ch, n_rep - blk0), rows = nblk * bk;
+      const char* kst = stage[c & 1];
+      for (int p = threadIdx.x; p < rows * rows_q; p += kCCThreads) {
+        int t = p % rows_q, r = p / rows_q;
+        int64_t s = (int64_t)rep[blk0 + r / bk] * bk + (r % bk);
+        bool valid = s < Tk && (!causal || s <= tpos0 + t);
+        float acc = -INFINITY;
+        if (valid) {
+          const float4* qr = reinterpret_cast<const float4*>(qs + t * qpitch);
+          acc = 0.f;
+          if constexpr (sizeof(T) == 4) {
+            const float4* kr = reinterpret_cast<const float4*>(kst + r * kpitch);
+            for (int i = 0; i < d / 4; ++i) {
+              float4 kv = kr[i], qv = qr[i];
+              acc = __fmaf_rn(qv.x, kv.x, acc);
+              acc = __fmaf_rn(qv.y, kv.y, acc);
+              acc = __fmaf_rn(qv.z, kv.z, acc);
+              acc = __fmaf_rn(qv.w, kv.w, acc);
+            }
+          } else {
+            const uint4* kr = reinterpret_cast<const uint4*>(kst + r * kpitch);
+            for (int i = 0; i < d / 8; ++i) {
+              uint4 kv = kr[i];
+              float4 qa = qr[2 * i], qb = qr[2 * i + 1];
+              acc = __fmaf_rn(qa.x, bf16_lo(kv.x), acc);
+              acc = __fmaf_rn(qa.y, bf16_hi(kv.x), acc);
+              acc = __fmaf_rn(qa.z, bf16_lo(kv.y), acc);
+              acc = __fmaf_rn(qa.w, bf16_hi(kv.y), acc);
+              acc = __fmaf_rn(qb.x, bf16_lo(kv.z), acc);
+              acc = __fmaf_rn(qb.y, bf16_hi(kv.z), acc);
+              acc = __fmaf_rn(qb.z, bf16_lo(kv.w), acc);
+              acc = __fmaf_rn(qb.w, bf16_hi(kv.w), acc);
+            }
+          }
+        }
+        pairs[r * rows_q + t] = acc;
+      }
+      __syncthreads();
+      for (int lb = threadIdx.x; lb < nblk; lb += kCCThreads) {
+        float best = -INFINITY;
+        for (int r = lb * bk; r < lb * bk + bk; ++r)
+          for (int t = 0; t < rows_q; ++t) {
+            float v = pairs[r * rows_q + t];
+            if (v > best) best = v;
+          }
+        out[blk0 + lb] = best;
+      }
+      __syncthreads();  // stage[c & 1] and pairs are reused by chunk c + 2 / c + 1
+    }
+  }
+};
+
+template <typename T, int NMAX>
+__global__ void __launch_bounds__(kCCThreads) mask_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
+                                                             int32_t* __restrict__ cnt, int ch, int kpitch) {
+  extern __shared__ __align__(16) char smem[];
+  SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
+  const int rows_max = min(sh.bq, sh.Tq);
+  const int qpitch = sh.d + 4;
+  float* qs = reinterpret_cast<float*>(smem + sizeof(SelState<NMAX>));
+  char* stage0 = reinterpret_cast<char*>(qs + rows_max * qpitch);
+  char* stage1 = stage0 + ch * sh.bk * kpitch;
+  float* pairs = reinterpret_cast<float*>(stage1 + ch * sh.bk * kpitch);
+
+  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    int b, h, q;
+    unit_coords(sh, u, b, h, q);
+    const int hk = h / (sh.Hq / sh.Hkv);
+    const int Tk = seq_len(sh, b);
+    const int Bq = visible_blocks(sh, q, Tk);
+    const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
+    const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    if (Bq > sh.n) {
+      for (int i = threadIdx.x; i < rows_q * sh.d; i += kCCThreads) {
+        int t = i / sh.d, c = i - t * sh.d;
+        const T* src = reinterpret_cast<const T*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + t));
+        float v;
+        if constexpr (sizeof(T) == 4) v = src[c];
+        else v = __bfloat162float(src[c]);
+        qs[t * qpitch + c] = v;
+      }
+      __syncthreads();
+    }
+    CCScorer<T> sc;
+    sc.qs = qs; sc.qpitch = qpitch; sc.stage[0] = stage0; sc.stage[1] = stage1; sc.kpitch = kpitch;
+    sc.pairs = pairs; sc.ks = ks; sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.d = sh.d; sc.bk = sh.bk;
+    sc.causal = sh.causal; sc.rows_q = rows_q; sc.ch = ch;
+    sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+    tree_search<NMAX, kCCThreads>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
+    __syncthreads();
+  }
+}
+
+// Host launcher.  Returns a cudaError_t.
+template <typename T, int NMAX>
+static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
+                             cudaStream_t stream, int num_sms) {
+  const int esize = sizeof(T);
+  const int kpitch = sh.d * esize + 16;
+  const int stage_bytes = 16 * 1024;
+  int ch = max(1, stage_bytes / (sh.bk * kpitch));
+  const int rows_max = min(sh.bq, sh.Tq);
+  size_t smem = sizeof(SelState<NMAX>) + (size_t)rows_max * (sh.d + 4) * 4 + 2 * (size_t)ch * sh.bk * kpitch +
+                (size_t)ch * sh.bk * rows_max * 4;
+  smem = (smem + 15) & ~(size_t)15;
+  auto kern = mask_cc_kernel<T, NMAX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCCThreads, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, kCCThreads, smem, stream>>>(sh, qs, ks, idx, cnt, ch, kpitch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, bool bf16, int32_t* idx, int32_t* cnt,
+                           cudaStream_t stream, int num_sms) {
+  if (bf16) {
+    if (sh.n <= 256) return launch_cc<__nv_bfloat16, 256>(sh, qs, ks, idx, cnt, stream, num_sms);
+    return launch_cc<__nv_bfloat16, 1024>(sh, qs, ks, idx, cnt, stream, num_sms);
+  }
+  if (sh.n <= 256) return launch_cc<float, 256>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return launch_cc<float, 1024>(sh, qs, ks, idx, cnt, stream, num_sms);
+}
+
+}  // namespace hip

@@ -1,0 +1,229 @@
+"""Thin Python binding of the C ABI in include/hip_attn.h (libhipattn.so, sm_100a).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels behind the ABI.
+PyTorch supplies device memory and the current stream.  There is no CPU fallback: if the library
+is missing or the device is not an sm_100 B200, calls raise.
+
+Names follow the paper (arXiv 2406.09827): k = token budget per query block, b_q / b_k = query /
+key block sizes, n = k / b_k selected key blocks per query block (reading G1).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhipattn.so")
+
+HIP_SUCCESS, HIP_ERROR_INVALID_VALUE, HIP_ERROR_NOT_SUPPORTED, HIP_ERROR_WORKSPACE, HIP_ERROR_CUDA = range(5)
+HIP_DTYPE_F32, HIP_DTYPE_BF16 = 0, 1
+HIP_FLAG_EXACT_SCORES = 1
+HIP_OP_MASK, HIP_OP_PREFILL, HIP_OP_DECODE = 0, 1, 2
+
+EXPORTS = ("hip_version", "hip_last_error", "hip_num_blocks", "hip_workspace_bytes", "hip_mask_estimate",
+           "hip_sparse_attention_prefill", "hip_sparse_attention_decode")
+
+
+class HipError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[hip status {status}] {msg}")
+        self.status = status
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("b_q", ctypes.c_int32), ("b_k", ctypes.c_int32), ("causal", ctypes.c_int32),
+                ("sm_scale", ctypes.c_float), ("flags", ctypes.c_uint32)]
+
+
+class TensorDesc(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("stride_b", ctypes.c_int64), ("stride_h", ctypes.c_int64),
+                ("stride_t", ctypes.c_int64)]
+
+
+class PagedKV(ctypes.Structure):
+    _fields_ = [("k_pages", ctypes.c_void_p), ("v_pages", ctypes.c_void_p), ("stride_page", ctypes.c_int64),
+                ("stride_h", ctypes.c_int64), ("stride_t", ctypes.c_int64), ("block_table", ctypes.c_void_p),
+                ("seq_lens", ctypes.c_void_p), ("page_size", ctypes.c_int32), ("max_pages_per_seq", ctypes.c_int32),
+                ("num_pages", ctypes.c_int32), ("max_seq_len", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libhipattn.so (ctypes).  Raises if it has not been built: there is no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+    lib.hip_version.restype = i32
+    lib.hip_last_error.restype = ctypes.c_char_p
+    lib.hip_num_blocks.restype = i32
+    lib.hip_num_blocks.argtypes = [ctypes.POINTER(Params)]
+    lib.hip_workspace_bytes.restype = sz
+    lib.hip_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int] + [i32] * 6 + [ctypes.POINTER(Params)]
+    lib.hip_mask_estimate.restype = ctypes.c_int
+    lib.hip_mask_estimate.argtypes = ([ctypes.c_int] + [i32] * 6 + [TensorDesc, TensorDesc, ctypes.POINTER(PagedKV),
+                                      ctypes.POINTER(Params), P, P, P, sz, P])
+    lib.hip_sparse_attention_prefill.restype = ctypes.c_int
+    lib.hip_sparse_attention_prefill.argtypes = ([ctypes.c_int] + [i32] * 6 + [TensorDesc] * 3 +
+                                                 [ctypes.POINTER(Params), P, P, TensorDesc, P, P])
+    lib.hip_sparse_attention_decode.restype = ctypes.c_int
+    lib.hip_sparse_attention_decode.argtypes = ([ctypes.c_int] + [i32] * 5 + [TensorDesc, ctypes.POINTER(PagedKV),
+                                                ctypes.POINTER(Params), P, P, TensorDesc, P, P, sz, P])
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != HIP_SUCCESS:
+        raise HipError(status, load().hip_last_error().decode())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return HIP_DTYPE_BF16
+    if t.dtype == torch.float32:
+        return HIP_DTYPE_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _desc(t: torch.Tensor) -> TensorDesc:
+    if t.dim() != 4:
+        raise ValueError("expected a [B, H, T, d] tensor")
+    if t.stride(3) != 1:
+        raise ValueError("the head dimension must be contiguous (stride 1)")
+    return TensorDesc(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+
+
+def _stream(t: torch.Tensor, stream=None) -> int:
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False) -> Params:
+    return Params(int(k), int(b_q), int(b_k), int(bool(causal)), float(sm_scale or 0.0),
+                  HIP_FLAG_EXACT_SCORES if exact else 0)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("all tensors must be CUDA tensors (no CPU path)")
+
+
+def num_blocks(k: int, b_k: int) -> int:
+    p = _params(k, 1, b_k, False)
+    return int(load().hip_num_blocks(ctypes.byref(p)))
+
+
+def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
+                  causal: bool = True, exact: bool = False, out=None, stream=None):
+    """hip_mask_estimate on contiguous keys.  q [B,Hq,Tq,d], k [B,Hkv,Tk,d] -> (idx, cnt)."""
+    _require_cuda(q, k)
+    lib = load()
+    B, Hq, Tq, d = q.shape
+    _, Hkv, Tk, _ = k.shape
+    p = _params(k_budget, b_q, b_k, causal, exact=exact)
+    n = int(lib.hip_num_blocks(ctypes.byref(p)))
+    bq = max(1, min(int(b_q), Tq))
+    nqb = (Tq + bq - 1) // bq
+    if out is None:
+        idx = torch.empty((B, Hq, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
+        cnt = torch.empty((B, Hq, nqb), dtype=torch.int32, device=q.device)
+    else:
+        idx, cnt = out
+    with torch.cuda.device(q.device):
+        _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, Tk, d, _desc(q), _desc(k), None,
+                                     ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), None, 0, _stream(q, stream)))
+    return idx, cnt
+
+
+def _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len: int) -> PagedKV:
+    if k_pages.dim() != 4 or k_pages.stride(3) != 1:
+        raise ValueError("pages must be [num_pages, Hkv, page_size, d] with d contiguous")
+    if v_pages is not None and v_pages.stride() != k_pages.stride():
+        raise ValueError("k_pages and v_pages must share strides")
+    if block_table.dtype != torch.int32 or seq_lens.dtype != torch.int32:
+        raise TypeError("block_table and seq_lens must be int32")
+    bt = block_table.contiguous()
+    return PagedKV(k_pages.data_ptr(), v_pages.data_ptr() if v_pages is not None else None, k_pages.stride(0),
+                   k_pages.stride(1), k_pages.stride(2), bt.data_ptr(), seq_lens.data_ptr(), k_pages.shape[2],
+                   bt.shape[1], k_pages.shape[0], int(max_seq_len)), bt
+
+
+def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, k_budget: int = 512, b_q: int = 32,
+                        b_k: int = 2, causal: bool = True, exact: bool = False, out=None, stream=None):
+    """hip_mask_estimate on a paged cache (decode: q [B,Hq,Tq,d], Tq rows at positions seq_len-Tq+t)."""
+    _require_cuda(q, k_pages, block_table, seq_lens)
+    lib = load()
+    B, Hq, Tq, d = q.shape
+    Hkv = k_pages.shape[1]
+    p = _params(k_budget, b_q, b_k, causal, exact=exact)
+    n = int(lib.hip_num_blocks(ctypes.byref(p)))
+    bq = max(1, min(int(b_q), Tq))
+    nqb = (Tq + bq - 1) // bq
+    pg, bt = _paged(k_pages, None, block_table, seq_lens, max_seq_len)
+    if out is None:
+        idx = torch.empty((B, Hq, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
+        cnt = torch.empty((B, Hq, nqb), dtype=torch.int32, device=q.device)
+    else:
+        idx, cnt = out
+    with torch.cuda.device(q.device):
+        _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, int(max_seq_len), d, _desc(q),
+                                     TensorDesc(None, 0, 0, 0), ctypes.byref(pg), ctypes.byref(p), idx.data_ptr(),
+                                     cnt.data_ptr(), None, 0, _stream(q, stream)))
+    del bt
+    return idx, cnt
+
+
+def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
+                             causal: bool = True, sm_scale=None, out=None, return_lse: bool = False, stream=None):
+    """hip_sparse_attention_prefill.  Returns o (and lse fp32 [B,Hq,Tq] if return_lse)."""
+    _require_cuda(q, k, v, idx, cnt)
+    lib = load()
+    B, Hq, Tq, d = q.shape
+    _, Hkv, Tk, _ = k.shape
+    p = _params(k_budget, b_q, b_k, causal, sm_scale)
+    o = torch.empty_like(q) if out is None else out
+    lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
+    with torch.cuda.device(q.device):
+        _check(lib.hip_sparse_attention_prefill(_dtype_code(q), B, Hq, Hkv, Tq, Tk, d, _desc(q), _desc(k), _desc(v),
+                                                ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), _desc(o),
+                                                lse.data_ptr() if lse is not None else None, _stream(q, stream)))
+    return (o, lse) if return_lse else o
+
+
+def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, idx, cnt, *,
+                            k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True, sm_scale=None,
+                            out=None, return_lse: bool = False, stream=None):
+    """hip_sparse_attention_decode on a paged cache.  q [B,Hq,Tq,d] -> o (and lse)."""
+    _require_cuda(q, k_pages, v_pages, block_table, seq_lens, idx, cnt)
+    lib = load()
+    B, Hq, Tq, d = q.shape
+    Hkv = k_pages.shape[1]
+    p = _params(k_budget, b_q, b_k, causal, sm_scale)
+    pg, bt = _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len)
+    o = torch.empty_like(q) if out is None else out
+    lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
+    with torch.cuda.device(q.device):
+        _check(lib.hip_sparse_attention_decode(_dtype_code(q), B, Hq, Hkv, Tq, d, _desc(q), ctypes.byref(pg),
+                                               ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), _desc(o),
+                                               lse.data_ptr() if lse is not None else None, None, 0,
+                                               _stream(q, stream)))
+    del bt
+    return (o, lse) if return_lse else o
+
+
+def hip_attention(q, k, v, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True,
+                  sm_scale=None, out=None, stream=None):
+    """One HiP attention layer (prefill): mask estimation then block-sparse attention."""
+    idx, cnt = mask_estimate(q, k, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal, stream=stream)
+    return sparse_attention_prefill(q, k, v, idx, cnt, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal,
+                                    sm_scale=sm_scale, out=out, stream=stream)

@@ -1,0 +1,295 @@
+"""GPU (sm_100a) vs CPU oracle parity, through the C ABI (paper_2406_09827_b200.hipattn).
+
+Bars (BASELINE.json north_star):
+  * mask indices: bit-exact wherever both sides take the selection decisions in the same fp32
+    arithmetic — the fp32 / HIP_FLAG_EXACT_SCORES / decode kernels (sequential fmaf = oracle F32C)
+    on every input, and the tcgen05 kernel on integer-valued inputs (every sum exact).  For the
+    tcgen05 kernel on Gaussian inputs the mismatching query blocks are reported as a fraction and
+    every one must be certified as a near-tie by the oracle's fp64 selection margins.
+  * attention outputs: max-abs <= 1e-4 (fp32) / 2e-2 (bf16) against the fp64 oracle on the same
+    selection (seeded synthetic selections from synth.py, or the oracle's own mask).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2406_09827_b200 import hipattn as H
+from paper_2406_09827_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+# rigorous bound for any fp32 evaluation order of a d-term dot product (tensor-core accumulation
+# included): |err| <= TAU * sum_c |q_c k_c|, TAU = d * 2^-22 (4x the round-to-nearest bound d*u)
+TAU_UNIT = 2.0 ** -22
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    H.load()
+    torch.cuda.init()
+
+
+def _visible(q, bq, bk, Tq, Tk, causal):
+    nkb = -(-Tk // bk)
+    if not causal:
+        return nkb
+    tlast = min((q + 1) * bq, Tq) - 1
+    return min((tlast + Tk - Tq) // bk + 1, nkb)
+
+
+def _gpu_mask(Q, K, k, bq, bk, causal, exact=False):
+    idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, causal=causal, exact=exact)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), cnt.cpu().numpy()
+
+
+def _assert_mask_equal(gi, gc, oi, oc):
+    assert np.array_equal(gc, oc), f"cnt mismatch at {np.argwhere(gc != oc)[:5]}"
+    bad = np.argwhere((gi != oi).any(-1))
+    assert len(bad) == 0, f"{len(bad)} query blocks differ, first {bad[:5].tolist()}"
+
+
+# ------------------------------------------------------------------------------------------------
+# Mask: bit-exact tiers
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dist", ["iid", "int", "llm"])
+def test_mask_fp32_c1_bitexact(orc, dist):
+    """BASELINE config C1: single head, T=4096, d=128, k=512, b_q=32, b_k=2, fp32 causal."""
+    Q, K, _ = synth.gen_qkv(1, 1, 1, 4096, 4096, 128, dist, seed=0, dtype=torch.float32, make_v=False)
+    gi, gc = _gpu_mask(Q, K, 512, 32, 2, True)
+    oi, oc = orc.mask(Q, K, 512, 32, 2, True, mode=orc.F32C)
+    _assert_mask_equal(gi, gc, oi, oc)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,Tq,Tk,d,k,bq,bk,causal,dist", [
+    (1, 4, 2, 3000, 3000, 128, 256, 32, 2, True, "iid"),     # ragged tails, GQA
+    (2, 2, 1, 700, 2100, 64, 128, 16, 4, True, "llm"),       # T_q < T_k, d=64
+    (1, 2, 2, 1000, 1500, 128, 64, 32, 1, False, "iid"),     # non-causal, b_k=1
+    (1, 1, 1, 50, 4000, 128, 512, 64, 8, True, "llm"),       # b_q=64 > 32 (CUDA-core path)
+    (1, 1, 1, 5, 3, 128, 2, 64, 8, False, "iid"),            # b_q > T_q and b_k > T_k
+    (1, 1, 1, 300, 300, 128, 2, 32, 2, True, "iid"),         # n = 1
+])
+def test_mask_exact_scores_bitexact(orc, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal, dist):
+    for dt in (torch.bfloat16, torch.float32):
+        Q, K, _ = synth.gen_qkv(B, Hq, Hkv, Tq, Tk, d, dist, seed=1, dtype=dt, make_v=False)
+        gi, gc = _gpu_mask(Q, K, k, bq, bk, causal, exact=True)
+        oi, oc = orc.mask(Q, K, k, min(bq, Tq), bk, causal, mode=orc.F32C)
+        _assert_mask_equal(gi, gc, oi, oc)
+
+
+@pytest.mark.parametrize("Tq,Tk,Hq,Hkv,bk,k,causal", [
+    (4096, 4096, 2, 1, 2, 512, True),
+    (3001, 3333, 4, 2, 2, 256, True),
+    (2048, 2048, 1, 1, 4, 512, False),
+    (1024, 5000, 2, 2, 1, 128, True),
+    (96, 96, 1, 1, 32, 64, True),
+])
+def test_mask_tcgen05_integer_bitexact(orc, Tq, Tk, Hq, Hkv, bk, k, causal):
+    """Integer-valued bf16 inputs: every fp32 partial sum is exact, so the tensor-core scores equal
+    the oracle's exactly and the masks must match bit-for-bit, ties and tie-breaks included."""
+    Q, K, _ = synth.gen_qkv(1, Hq, Hkv, Tq, Tk, 128, "int", seed=2, dtype=torch.bfloat16, make_v=False)
+    gi, gc = _gpu_mask(Q, K, k, 32, bk, causal)
+    oi, oc = orc.mask(Q, K, k, 32, bk, causal, mode=orc.F32C)
+    _assert_mask_equal(gi, gc, oi, oc)
+
+
+def _certify(orc, Q, K, k, bq, bk, causal, gi, gc):
+    """Mismatch fraction of the tcgen05 mask vs the F64 oracle, and whether every mismatching query
+    block is a certified near-tie: some selection gap of the exact (fp64) run <= 2 * eps where
+    eps = TAU * max over scored pairs of sum |q_c k_c| bounds every fp32 score error."""
+    oi, oc, dg = orc.mask(Q, K, k, bq, bk, causal, mode=orc.F64, diag=True)
+    assert np.array_equal(gc, oc)
+    d = Q.shape[-1]
+    bad = (gi != oi).any(-1)
+    eps = TAU_UNIT * d * dg["emax"]
+    explained = dg["margin_min"] <= 2 * eps
+    return bad.mean(), int(bad.sum()), int((bad & ~explained).sum())
+
+
+@pytest.mark.parametrize("dist", ["iid", "llm"])
+def test_mask_tcgen05_gaussian_certified(orc, dist):
+    Q, K, _ = synth.gen_qkv(1, 4, 2, 4096, 4096, 128, dist, seed=3, dtype=torch.bfloat16, make_v=False)
+    gi, gc = _gpu_mask(Q, K, 512, 32, 2, True)
+    frac, nbad, unexplained = _certify(orc, Q, K, 512, 32, 2, True, gi, gc)
+    print(f"\n[parity] tcgen05 mask vs F64 oracle ({dist}): {nbad} of {gi.shape[1] * gi.shape[2]} query blocks "
+          f"differ ({100 * frac:.2f}%), unexplained {unexplained}")
+    assert unexplained == 0
+    assert frac <= 0.10
+
+
+# ------------------------------------------------------------------------------------------------
+# Attention on seeded synthetic selections (no mask involved)
+# ------------------------------------------------------------------------------------------------
+def _synthetic_selection(B, Hq, Tq, Tk, k, bq, bk, causal, seed):
+    nqb = -(-Tq // bq)
+    hi = torch.tensor([[[_visible(q, bq, bk, Tq, Tk, causal) for q in range(nqb)]] * Hq] * B)
+    return synth.gen_block_indices(B, Hq, nqb, k // bk, hi, seed=seed)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("B,Hq,Hkv,Tq,Tk,d,k,bq,bk,causal", [
+    (1, 2, 1, 1000, 1000, 128, 512, 32, 2, True),
+    (2, 4, 2, 333, 900, 128, 256, 32, 4, True),
+    (1, 2, 2, 257, 257, 64, 128, 16, 2, False),
+    (1, 1, 1, 100, 100, 128, 64, 64, 8, True),
+    (1, 2, 1, 130, 4000, 128, 512, 32, 1, True),
+])
+def test_attention_prefill_parity(orc, dt, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal):
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, Tq, Tk, d, "llm", seed=4, dtype=dt)
+    idx, cnt = _synthetic_selection(B, Hq, Tq, Tk, k, bq, bk, causal, seed=4)
+    o, lse = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx.cuda(), cnt.cuda(), k_budget=k, b_q=bq,
+                                        b_k=bk, causal=causal, return_lse=True)
+    torch.cuda.synchronize()
+    Oo, lo = orc.sparse_attention(Q, K, V, k, bq, bk, causal, idx, cnt)
+    err = np.abs(o.float().cpu().numpy() - Oo).max()
+    assert err <= TOL[dt], err
+    lg = lse.cpu().numpy()
+    fin = np.isfinite(lo)
+    assert np.array_equal(np.isfinite(lg), fin)
+    assert np.abs(lg[fin] - lo[fin]).max() <= 1e-3
+
+
+def test_attention_empty_rows(orc):
+    """k = b_k: one block per query block; rows before the block's first token see nothing:
+    O = 0, lse = -inf (G13)."""
+    for dt in (torch.bfloat16, torch.float32):
+        Q, K, V = synth.gen_qkv(1, 1, 1, 256, 256, 128, "iid", seed=5, dtype=dt)
+        idx, cnt = orc.mask(Q, K, 2, 32, 2, True)
+        o, lse = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), torch.from_numpy(idx).cuda(),
+                                            torch.from_numpy(cnt).cuda(), k_budget=2, b_q=32, b_k=2, causal=True,
+                                            return_lse=True)
+        Oo, lo = orc.sparse_attention(Q, K, V, 2, 32, 2, True, idx, cnt)
+        assert np.isneginf(lo).any()
+        lg = lse.cpu().numpy()
+        assert np.array_equal(np.isneginf(lg), np.isneginf(lo))
+        assert (o.float().cpu().numpy()[np.isneginf(lo)] == 0).all()
+        assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+
+
+def test_exact_case_equals_dense(orc):
+    """PIN-1 on the GPU: k >= T -> HiP attention == dense causal attention."""
+    for dt in (torch.bfloat16, torch.float32):
+        Q, K, V = synth.gen_qkv(1, 2, 1, 384, 384, 128, "llm", seed=6, dtype=dt)
+        o = H.hip_attention(Q.cuda(), K.cuda(), V.cuda(), k_budget=512, b_q=32, b_k=2, causal=True)
+        Od, _ = orc.dense_attention(Q, K, V, True)
+        assert np.abs(o.float().cpu().numpy() - Od).max() <= TOL[dt]
+
+
+# ------------------------------------------------------------------------------------------------
+# Decode on a paged KV cache
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dt,dist", [(torch.bfloat16, "iid"), (torch.bfloat16, "int"), (torch.float32, "iid")])
+@pytest.mark.parametrize("ps", [16, 64])
+def test_decode_paged_parity(orc, dt, dist, ps):
+    B, Hq, Hkv, d, k, bk = 4, 8, 2, 128, 512, 2
+    seq = [5000, 1, 777, 4096]
+    Q = synth.gen_decode_q(B, Hq, d, seed=7, dtype=dt, dist=dist)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=7, dtype=dt, dist=dist)
+    T = max(seq)
+    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk,
+                                     causal=True)
+    o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T, idx, cnt, k_budget=k,
+                                       b_q=1, b_k=bk, causal=True, return_lse=True)
+    torch.cuda.synchronize()
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F32C)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    Oo, lo = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, oi, oc)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+    assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
+
+
+def test_paged_equals_contiguous_and_page_permutation():
+    """PIN-9: the paged path sees exactly the contiguous problem (bit-identical), for any page order."""
+    B, Hq, Hkv, d, k, bk = 2, 4, 2, 128, 256, 2
+    seq = [3000, 2048]
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=8).cuda()
+    _, Kc, Vc = synth.gen_qkv(B, Hkv, Hkv, 1, T, d, "iid", seed=8)
+    outs = []
+    for perm_seed in (0, 1):
+        kp, vp, bt, sl = synth.to_paged(Kc, Vc, seq, 64, seed=perm_seed)
+        idx, cnt = H.mask_estimate_paged(Q, kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk)
+        o = H.sparse_attention_decode(Q, kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T, idx, cnt, k_budget=k, b_q=1,
+                                      b_k=bk)
+        outs.append((idx.cpu(), o.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    for b in range(B):
+        Kb, Vb = Kc[b:b + 1, :, : seq[b]].cuda(), Vc[b:b + 1, :, : seq[b]].cuda()
+        idx_c, cnt_c = H.mask_estimate(Q[b:b + 1], Kb, k_budget=k, b_q=1, b_k=bk, exact=True)
+        assert torch.equal(idx_c.cpu(), outs[0][0][b:b + 1])
+
+
+def test_batch_invariance():
+    """A sequence's result does not depend on the other sequences in the batch (PIN-9)."""
+    Q, K, V = synth.gen_qkv(3, 2, 2, 600, 600, 128, "llm", seed=9)
+    Q, K, V = Q.cuda(), K.cuda(), V.cuda()
+    o_all = H.hip_attention(Q, K, V, k_budget=128, b_q=32, b_k=2)
+    o_one = H.hip_attention(Q[1:2].contiguous(), K[1:2].contiguous(), V[1:2].contiguous(), k_budget=128, b_q=32, b_k=2)
+    assert torch.equal(o_all[1:2], o_one)
+
+
+def test_strided_views():
+    """Non-contiguous [B,H,T,d] views (e.g. a fused QKV buffer) give the same bits."""
+    B, Hq, T, d = 1, 2, 500, 128
+    base = torch.randn(B, T, 3, Hq, d, generator=torch.Generator().manual_seed(0)).to(torch.bfloat16).cuda()
+    q, k, v = (base[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    o1 = H.hip_attention(q, k, v, k_budget=128, b_q=32, b_k=2)
+    o2 = H.hip_attention(q.contiguous(), k.contiguous(), v.contiguous(), k_budget=128, b_q=32, b_k=2)
+    assert torch.equal(o1, o2)
+
+
+# ------------------------------------------------------------------------------------------------
+# End to end (mask -> attention) vs oracle (mask -> attention)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "llm"), (torch.bfloat16, "int"), (torch.bfloat16, "llm")])
+def test_hip_layer_end_to_end(orc, dt, dist):
+    B, Hq, Hkv, T, d, k, bq, bk = 1, 2, 1, 2048, 128, 256, 32, 2
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, T, T, d, dist, seed=10, dtype=dt)
+    gi, gc = _gpu_mask(Q, K, k, bq, bk, True)
+    o = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), torch.from_numpy(gi).cuda(),
+                                   torch.from_numpy(gc).cuda(), k_budget=k, b_q=bq, b_k=bk).float().cpu().numpy()
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, mode=orc.F32C if dt == torch.float32 or dist == "int" else orc.F64)
+    Oo, _ = orc.sparse_attention(Q, K, V, k, bq, bk, True, oi, oc)
+    same = ~(gi != oi).any(-1)  # [B,Hq,nqb]
+    rows = np.repeat(same, bq, axis=-1)[..., :T]
+    assert same.mean() >= 0.9
+    assert np.abs(o - Oo)[rows].max() <= TOL[dt]
+
+
+# ------------------------------------------------------------------------------------------------
+# Full-size configuration (BASELINE C2 shape, sampled): the launch bench.py times
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.slow
+def test_full_size_c2_sampled(orc):
+    B, Hq, Hkv, T, d, k, bq, bk = 1, 32, 32, 32768, 128, 512, 32, 2
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, T, T, d, "llm", seed=0, dtype=torch.bfloat16, device="cuda")
+    idx, cnt = H.mask_estimate(Q, K, k_budget=k, b_q=bq, b_k=bk)
+    o = H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=k, b_q=bq, b_k=bk)
+    torch.cuda.synchronize()
+    nqb = T // bq
+    rng = np.random.default_rng(0)
+    units = [(h, q) for h in rng.integers(0, Hq, 48) for q in
+             [0, 15, 16, 31, 32, nqb - 1, int(rng.integers(33, nqb - 1))]]
+    n_bad = n_unexpl = 0
+    gi_all, gc_all = idx.cpu().numpy(), cnt.cpu().numpy()
+    for h, q in units:
+        t1 = (q + 1) * bq
+        Qs = Q[:, h:h + 1, q * bq:t1].cpu()
+        Ks, Vs = K[:, h:h + 1, :t1].cpu(), V[:, h:h + 1, :t1].cpu()
+        oi, oc, dg = orc.mask(Qs, Ks, k, bq, bk, True, mode=orc.F64, diag=True)
+        gi = gi_all[0, h, q]
+        assert gc_all[0, h, q] == oc[0, 0, 0]
+        if not np.array_equal(gi, oi[0, 0, 0]):
+            n_bad += 1
+            eps = TAU_UNIT * d * dg["emax"][0, 0, 0]
+            n_unexpl += int(dg["margin_min"][0, 0, 0] > 2 * eps)
+            continue
+        Oo, _ = orc.sparse_attention(Qs, Ks, Vs, k, bq, bk, True, oi, oc)
+        assert np.abs(o[0, h, q * bq:t1].float().cpu().numpy() - Oo[0, 0]).max() <= 2e-2
+    print(f"\n[parity] C2 sampled: {n_bad}/{len(units)} query blocks differ, unexplained {n_unexpl}")
+    assert n_unexpl == 0
