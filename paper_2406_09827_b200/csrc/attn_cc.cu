@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
   float* qs = reinterpret_cast<float*>(smem);                 // [R][QP]
   float* S = qs + R * QP;                                      // [R][kKC + 1]
   int* tok = reinterpret_cast<int*>(S + R * (kKC + 1));        // [2][kKC] token of each staged key (-1 none)
-  char* kst = reinterpret_cast<char*>(tok + 2 * kKC);          // [2][kKC][KP]
+  char* kst = smem + align_up((size_t)((char*)(tok + 2 * kKC) - smem), 128);  // [2][kKC][KP]
   char* vst = kst + 2 * kKC * KP;                              // [2][kKC][KP]
   float* part = reinterpret_cast<float*>(kst);                 // reused for the WK merge
 
@@ -245,7 +245,7 @@ static cudaError_t launch_acc(const Shape& sh, const QSrc& qs, const RowSrc& ks,
   if (R > 64) return cudaErrorInvalidValue;
   int WR = R >= 8 ? 8 : (R >= 4 ? 4 : (R >= 2 ? 2 : 1));
   constexpr int KP = D * sizeof(T) + 16;
-  size_t smem = (size_t)R * (D + 4) * 4 + (size_t)R * (kKC + 1) * 4 + 2 * kKC * 4 + 4 * (size_t)kKC * KP;
+  size_t smem = align_up((size_t)R * (D + 4) * 4 + (size_t)R * (kKC + 1) * 4 + 2 * kKC * 4, 128) + 4 * (size_t)kKC * KP;
   size_t merge = (size_t)(8 / WR) * R * (D + 2) * 4;
   if (merge > 4 * (size_t)kKC * KP) smem += merge - 4 * (size_t)kKC * KP;
   smem = (smem + 15) & ~(size_t)15;

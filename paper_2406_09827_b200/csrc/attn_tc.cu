@@ -32,8 +32,8 @@ struct AttnTCSmem {
   static constexpr uint32_t ring0 = kATQTile;
   static constexpr uint32_t ring1 = ring0 + kATTile;
   static constexpr uint32_t p = ring1 + kATTile;                 // 4 chunks
-  static constexpr uint32_t red = p + 4 * kATPChunk;             // [2][4][32] floats
-  static constexpr uint32_t misc = red + 2 * 4 * 32 * 4;
+  static constexpr uint32_t red = p + 4 * kATPChunk;             // [3][4][32] floats
+  static constexpr uint32_t misc = red + 3 * 4 * 32 * 4;
   static constexpr uint32_t total = misc + 64;
 };
 
@@ -188,9 +188,9 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             mrow[j] = fmaxf(fmaxf(red[j], red[32 + j]), fmaxf(red[64 + j], red[96 + j]));
-          float lq = 0.f;
+          float lq = 0.f, lu = 0.f;  // sums of the bf16-rounded p (normalises O) / unrounded p (lse)
           for (int ch = 0; ch < nch; ++ch) {
-            float v[32];
+            float v[32], w[32];
             tmem_ld_32x32b_x32(tmem_lane + 32 * ch, v);
             const int64_t s = key_token(ch);
             uint32_t pk[16];
@@ -203,6 +203,8 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
                 const bool ok = s >= 0 && jj < rows_q && (!sh.causal || s <= tpos0 + jj) && mrow[jj] != -INFINITY;
                 p2[e] = ok ? exp2f(v[jj] * scale_log2 - mrow[jj]) : 0.f;
               }
+              w[j] = p2[0];
+              w[j + 1] = p2[1];
               __nv_bfloat162 pb = __floats2bfloat162_rn(p2[0], p2[1]);
               pk[j >> 1] = *reinterpret_cast<uint32_t*>(&pb);
               float2 pr = __bfloat1622float2(pb);
@@ -217,8 +219,10 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
             for (int cp = 0; cp < 4; ++cp)
               *reinterpret_cast<uint4*>(pc + cp * 2048) = make_uint4(pk[4 * cp], pk[4 * cp + 1], pk[4 * cp + 2], pk[4 * cp + 3]);
             lq += reduce_scatter32<false>(v, lane);
+            if (lse) lu += reduce_scatter32<false>(w, lane);
           }
           red[128 + warp * 32 + lane] = lq;
+          red[256 + warp * 32 + lane] = lu;
           tc_fence_before();
           fence_proxy_async_smem();
           __syncthreads();
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
     }
     if (lse && threadIdx.x < rows_q) {
       const int j = threadIdx.x;
-      const float l = red[128 + j] + red[160 + j] + red[192 + j] + red[224 + j];
+      const float l = red[256 + j] + red[288 + j] + red[320 + j] + red[352 + j];
       const float m = fmaxf(fmaxf(red[j], red[32 + j]), fmaxf(red[64 + j], red[96 + j]));
       lse[((int64_t)b * sh.Hq + h) * sh.Tq + (int64_t)q * sh.bq + j] = l > 0.f ? m * kATLn2 + logf(l) : -INFINITY;
     }

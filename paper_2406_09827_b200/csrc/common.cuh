@@ -81,6 +81,8 @@ __device__ __forceinline__ int visible_blocks(const Shape& sh, int q, int Tk) {
 // ----------------------------------------------------------------------------------------------
 // Small utilities
 // ----------------------------------------------------------------------------------------------
+__host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(kCCThreads) mask_cc_kernel(Shape sh, QSrc qsrc
   SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
   const int rows_max = min(sh.bq, sh.Tq);
   const int qpitch = sh.d + 4;
-  float* qs = reinterpret_cast<float*>(smem + sizeof(SelState<NMAX>));
-  char* stage0 = reinterpret_cast<char*>(qs + rows_max * qpitch);
+  float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
+  char* stage0 = reinterpret_cast<char*>(qs + rows_max * qpitch);  // qpitch*4 is a multiple of 16
   char* stage1 = stage0 + ch * sh.bk * kpitch;
   float* pairs = reinterpret_cast<float*>(stage1 + ch * sh.bk * kpitch);
 
@@ -152,7 +152,7 @@ static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   const int stage_bytes = 16 * 1024;
   int ch = max(1, stage_bytes / (sh.bk * kpitch));
   const int rows_max = min(sh.bq, sh.Tq);
-  size_t smem = sizeof(SelState<NMAX>) + (size_t)rows_max * (sh.d + 4) * 4 + 2 * (size_t)ch * sh.bk * kpitch +
+  size_t smem = align_up(sizeof(SelState<NMAX>), 128) + (size_t)rows_max * (sh.d + 4) * 4 + 2 * (size_t)ch * sh.bk * kpitch +
                 (size_t)ch * sh.bk * rows_max * 4;
   smem = (smem + 15) & ~(size_t)15;
   auto kern = mask_cc_kernel<T, NMAX>;

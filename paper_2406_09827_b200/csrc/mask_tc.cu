@@ -32,7 +32,7 @@ struct MaskTCSmemLayout {
   static constexpr uint32_t k0 = kQTileBytes;
   static constexpr uint32_t k1 = k0 + kKTileBytes;
   static constexpr uint32_t sel = k1 + kKTileBytes;
-  static constexpr uint32_t misc = sel + sizeof(SelState<kMTNmax>);
+  static constexpr uint32_t misc = (uint32_t)align_up(sel + sizeof(SelState<kMTNmax>), 128);  // mbarrier: 8B
   static constexpr uint32_t total = misc + 64;
 };
 

@@ -57,6 +57,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total)
   return base + x - v;
 }
 
+// NaN never occurs for finite inputs; mapping it to -inf keeps the ranking a total order.
+__device__ __forceinline__ float nan_to_ninf(float x) { return x != x ? -INFINITY : x; }
+
 __device__ __forceinline__ int next_pow2(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -149,7 +152,9 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
   constexpr int PER = (NMAX + NT - 1) / NT;
   int cur = 0;
   bool first = true;
-  for (;;) {
+  // Every iteration at least halves the largest node, so ceil(log2(B_q)) <= 31 iterations end the
+  // search; the cap only guards against non-finite inputs (NaN scores are mapped to -inf below).
+  for (int iter = 0; iter < 40; ++iter) {
     // --- branching (Alg. 1 lines 6-9): count the nodes that split, compact the right children
     const int j0 = tid * PER;
     int mine = 0;
@@ -181,9 +186,9 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     // --- representative scores (Alg. 1 lines 10-13)
     const int n_rep = first ? n + nB : nB;
     scorer.score(st.rep, n_rep, st.rep_s);
-    for (int i = tid; i < nB; i += NT) st.bs[i] = st.rep_s[(first ? n : 0) + i];
+    for (int i = tid; i < nB; i += NT) st.bs[i] = nan_to_ninf(st.rep_s[(first ? n : 0) + i]);
     if (first)
-      for (int j = tid; j < n; j += NT) st.s[cur][j] = st.rep_s[j];
+      for (int j = tid; j < n; j += NT) st.s[cur][j] = nan_to_ninf(st.rep_s[j]);
     __syncthreads();
     // --- top-n (Alg. 1 lines 14-15)
     if (first) bitonic_desc<NT>(st.s[cur], st.f[cur], st.l[cur], n);

@@ -71,7 +71,8 @@ def test_mask_fp32_c1_bitexact(orc, dist):
     (2, 2, 1, 700, 2100, 64, 128, 16, 4, True, "llm"),       # T_q < T_k, d=64
     (1, 2, 2, 1000, 1500, 128, 64, 32, 1, False, "iid"),     # non-causal, b_k=1
     (1, 1, 1, 50, 4000, 128, 512, 64, 8, True, "llm"),       # b_q=64 > 32 (CUDA-core path)
-    (1, 1, 1, 5, 3, 128, 2, 64, 8, False, "iid"),            # b_q > T_q and b_k > T_k
+    (1, 1, 1, 5, 3, 128, 16, 64, 8, False, "iid"),           # b_q > T_q and b_k > T_k
+    (1, 1, 1, 5, 700, 128, 16, 64, 8, False, "iid"),         # one ragged query block, 88 key blocks
     (1, 1, 1, 300, 300, 128, 2, 32, 2, True, "iid"),         # n = 1
 ])
 def test_mask_exact_scores_bitexact(orc, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal, dist):
