@@ -439,6 +439,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip the decode / 128k extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--decode-only", action="store_true", help="only the C3 decode step (profiling aid)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -462,6 +463,9 @@ def main():
         dist.init_process_group("nccl", device_id=device)
         pg = dist.group.WORLD
 
+    if args.decode_only:
+        print(json.dumps(bench_decode(args, device)), flush=True)
+        return
     r = bench_prefill(cfg, args, rank, world, device, pg)
     heads = r["heads_per_rank"] * world
     pk = peaks()

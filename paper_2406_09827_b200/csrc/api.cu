@@ -182,6 +182,8 @@ hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_
   const bool exact = (params->flags & HIP_FLAG_EXACT_SCORES) != 0;
   if (dtype == HIP_DTYPE_BF16 && !exact && hip::mask_tc_supported(sh))
     e = hip::launch_mask_tc(sh, qs, ks, block_idx, block_cnt, st, sms);
+  else if (hip::mask_decode_supported(sh))
+    e = hip::launch_mask_decode(sh, qs, ks, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, st, sms);
   else
     e = hip::launch_mask_cc(sh, qs, ks, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, st, sms);
   if (e != cudaSuccess) return cuda_fail(e, "hip_mask_estimate launch");

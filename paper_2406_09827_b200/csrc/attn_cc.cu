@@ -14,11 +14,12 @@ namespace hip {
 
 constexpr int kACThreads = 256;
 constexpr int kKC = 32;  // keys per staged chunk
+constexpr int kACStages = 3;  // cp.async ring depth (2 chunks in flight while one is consumed)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
+template <typename T, int D, int RPWM>
+__global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
                                                              const int32_t* __restrict__ idx,
                                                              const int32_t* __restrict__ cnt, float scale_log2,
                                                              char* __restrict__ o, int64_t osb, int64_t osh,
@@ -30,9 +31,9 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
   const int QP = D + 4;
   float* qs = reinterpret_cast<float*>(smem);                 // [R][QP]
   float* S = qs + R * QP;                                      // [R][kKC + 1]
-  int* tok = reinterpret_cast<int*>(S + R * (kKC + 1));        // [2][kKC] token of each staged key (-1 none)
-  char* kst = smem + align_up((size_t)((char*)(tok + 2 * kKC) - smem), 128);  // [2][kKC][KP]
-  char* vst = kst + 2 * kKC * KP;                              // [2][kKC][KP]
+  int* tok = reinterpret_cast<int*>(S + R * (kKC + 1));        // [S][kKC] token of each staged key (-1 none)
+  char* kst = smem + align_up((size_t)((char*)(tok + kACStages * kKC) - smem), 128);  // [S][kKC][KP]
+  char* vst = kst + kACStages * kKC * KP;                      // [S][kKC][KP]
   float* part = reinterpret_cast<float*>(kst);                 // reused for the WK merge
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -63,9 +64,9 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
       qs[t * QP + cc] = v;
     }
 
-    float m[8], l[8], acc[8][E];
+    float m[RPWM], l[RPWM], acc[RPWM][E];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < RPWM; ++i) {
       m[i] = -INFINITY;
       l[i] = 0.f;
 #pragma unroll
@@ -74,9 +75,11 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
 
     const int nch = (nkeys + kKC - 1) / kKC;
     auto issue = [&](int ch) {
+      if (ch >= nch) return;
       const int k0 = ch * kKC, kc = min(kKC, nkeys - k0);
       constexpr int pieces = D * sizeof(T) / 16;
-      int* tk = tok + (ch & 1) * kKC;
+      const int slot = ch % kACStages;
+      int* tk = tok + slot * kKC;
       for (int p = threadIdx.x; p < kKC * pieces * 2; p += kACThreads) {
         int which = p / (kKC * pieces);  // 0 = K, 1 = V
         int rem = p - which * kKC * pieces;
@@ -89,20 +92,23 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
         }
         if (which == 0 && c16 == 0) tk[r] = (int)s;
         const RowSrc& src = which ? vs : ks;
-        char* dst = (which ? vst : kst) + ((ch & 1) * kKC + r) * KP + c16 * 16;
+        char* dst = (which ? vst : kst) + (slot * kKC + r) * KP + c16 * 16;
         const char* g = row_ptr(src, b, hk, s >= 0 ? s : 0) + c16 * 16;
         cp_async16(smem_u32(dst), g, s >= 0 ? 16u : 0u);
       }
     };
     __syncthreads();
-    if (nch > 0) issue(0);
-    cp_async_commit();
-    for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) issue(ch + 1);
+#pragma unroll
+    for (int ch = 0; ch < kACStages - 1; ++ch) {
+      issue(ch);
       cp_async_commit();
-      cp_async_wait<1>();
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+      issue(ch + kACStages - 1);  // slot of chunk ch - 1, freed by the last barrier
+      cp_async_commit();
+      cp_async_wait<kACStages - 1>();
       __syncthreads();
-      const int buf = ch & 1;
+      const int buf = ch % kACStages;
       const int* tk = tok + buf * kKC;
       // scores x * log2(e), x = sm_scale q.k (G11); invalid -> -inf
       for (int p = threadIdx.x; p < rows_q * kKC; p += kACThreads) {
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
       __syncthreads();
       // online softmax + PV: this warp's rows x this warp's keys (k = wk + WK * j)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < RPWM; ++i) {
         const int t = wr + i * WR;
         if (i >= RPW || t >= rows_q) continue;
         const int k = wk + WK * lane;
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
     if (WK > 1) {
       const int stride = D + 2;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < RPWM; ++i) {
         const int t = wr + i * WR;
         if (i >= RPW || t >= rows_q) continue;
         float* pp = part + ((size_t)wk * R + t) * stride;
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
       __syncthreads();
       if (wk == 0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < RPWM; ++i) {
           const int t = wr + i * WR;
           if (i >= RPW || t >= rows_q) continue;
           float mm = -INFINITY;
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
     }
     if (wk == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < RPWM; ++i) {
         const int t = wr + i * WR;
         if (i >= RPW || t >= rows_q) continue;
         const bool empty = !(l[i] > 0.f);
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kACThreads) attn_cc_kernel(Shape sh, QSrc qsrc
   }
 }
 
-template <typename T, int D>
+template <typename T, int D, int RPWM>
 static cudaError_t launch_acc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
                               const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                               float* lse, cudaStream_t stream, int num_sms) {
@@ -245,15 +251,14 @@ static cudaError_t launch_acc(const Shape& sh, const QSrc& qs, const RowSrc& ks,
   if (R > 64) return cudaErrorInvalidValue;
   int WR = R >= 8 ? 8 : (R >= 4 ? 4 : (R >= 2 ? 2 : 1));
   constexpr int KP = D * sizeof(T) + 16;
-  size_t smem = align_up((size_t)R * (D + 4) * 4 + (size_t)R * (kKC + 1) * 4 + 2 * kKC * 4, 128) + 4 * (size_t)kKC * KP;
+  const size_t stages = 2 * (size_t)kACStages * kKC * KP;
+  size_t smem = align_up((size_t)R * (D + 4) * 4 + (size_t)R * (kKC + 1) * 4 + kACStages * kKC * 4, 128) + stages;
   size_t merge = (size_t)(8 / WR) * R * (D + 2) * 4;
-  if (merge > 4 * (size_t)kKC * KP) smem += merge - 4 * (size_t)kKC * KP;
-  smem = (smem + 15) & ~(size_t)15;
-  auto kern = attn_cc_kernel<T, D>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kACThreads, smem);
+  if (merge > stages) smem += merge - stages;
+  smem = align_up(smem, 16);
+  auto kern = attn_cc_kernel<T, D, RPWM>;
+  int per_sm = 1;
+  cudaError_t e = persistent_ctas(kern, kACThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * std::max(per_sm, 1));
@@ -262,17 +267,28 @@ static cudaError_t launch_acc(const Shape& sh, const QSrc& qs, const RowSrc& ks,
   return cudaGetLastError();
 }
 
+template <typename T, int D>
+static cudaError_t launch_acc_r(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
+                                const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
+                                float* lse, cudaStream_t stream, int num_sms) {
+  // rows per warp = ceil(R / WR) <= 2 whenever R <= 8 (decode / multi-query): fewer registers,
+  // 4 CTAs per SM
+  if (std::min(sh.bq, sh.Tq) <= 8)
+    return launch_acc<T, D, 2>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+  return launch_acc<T, D, 8>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+}
+
 cudaError_t launch_attn_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, bool bf16,
                            const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh,
                            int64_t ost, float* lse, cudaStream_t stream, int num_sms) {
   if (bf16) {
     if (sh.d == 128)
-      return launch_acc<__nv_bfloat16, 128>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
-    return launch_acc<__nv_bfloat16, 64>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+      return launch_acc_r<__nv_bfloat16, 128>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+    return launch_acc_r<__nv_bfloat16, 64>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
   }
   if (sh.d == 128)
-    return launch_acc<float, 128>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
-  return launch_acc<float, 64>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+    return launch_acc_r<float, 128>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+  return launch_acc_r<float, 64>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
 }
 
 }  // namespace hip

@@ -33,7 +33,8 @@ struct AttnTCSmem {
   static constexpr uint32_t ring1 = ring0 + kATTile;
   static constexpr uint32_t p = ring1 + kATTile;                 // 4 chunks
   static constexpr uint32_t red = p + 4 * kATPChunk;             // [3][4][32] floats
-  static constexpr uint32_t misc = red + 3 * 4 * 32 * 4;
+  static constexpr uint32_t tok = red + (3 * 4 * 32 + 32) * 4;   // [512] int token per key slot
+  static constexpr uint32_t misc = tok + 512 * 4;
   static constexpr uint32_t total = misc + 64;
 };
 
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_lane = tmem + ((uint32_t)(32 * warp) << 16);
   uint32_t phase = 0;
+  const int lbk = 31 - __clz(sh.bk);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -114,34 +116,39 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
       const char* src = q_ptr(qsrc, b, h, (int64_t)q * sh.bq + (ok ? r : 0)) + c16 * 16;
       cp_async16(sb + L::q + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
     }
-    // item i < nch: K tile i; item nch + i: V tile i; slot = i & 1
+    // token of every selected key slot (or -1 past T_k / past cnt), staged once per unit
+    int* tok = reinterpret_cast<int*>(base + L::tok);
+    for (int k = threadIdx.x; k < nch * 128; k += kATThreads) {
+      int s = -1;
+      if (k < nkeys) {
+        const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
+        s = (j << lbk) + (k & ((1 << lbk) - 1));
+        if (s >= Tk) s = -1;
+      }
+      tok[k] = s;
+    }
+    __syncthreads();
+    const char* kbase = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
+    const char* vbase = vs.base + (b * vs.sb + hk * vs.sh) * (int64_t)vs.esize;
+    const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
+    // item i < nch: K tile i; item nch + i: V tile i; slot = i & 1.  16 threads per 256-B row.
     auto issue = [&](int item) {
       const bool isv = item >= nch;
       const int ch = isv ? item - nch : item;
-      const RowSrc& src = isv ? vs : ks;
-      const uint32_t dst = (item & 1) ? sb + L::ring1 : sb + L::ring0;
-#pragma unroll 4
-      for (int p = threadIdx.x; p < 128 * 16; p += kATThreads) {
-        const int r = p >> 4, c16 = p & 15;
-        const int k = ch * 128 + r;
-        int64_t s = -1;
-        if (k < nkeys) {
-          const int j = min(max(__ldg(blk + k / sh.bk), 0), nkb - 1);
-          s = (int64_t)j * sh.bk + (k - (k / sh.bk) * sh.bk);
-          if (s >= Tk) s = -1;
-        }
-        const char* g = row_ptr(src, b, hk, s >= 0 ? s : 0) + c16 * 16;
-        cp_async16(dst + (c16 >> 3) * kATRegion + sw128_off(r, c16 & 7), g, s >= 0 ? 16u : 0u);
+      const char* g0 = isv ? vbase : kbase;
+      const uint32_t rb = isv ? vrow : krow;
+      const int c16 = threadIdx.x & 15, r0 = threadIdx.x >> 4;  // r0 < 8
+      const uint32_t dst = ((item & 1) ? sb + L::ring1 : sb + L::ring0) + (c16 >> 3) * kATRegion + r0 * 128 +
+                           (((c16 & 7) ^ r0) << 4);
+      const int* tk = tok + ch * 128 + r0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int s = tk[8 * i];
+        cp_async16(dst + i * 1024, g0 + (uint64_t)(uint32_t)(s >= 0 ? s : 0) * rb + c16 * 16, s >= 0 ? 16u : 0u);
       }
     };
     // token of this thread's key in chunk ch (or -1): used for masking
-    auto key_token = [&](int ch) -> int64_t {
-      const int k = ch * 128 + 32 * warp + lane;
-      if (k >= nkeys) return -1;
-      const int j = min(max(__ldg(blk + k / sh.bk), 0), nkb - 1);
-      const int64_t s = (int64_t)j * sh.bk + (k - (k / sh.bk) * sh.bk);
-      return s < Tk ? s : -1;
-    };
+    auto key_token = [&](int ch) -> int64_t { return tok[ch * 128 + 32 * warp + lane]; };
 
     const int nitems = 2 * nch;
     issue(0);
@@ -175,10 +182,15 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
             float v[32];
             tmem_ld_32x32b_x32(tmem_lane + 32 * ch, v);
             const int64_t s = key_token(ch);
+            if (s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0)) {  // visible to every row
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const bool ok = s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j);
-              v[j] = ok ? v[j] * scale_log2 : -INFINITY;
+              for (int j = 0; j < 32; ++j) v[j] *= scale_log2;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const bool ok = s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j);
+                v[j] = ok ? v[j] * scale_log2 : -INFINITY;
+              }
             }
             mq = fmaxf(mq, reduce_scatter32<true>(v, lane));
           }
@@ -193,6 +205,7 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
             float v[32], w[32];
             tmem_ld_32x32b_x32(tmem_lane + 32 * ch, v);
             const int64_t s = key_token(ch);
+            const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0);  // => every m finite
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
@@ -200,8 +213,9 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int jj = j + e;
-                const bool ok = s >= 0 && jj < rows_q && (!sh.causal || s <= tpos0 + jj) && mrow[jj] != -INFINITY;
-                p2[e] = ok ? exp2f(v[jj] * scale_log2 - mrow[jj]) : 0.f;
+                const bool ok = all_vis || (s >= 0 && jj < rows_q && (!sh.causal || s <= tpos0 + jj) &&
+                                            mrow[jj] != -INFINITY);
+                p2[e] = ok ? ex2_approx(fmaf(v[jj], scale_log2, -mrow[jj])) : 0.f;
               }
               w[j] = p2[0];
               w[j + 1] = p2[1];
@@ -245,18 +259,29 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
       }
       __syncthreads();  // slot (it & 1) consumed before issue(it + 2)
     }
-    // ---- epilogue: O^T lanes = d, columns = queries
+    // ---- epilogue: O^T lanes = d, columns = queries -> normalise, stage [32 q][128 d] bf16 in the
+    // (now free) P buffer, then 16-byte coalesced row stores
+    float* invl = red + 384;
+    if (threadIdx.x < 32) {
+      const int j = threadIdx.x;
+      const float l = red[128 + j] + red[160 + j] + red[192 + j] + red[224 + j];
+      invl[j] = l > 0.f ? 1.f / l : 0.f;
+    }
     tc_fence_after();
     float v[32];
     tmem_ld_32x32b_x32(tmem_lane + 128, v);
+    __syncthreads();
     const int d = 32 * warp + lane;
+    __nv_bfloat16* ostage = reinterpret_cast<__nv_bfloat16*>(base + L::p);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < 32; ++j) ostage[j * 128 + d] = __float2bfloat16_rn(v[j] * invl[j]);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int p = threadIdx.x + kATThreads * i, j = p >> 4, c16 = p & 15;
       if (j < rows_q) {
-        const float l = red[128 + j] + red[160 + j] + red[192 + j] + red[224 + j];
-        const float val = l > 0.f ? v[j] / l : 0.f;
-        reinterpret_cast<__nv_bfloat16*>(o)[b * osb + h * osh + ((int64_t)q * sh.bq + j) * ost + d] =
-            __float2bfloat16_rn(val);
+        char* dst = o + (b * osb + h * osh + ((int64_t)q * sh.bq + j) * ost) * 2 + c16 * 16;
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(base + L::p + j * 256 + c16 * 16);
       }
     }
     if (lse && threadIdx.x < rows_q) {
@@ -274,19 +299,16 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
 }
 
 bool attn_tc_supported(const Shape& sh) {
-  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && (128 % sh.bk) == 0 && (int64_t)sh.n * sh.bk <= 512;
+  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 && (int64_t)sh.n * sh.bk <= 512;
 }
 
 cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
                            const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                            float* lse, cudaStream_t stream, int num_sms) {
   const size_t smem = AttnTCSmem::total + 1024;
-  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaError_t e = persistent_ctas(attn_tc_kernel, kATThreads, smem, 256, &per_sm);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_tc_kernel, kATThreads, smem);
-  if (e != cudaSuccess) return e;
-  per_sm = std::min(std::max(per_sm, 1), 2);  // TMEM: 256 columns per CTA
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
   attn_tc_kernel<<<(unsigned)grid, kATThreads, smem, stream>>>(sh, qs, ks, vs, idx, cnt, sm_scale * kATLog2e, o, osb,

@@ -4,15 +4,56 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace hip {
 
+// Resident CTAs per SM for a persistent launch, computed from the real limits (shared memory with
+// the per-block reservation, registers, threads, TMEM columns) instead of the occupancy API, and
+// with the shared-memory carveout forced to the maximum.  Sets the dynamic-smem attribute.
+template <typename K>
+inline cudaError_t persistent_ctas(K kernel, int threads, size_t smem, int tmem_cols, int* per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  int dev = 0, smem_sm = 0, reserved = 0, regs_sm = 0, thr_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  const size_t per_block = smem + fa.sharedSizeBytes + (size_t)reserved;
+  int n = (int)(smem_sm / std::max<size_t>(per_block, 1));
+  const int regs = std::max(fa.numRegs, 1) * threads;
+  n = std::min(n, regs_sm / regs);
+  n = std::min(n, thr_sm / threads);
+  if (tmem_cols > 0) n = std::min(n, 512 / tmem_cols);
+  n = std::min(n, 32);
+  *per_sm = std::max(n, 1);
+  if (getenv("HIPATTN_VERBOSE"))
+    fprintf(stderr, "[hipattn] launch: threads=%d smem=%zu regs=%d -> %d CTAs/SM\n", threads, smem, fa.numRegs,
+            *per_sm);
+  return cudaSuccess;
+}
+
 // CUDA-core mask estimation (exact sequential fp32 scores), contiguous or paged keys.
 cudaError_t launch_mask_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, bool bf16, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms);
+
+// Short query blocks (decode, <= 4 rows): direct-load GEMV scoring, exact sequential fp32.
+bool mask_decode_supported(const Shape& sh);
+cudaError_t launch_mask_decode(const Shape& sh, const QSrc& qs, const RowSrc& ks, bool bf16, int32_t* idx,
+                               int32_t* cnt, cudaStream_t stream, int num_sms);
 
 // tcgen05 mask estimation (bf16, d = 128, b_q <= 32, b_k | 32), contiguous or paged keys.
 bool mask_tc_supported(const Shape& sh);

@@ -16,11 +16,14 @@ namespace hip {
 
 constexpr int kCCThreads = 256;
 
+constexpr int kCCStages = 4;  // cp.async ring depth: 3 chunks in flight while one is scored
+
 template <typename T>
 struct CCScorer {
   const float* qs;   // [rows_q][qpitch] fp32
   int qpitch;        // floats
-  char* stage[2];    // staged key rows
+  char* stage0;      // kCCStages staged chunks of key rows
+  int stage_bytes;
   int kpitch;        // bytes
   float* pairs;      // [rows_per_chunk][rows_q]
   RowSrc ks;
@@ -29,8 +32,9 @@ struct CCScorer {
 
   __device__ void issue(const int* rep, int n_rep, int c) {
     const int blk0 = c * ch, nblk = min(ch, n_rep - blk0);
+    if (nblk <= 0) return;
     const int rows = nblk * bk, pieces = (d * (int)sizeof(T)) / 16;
-    const uint32_t dst0 = smem_u32(stage[c & 1]);
+    const uint32_t dst0 = smem_u32(stage0 + (c % kCCStages) * stage_bytes);
     for (int p = threadIdx.x; p < rows * pieces; p += kCCThreads) {
       int r = p / pieces, c16 = p - r * pieces;
       int64_t s = (int64_t)rep[blk0 + r / bk] * bk + (r % bk);
@@ -42,15 +46,18 @@ struct CCScorer {
 
   __device__ void score(const int* rep, int n_rep, float* out) {
     const int nch = (n_rep + ch - 1) / ch;
-    issue(rep, n_rep, 0);
-    cp_async_commit();
-    for (int c = 0; c < nch; ++c) {
-      if (c + 1 < nch) issue(rep, n_rep, c + 1);
+#pragma unroll
+    for (int c = 0; c < kCCStages - 1; ++c) {
+      issue(rep, n_rep, c);
       cp_async_commit();
-      cp_async_wait<1>();
+    }
+    for (int c = 0; c < nch; ++c) {
+      issue(rep, n_rep, c + kCCStages - 1);  // slot of chunk c - 1, freed by the last barrier
+      cp_async_commit();
+      cp_async_wait<kCCStages - 1>();
       __syncthreads();
       const int blk0 = c * ch, nblk = min(ch, n_rep - blk0), rows = nblk * bk;
-      const char* kst = stage[c & 1];
+      const char* kst = stage0 + (c % kCCStages) * stage_bytes;
       for (int p = threadIdx.x; p < rows * rows_q; p += kCCThreads) {
         int t = p % rows_q, r = p / rows_q;
         int64_t s = (int64_t)rep[blk0 + r / bk] * bk + (r % bk);
@@ -96,22 +103,23 @@ struct CCScorer {
           }
         out[blk0 + lb] = best;
       }
-      __syncthreads();  // stage[c & 1] and pairs are reused by chunk c + 2 / c + 1
+      __syncthreads();  // the stage of chunk c and pairs are reused
     }
+    cp_async_wait<0>();
   }
 };
 
 template <typename T, int NMAX>
-__global__ void __launch_bounds__(kCCThreads) mask_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
-                                                             int32_t* __restrict__ cnt, int ch, int kpitch) {
+__global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
+                                                                int32_t* __restrict__ cnt, int ch, int kpitch,
+                                                                int stage_bytes) {
   extern __shared__ __align__(16) char smem[];
   SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
   const int rows_max = min(sh.bq, sh.Tq);
   const int qpitch = sh.d + 4;
   float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
   char* stage0 = reinterpret_cast<char*>(qs + rows_max * qpitch);  // qpitch*4 is a multiple of 16
-  char* stage1 = stage0 + ch * sh.bk * kpitch;
-  float* pairs = reinterpret_cast<float*>(stage1 + ch * sh.bk * kpitch);
+  float* pairs = reinterpret_cast<float*>(stage0 + kCCStages * stage_bytes);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -134,7 +142,7 @@ __global__ void __launch_bounds__(kCCThreads) mask_cc_kernel(Shape sh, QSrc qsrc
       __syncthreads();
     }
     CCScorer<T> sc;
-    sc.qs = qs; sc.qpitch = qpitch; sc.stage[0] = stage0; sc.stage[1] = stage1; sc.kpitch = kpitch;
+    sc.qs = qs; sc.qpitch = qpitch; sc.stage0 = stage0; sc.stage_bytes = stage_bytes; sc.kpitch = kpitch;
     sc.pairs = pairs; sc.ks = ks; sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.d = sh.d; sc.bk = sh.bk;
     sc.causal = sh.causal; sc.rows_q = rows_q; sc.ch = ch;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
@@ -149,21 +157,22 @@ static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
                              cudaStream_t stream, int num_sms) {
   const int esize = sizeof(T);
   const int kpitch = sh.d * esize + 16;
-  const int stage_bytes = 16 * 1024;
-  int ch = max(1, stage_bytes / (sh.bk * kpitch));
-  const int rows_max = min(sh.bq, sh.Tq);
-  size_t smem = align_up(sizeof(SelState<NMAX>), 128) + (size_t)rows_max * (sh.d + 4) * 4 + 2 * (size_t)ch * sh.bk * kpitch +
-                (size_t)ch * sh.bk * rows_max * 4;
-  smem = (smem + 15) & ~(size_t)15;
+  const int rows_max = std::min(sh.bq, sh.Tq);
+  // decode (a single query row) is HBM-latency-bound: small chunks, many in flight; prefill rows
+  // amortise bigger chunks.
+  const int target = rows_max <= 4 ? 10 * 1024 : 16 * 1024;
+  const int ch = std::max(1, target / (sh.bk * kpitch));
+  const int stage_bytes = (int)align_up((size_t)ch * sh.bk * kpitch, 128);
+  size_t smem = align_up(sizeof(SelState<NMAX>), 128) + (size_t)rows_max * (sh.d + 4) * 4 +
+                (size_t)kCCStages * stage_bytes + (size_t)ch * sh.bk * rows_max * 4;
+  smem = align_up(smem, 16);
   auto kern = mask_cc_kernel<T, NMAX>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCCThreads, smem);
+  int per_sm = 1;
+  cudaError_t e = persistent_ctas(kern, kCCThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * std::max(per_sm, 1));
-  kern<<<(unsigned)grid, kCCThreads, smem, stream>>>(sh, qs, ks, idx, cnt, ch, kpitch);
+  int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
+  kern<<<(unsigned)grid, kCCThreads, smem, stream>>>(sh, qs, ks, idx, cnt, ch, kpitch, stage_bytes);
   return cudaGetLastError();
 }
 

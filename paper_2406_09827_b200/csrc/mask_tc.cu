@@ -4,59 +4,71 @@
 // Block approximation makes every representative score a small dense contraction:
 // the b_q x d query block against the b_k x d rows of each representative key block.  Per iteration
 // the CTA gathers the (up to 2n, then n) representative key blocks of its query block, 128 key rows
-// per tile, straight from HBM/L2 into a 128-byte-swizzled K-major shared tile (coalesced 16-byte
-// cp.async; one key row = 256 B), and one thread issues
+// per tile, straight from L2/HBM into a 128-byte-swizzled K-major shared tile (coalesced 16-byte
+// cp.async: 16 threads per 256-byte key row, one 32x32->64-bit multiply-add per row address), and
+// one thread issues
 //     S^T[128 keys x 32 queries] = K_tile[128 x 128] . Q_block^T      (tcgen05.mma, M=128, N=32)
-// into 32 TMEM columns.  The epilogue warps read their 32 TMEM lanes (one key per thread, 32 query
-// columns), take the max over the valid (causal) query rows, then the max over the b_k lanes of a
-// block with shuffles -> one fp32 score per representative block, in shared memory.  The
-// selection (split, rank-merge top-n, tie toward the smaller block) is select.cuh.
+// into 32 TMEM columns (with NBUF = 2 the next tile's gather is in flight meanwhile).
+// Four warps read their 32 TMEM lanes (one key per thread, 32 query columns) and take the max over
+// the valid query rows (a plain 32-way max unless the block touches the causal diagonal), then the
+// max over the b_k lanes of a block with shuffles -> one fp32 score per block in shared memory.
+// The selection (split, unrolled register bitonic sort, rank merge, tie toward the smaller block)
+// is select.cuh.
 //
 // Why keys on M: b_q = 32 is below the smallest tcgen05 M (64), so the query block is the N=32
 // operand and the gathered keys fill M = 128.  The kernel is bound by the L2->SM
-// gather of representative rows (32 FLOP per gathered byte, far below the tensor-core ridge).
+// gather of representative rows (32 FLOP per gathered byte, far below the tensor-core ridge), so
+// the launch keeps several query blocks per SM in flight (persistent CTAs, NT x NBUF variants).
 #include "kernels.h"
 #include "select.cuh"
 
 namespace hip {
 
-constexpr int kMTThreads = 128;
 constexpr int kMTNmax = 256;
 constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 rows x 128 B
 constexpr uint32_t kKRegion = 128 * 128;         // 128 rows x 128 B
 constexpr uint32_t kKTileBytes = 2 * kKRegion;   // d = 128 -> two regions
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
+template <int NBUF>
 struct MaskTCSmemLayout {
   static constexpr uint32_t q = 0;
   static constexpr uint32_t k0 = kQTileBytes;
-  static constexpr uint32_t k1 = k0 + kKTileBytes;
-  static constexpr uint32_t sel = k1 + kKTileBytes;
+  static constexpr uint32_t sel = k0 + NBUF * kKTileBytes;
   static constexpr uint32_t misc = (uint32_t)align_up(sel + sizeof(SelState<kMTNmax>), 128);  // mbarrier: 8B
   static constexpr uint32_t total = misc + 64;
 };
 
+template <int NT, int NBUF, bool kPaged>
 struct TCScorer {
-  uint32_t q_s, k_s[2];
+  static constexpr int RPP = NT / 16;  // key rows per pass of the CTA (16 threads per row)
+  uint32_t q_s, k_s0;
   uint64_t* mbar;
   uint32_t* phase;
   uint32_t tmem;
   RowSrc ks;
-  int b, hk, Tk, bk, causal, rows_q, bpt;
+  const char* kh;        // contiguous: row 0 of this (b, kv head)
+  uint32_t row_bytes;    // contiguous: bytes between key rows
+  int b, hk, Tk, lbk, causal, rows_q, bpt;
   int64_t tpos0;
 
-  __device__ void issue(const int* rep, int n_rep, int c) {
+  __device__ __forceinline__ const char* row(int s) const {
+    if constexpr (kPaged) return row_ptr(ks, b, hk, s);
+    else return kh + (uint64_t)(uint32_t)s * row_bytes;
+  }
+
+  __device__ __forceinline__ void issue(const int* rep, int n_rep, int c) {
     const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
-    const uint32_t dst = k_s[c & 1];
-#pragma unroll 4
-    for (int p = threadIdx.x; p < 128 * 16; p += kMTThreads) {
-      const int r = p >> 4, c16 = p & 15;
-      const int lb = r / bk;
-      int64_t s = -1;
-      if (lb < nblk) s = (int64_t)rep[blk0 + lb] * bk + (r - lb * bk);
-      const bool ok = s >= 0 && s < Tk;
-      const char* src = row_ptr(ks, b, hk, ok ? s : 0) + c16 * 16;
-      cp_async16(dst + (c16 >> 3) * kKRegion + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
+    const int tid = threadIdx.x, c16 = tid & 15, r0 = tid >> 4;
+    const int bmask = (1 << lbk) - 1;
+    const uint32_t dst = k_s0 + (c % NBUF) * kKTileBytes + (c16 >> 3) * kKRegion + (r0 >> 3) * 1024 +
+                         (r0 & 7) * 128 + (((c16 & 7) ^ (r0 & 7)) << 4);
+#pragma unroll
+    for (int i = 0; i < 128 / RPP; ++i) {
+      const int r = r0 + RPP * i, lb = r >> lbk;
+      const int s = lb < nblk ? (rep[blk0 + lb] << lbk) + (r & bmask) : Tk;
+      const bool ok = s < Tk;
+      cp_async16(dst + i * (RPP / 8) * 1024, row(ok ? s : 0) + c16 * 16, ok ? 16u : 0u);
     }
   }
 
@@ -66,14 +78,18 @@ struct TCScorer {
     issue(rep, n_rep, 0);
     cp_async_commit();
     for (int c = 0; c < ntiles; ++c) {
-      if (c + 1 < ntiles) issue(rep, n_rep, c + 1);
-      cp_async_commit();
-      cp_async_wait<1>();
+      if constexpr (NBUF == 2) {
+        if (c + 1 < ntiles) issue(rep, n_rep, c + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
       fence_proxy_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
         tc_fence_after();
-        const uint32_t kt = k_s[c & 1];
+        const uint32_t kt = k_s0 + (c % NBUF) * kKTileBytes;
 #pragma unroll
         for (int s = 0; s < 8; ++s) {  // d = 128 = 8 x K16
           uint64_t a = smem_desc(kt + (s >> 2) * kKRegion + (s & 3) * 32, 16, 1024, kLayoutSw128);
@@ -84,36 +100,52 @@ struct TCScorer {
       }
       mbar_wait(mbar, *phase);
       *phase ^= 1u;
-      tc_fence_after();
-      float v[32];
-      tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * warp) << 16), v);
-      const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
-      const int r = 32 * warp + lane, lb = r / bk;
-      float best = -INFINITY;
-      if (lb < nblk) {
-        const int64_t s = (int64_t)rep[blk0 + lb] * bk + (r - lb * bk);
-        if (s < Tk) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < rows_q && (!causal || s <= tpos0 + j)) best = fmaxf(best, v[j]);
-        }
+      if constexpr (NBUF == 1) {  // the tile has been consumed by the MMA: refill it now
+        if (c + 1 < ntiles) issue(rep, n_rep, c + 1);
+        cp_async_commit();
       }
-      for (int off = 1; off < bk; off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-      if (lb < nblk && (r - lb * bk) == 0) out[blk0 + lb] = best;
-      tc_fence_before();
-      __syncthreads();  // TMEM read before the next MMA; tile c consumed before issue(c + 2)
+      if (warp < 4) {
+        tc_fence_after();
+        float v[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * warp) << 16), v);
+        const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
+        const int r = 32 * warp + lane, lb = r >> lbk;
+        float best = -INFINITY;
+        if (lb < nblk) {
+          const int s = (rep[blk0 + lb] << lbk) + (r & ((1 << lbk) - 1));
+          if (s < Tk) {
+            if (rows_q == 32 && (!causal || s <= tpos0)) {  // every query row sees this key
+              float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]), m2 = fmaxf(v[4], v[5]), m3 = fmaxf(v[6], v[7]);
+#pragma unroll
+              for (int j = 8; j < 32; j += 4) {
+                m0 = fmaxf(m0, v[j]); m1 = fmaxf(m1, v[j + 1]); m2 = fmaxf(m2, v[j + 2]); m3 = fmaxf(m3, v[j + 3]);
+              }
+              best = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < rows_q && (!causal || s <= tpos0 + j)) best = fmaxf(best, v[j]);
+            }
+          }
+        }
+        for (int off = 1; off < (1 << lbk); off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
+        if (lb < nblk && (r & ((1 << lbk) - 1)) == 0) out[blk0 + lb] = best;
+        tc_fence_before();
+      }
+      __syncthreads();  // TMEM read before the next MMA; tile consumed before it is refilled
     }
   }
 };
 
-__global__ void __launch_bounds__(kMTThreads) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
-                                                             int32_t* __restrict__ cnt) {
+template <int NT, int NBUF, bool kPaged>
+__global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
+                                                     int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout;
+  using L = MaskTCSmemLayout<NBUF>;
   SelState<kMTNmax>& st = *reinterpret_cast<SelState<kMTNmax>*>(base + L::sel);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8);
@@ -129,6 +161,7 @@ __global__ void __launch_bounds__(kMTThreads) mask_tc_kernel(Shape sh, QSrc qsrc
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   uint32_t phase = 0;
+  const int lbk = 31 - __clz(sh.bk);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -141,7 +174,7 @@ __global__ void __launch_bounds__(kMTThreads) mask_tc_kernel(Shape sh, QSrc qsrc
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
     if (Bq > sh.n) {
       // query block -> K-major SW128 tile (B operand, N = 32 rows, rows >= rows_q zero)
-      for (int p = threadIdx.x; p < 32 * 16; p += kMTThreads) {
+      for (int p = threadIdx.x; p < 32 * 16; p += NT) {
         const int r = p >> 4, c16 = p & 15;
         const bool ok = r < rows_q;
         const char* src = q_ptr(qsrc, b, h, (int64_t)q * sh.bq + (ok ? r : 0)) + c16 * 16;
@@ -149,18 +182,19 @@ __global__ void __launch_bounds__(kMTThreads) mask_tc_kernel(Shape sh, QSrc qsrc
       }
       cp_async_commit();
     }
-    TCScorer sc;
+    TCScorer<NT, NBUF, kPaged> sc;
     sc.q_s = sbase + L::q;
-    sc.k_s[0] = sbase + L::k0;
-    sc.k_s[1] = sbase + L::k1;
+    sc.k_s0 = sbase + L::k0;
     sc.mbar = mbar;
     sc.phase = &phase;
     sc.tmem = tmem;
     sc.ks = ks;
-    sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.bk = sh.bk; sc.causal = sh.causal; sc.rows_q = rows_q;
-    sc.bpt = 128 / sh.bk;
+    sc.kh = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
+    sc.row_bytes = (uint32_t)(ks.st * ks.esize);
+    sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
+    sc.bpt = 128 >> lbk;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
-    tree_search<kMTNmax, kMTThreads>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
+    tree_search<kMTNmax, NT>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
     __syncthreads();
   }
   tc_fence_before();
@@ -169,24 +203,35 @@ __global__ void __launch_bounds__(kMTThreads) mask_tc_kernel(Shape sh, QSrc qsrc
 }
 
 // The tensor-core path needs a real query block on N (>= 8 rows); single-row decode scoring is a
-// GEMV and runs on CUDA cores (mask_cc.cu, HBM-bound).
+// GEMV and runs on CUDA cores (mask_decode.cu, HBM-bound).  b_k must be a power of two <= 32 so
+// that a block's rows sit in one warp's TMEM lanes.
 bool mask_tc_supported(const Shape& sh) {
   return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && sh.bk <= 32 && (32 % sh.bk) == 0 && sh.n <= kMTNmax;
 }
 
-cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
-                           cudaStream_t stream, int num_sms) {
-  const size_t smem = MaskTCSmemLayout::total + 1024;
-  cudaError_t e = cudaFuncSetAttribute(mask_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int NT, int NBUF>
+static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
+                            cudaStream_t stream, int num_sms) {
+  const size_t smem = MaskTCSmemLayout<NBUF>::total + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<NT, NBUF, true> : mask_tc_kernel<NT, NBUF, false>;
+  int per_sm = 1;
+  cudaError_t e = persistent_ctas(kern, NT, smem, 32, &per_sm);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mask_tc_kernel, kMTThreads, smem);
-  if (e != cudaSuccess) return e;
-  per_sm = std::min(std::max(per_sm, 1), 16);  // TMEM: 32 columns per CTA, 512 per SM
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
-  mask_tc_kernel<<<(unsigned)grid, kMTThreads, smem, stream>>>(sh, qs, ks, idx, cnt);
+  kern<<<(unsigned)grid, NT, smem, stream>>>(sh, qs, ks, idx, cnt);
   return cudaGetLastError();
+}
+
+cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
+                           cudaStream_t stream, int num_sms) {
+  // HIPATTN_MASK_TC=<threads>x<buffers> selects a variant (tuning aid).  Default 256x1: measured on
+  // C2 (profiles/r01): 256x1 6.07 ms, 128x1 6.89, 256x2 7.17, 128x2 11.8.
+  const char* v = getenv("HIPATTN_MASK_TC");
+  if (v && !strcmp(v, "256x2")) return launch_v<256, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x1")) return launch_v<128, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x2")) return launch_v<128, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return launch_v<256, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
 
 }  // namespace hip

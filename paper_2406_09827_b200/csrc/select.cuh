@@ -2,14 +2,19 @@
 // (Alg. 1 lines 4-17).  Scoring of the representative key blocks is delegated to a
 // Scorer (CUDA-core sequential fp32 in mask_cc.cu, tcgen05 in mask_tc.cu).
 //
-// Data layout in shared memory (SelState): the n current nodes (f, l, score) are kept SORTED by
-// the ranking key (score desc, first block asc; reading G10).  Splitting a node at
-// m = floor((f + l + 1) / 2) (reading G3) turns it into a left child (f, m - 1) that keeps the
-// node's key (same first block => same representative => same score, exact) and a right child
-// (m, l) that needs a fresh score.  So each iteration the left children form a list A that is
-// already sorted, the right children a list B of <= n fresh scores: B is bitonic-sorted and
-// merged with A by rank (binary search), keeping the top n.  On the first
-// iteration A's scores are fresh too (2n scored blocks, PIN-7) and A is sorted as well.
+// Ranking key (reading G10): larger score first, equal scores -> smaller first block.
+// It is packed into one 64-bit integer, key = orderable(score) << 32 | ~first, so ranking is a
+// plain unsigned compare (+0 and -0 are normalised to the same key; NaN, impossible for finite
+// inputs, is mapped to -inf so the order stays total).
+//
+// The n current nodes are kept SORTED by key.  Splitting a node at m = floor((f + l + 1) / 2)
+// (reading G3) gives a left child (f, m - 1) that keeps the node's key (same first block => same
+// representative => same score, exact) and a right child (m, l) that needs a fresh score.  So
+// each iteration the left children form a list A that is already sorted and the right children a
+// list B of <= n fresh keys: B is sorted with a register/shuffle bitonic network (only the strides
+// that cross warps go through shared memory), then A and B are merged by rank (binary search) and
+// the first n kept.  On the first iteration A's scores are fresh too (2n scored
+// blocks, PIN-7) and A is sorted the same way.
 #pragma once
 
 #include "common.cuh"
@@ -18,17 +23,26 @@ namespace hip {
 
 template <int NMAX>
 struct SelState {
-  int f[2][NMAX];
-  int l[2][NMAX];
-  float s[2][NMAX];
-  int bf[NMAX];
+  uint64_t key[2][NMAX];   // nodes, sorted by key (descending)
+  int l[2][NMAX];          // last block of each node (first block = ~low word of key)
+  uint64_t bkey[NMAX];     // right children (B list)
   int bl[NMAX];
-  float bs[NMAX];
-  int rep[2 * NMAX];      // representative blocks to score this iteration
-  float rep_s[2 * NMAX];  // their scores (written by the Scorer)
+  int rep[2 * NMAX];       // representative blocks to score this iteration
+  float rep_s[2 * NMAX];   // their scores (written by the Scorer)
   int warp_tot[32];
   int total;
 };
+
+__device__ __forceinline__ uint32_t ord_score(float s) {
+  s = (s != s) ? -INFINITY : s;  // NaN -> -inf
+  s = (s == 0.f) ? 0.f : s;      // -0 -> +0
+  uint32_t u = __float_as_uint(s);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ uint64_t make_key(float s, int first) {
+  return ((uint64_t)ord_score(s) << 32) | (uint32_t)(~(uint32_t)first);
+}
+__device__ __forceinline__ int key_first(uint64_t k) { return (int)(~(uint32_t)k); }
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total) {
@@ -57,73 +71,104 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total)
   return base + x - v;
 }
 
-// NaN never occurs for finite inputs; mapping it to -inf keeps the ranking a total order.
-__device__ __forceinline__ float nan_to_ninf(float x) { return x != x ? -INFINITY : x; }
-
 __device__ __forceinline__ int next_pow2(int x) {
   int p = 1;
   while (p < x) p <<= 1;
   return p;
 }
 
-// Bitonic sort of P = next_pow2(cnt) entries by key descending; entries [cnt, P) are padded with
-// (-inf, INT_MAX) which rank below every real candidate.  Ends with __syncthreads().
-template <int NT>
-__device__ void bitonic_desc(float* s, int* f, int* l, int cnt) {
-  const int P = next_pow2(cnt);
-  for (int i = cnt + threadIdx.x; i < P; i += NT) {
-    s[i] = -INFINITY;
-    f[i] = 0x7fffffff;
-    l[i] = 0x7fffffff;
-  }
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += NT) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          bool up = (i & k) == 0;
-          float si = s[i], sj = s[ixj];
-          int fi = f[i], fj = f[ixj];
-          bool jg = key_greater(sj, fj, si, fi);
-          if (jg == up) {
-            s[i] = sj; s[ixj] = si;
-            f[i] = fj; f[ixj] = fi;
-            int li = l[i]; l[i] = l[ixj]; l[ixj] = li;
-          }
+// One compare-exchange step of the network, element e against e ^ J inside blocks of K.
+template <int K, int J>
+__device__ __forceinline__ void bitonic_step(uint64_t& key, int& pay, uint64_t pk, int pp, int e) {
+  const bool want_max = ((e & K) == 0) == ((e & J) == 0);
+  if (want_max ? (pk > key) : (pk < key)) { key = pk; pay = pp; }
+}
+
+template <int P, int NT, int K, int J>
+__device__ __forceinline__ void bitonic_stage(uint64_t (&key)[(P + NT - 1) / NT], int (&pay)[(P + NT - 1) / NT],
+                                              uint64_t* skey, int* spay) {
+  constexpr int E = P >= NT ? P / NT : 1;
+  const int tid = threadIdx.x;
+  const bool active = tid < P;
+  if constexpr (J >= NT) {  // partner in the same thread
+    constexpr int JR = J / NT;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if ((r & JR) == 0) {
+        const int e = r * NT + tid;
+        const bool desc_seg = (e & K) == 0;  // e is the lower index of the pair
+        if (desc_seg ? (key[r | JR] > key[r]) : (key[r | JR] < key[r])) {
+          uint64_t tk = key[r]; key[r] = key[r | JR]; key[r | JR] = tk;
+          int tp = pay[r]; pay[r] = pay[r | JR]; pay[r | JR] = tp;
         }
       }
-      __syncthreads();
+    }
+  } else if constexpr (J >= 32) {  // partner in another warp: through shared memory
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+      if (active) { skey[r * NT + tid] = key[r]; spay[r * NT + tid] = pay[r]; }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+      if (active) {
+        const int e = r * NT + tid;
+        bitonic_step<K, J>(key[r], pay[r], skey[e ^ J], spay[e ^ J], e);
+      }
+  } else if (active) {  // partner in the same warp
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)key[r], J);
+      const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(key[r] >> 32), J);
+      const int pp = __shfl_xor_sync(0xffffffffu, pay[r], J);
+      bitonic_step<K, J>(key[r], pay[r], ((uint64_t)hi << 32) | lo, pp, r * NT + tid);
     }
   }
 }
 
-template <int NT>
-__device__ void bitonic_asc_int(int* f, int cnt) {
-  const int P = next_pow2(cnt);
-  for (int i = cnt + threadIdx.x; i < P; i += NT) f[i] = 0x7fffffff;
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += NT) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          bool up = (i & k) == 0;
-          int a = f[i], b = f[ixj];
-          if ((a > b) == up) { f[i] = b; f[ixj] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  }
+template <int P, int NT, int K, int J>
+__device__ __forceinline__ void bitonic_stages(uint64_t (&key)[(P + NT - 1) / NT], int (&pay)[(P + NT - 1) / NT],
+                                               uint64_t* skey, int* spay) {
+  bitonic_stage<P, NT, K, J>(key, pay, skey, spay);
+  if constexpr (J > 1) bitonic_stages<P, NT, K, J / 2>(key, pay, skey, spay);
+  else if constexpr (K < P) bitonic_stages<P, NT, 2 * K, K>(key, pay, skey, spay);
 }
 
-// Number of entries of the descending-sorted list (s, f)[0, cnt) whose key is greater than (x, y).
-__device__ __forceinline__ int count_greater(const float* s, const int* f, int cnt, float x, int y) {
+// Bitonic sort, descending, of cnt <= P (key, payload) pairs held in shared memory (P a power of
+// two >= 32, compile-time: the whole network is unrolled); the result is written back to the
+// first cnt slots, entries past cnt are padded with key 0 (ranks below every real key).  Element
+// e = r * NT + threadIdx.x lives in register r of its thread: strides < 32 are warp shuffles,
+// strides >= NT in-thread, only strides in [32, NT) go through shared memory.  All NT threads call.
+template <int P, int NT>
+__device__ void bitonic_desc(uint64_t* skey, int* spay, int cnt) {
+  static_assert(P >= 32 && (P & (P - 1)) == 0, "P must be a power of two >= 32");
+  constexpr int E = P >= NT ? P / NT : 1;
+  const int tid = threadIdx.x;
+  const bool active = tid < P;
+  uint64_t key[E];
+  int pay[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int e = r * NT + tid;
+    key[r] = (active && e < cnt) ? skey[e] : 0ull;
+    pay[r] = (active && e < cnt) ? spay[e] : 0;
+  }
+  bitonic_stages<P, NT, 2, 1>(key, pay, skey, spay);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int e = r * NT + tid;
+    if (active && e < cnt) { skey[e] = key[r]; spay[e] = pay[r]; }
+  }
+  __syncthreads();
+}
+
+// Number of entries of the descending list key[0, cnt) strictly greater than x.
+__device__ __forceinline__ int count_greater(const uint64_t* key, int cnt, uint64_t x) {
   int lo = 0, hi = cnt;
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
-    if (key_greater(s[mid], f[mid], x, y)) lo = mid + 1; else hi = mid;
+    if (key[mid] > x) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
@@ -134,6 +179,8 @@ __device__ __forceinline__ int count_greater(const float* s, const int* f, int c
 // with a __syncthreads().
 template <int NMAX, int NT, class Scorer>
 __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, int32_t* out_idx, int32_t* out_cnt) {
+  constexpr int EMAX = (NMAX + NT - 1) / NT;
+  static_assert(NMAX >= 32 && (NMAX & (NMAX - 1)) == 0, "NMAX must be a power of two >= 32");
   const int tid = threadIdx.x;
   if (Bq <= n) {  // exact case (G1): every visible block
     for (int j = tid; j < n; j += NT) out_idx[j] = j < Bq ? j : -1;
@@ -142,40 +189,39 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
   }
   // Initial nodes (Alg. 1 line 4, readings G1-G3): f_j = floor((2 j B_q + n) / (2 n)).
   for (int j = tid; j < n; j += NT) {
-    int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
-    int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
-    st.f[0][j] = (int)fj;
+    const int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
+    const int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
+    st.key[0][j] = make_key(0.f, (int)fj);
     st.l[0][j] = (int)fj1 - 1;
-    st.s[0][j] = 0.f;
   }
   __syncthreads();
-  constexpr int PER = (NMAX + NT - 1) / NT;
+  constexpr int PER = EMAX;
   int cur = 0;
   bool first = true;
-  // Every iteration at least halves the largest node, so ceil(log2(B_q)) <= 31 iterations end the
-  // search; the cap only guards against non-finite inputs (NaN scores are mapped to -inf below).
+  // Every iteration at least halves the largest node, so <= 31 iterations end the search; the cap
+  // only guards against non-finite inputs.
   for (int iter = 0; iter < 40; ++iter) {
     // --- branching (Alg. 1 lines 6-9): count the nodes that split, compact the right children
     const int j0 = tid * PER;
     int mine = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      int j = j0 + i;
-      if (j < n && st.l[cur][j] > st.f[cur][j]) ++mine;
+      const int j = j0 + i;
+      if (j < n && st.l[cur][j] > key_first(st.key[cur][j])) ++mine;
     }
     int pos = block_excl_scan<NT>(mine, st.warp_tot, &st.total);
     const int nB = st.total;
     if (nB == 0) break;  // every node is a single block (G5/G6)
+    const int boff = first ? n : 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      int j = j0 + i;
+      const int j = j0 + i;
       if (j < n) {
-        int f = st.f[cur][j], l = st.l[cur][j];
+        const int f = key_first(st.key[cur][j]), l = st.l[cur][j];
         if (l > f) {
-          int m = (f + l + 1) >> 1;
-          st.bf[pos] = m;
+          const int m = (f + l + 1) >> 1;
           st.bl[pos] = l;
-          st.rep[(first ? n : 0) + pos] = m;
+          st.rep[boff + pos] = m;
           ++pos;
           st.l[cur][j] = m - 1;  // left child keeps (score, first)
         }
@@ -184,35 +230,37 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     }
     __syncthreads();
     // --- representative scores (Alg. 1 lines 10-13)
-    const int n_rep = first ? n + nB : nB;
-    scorer.score(st.rep, n_rep, st.rep_s);
-    for (int i = tid; i < nB; i += NT) st.bs[i] = nan_to_ninf(st.rep_s[(first ? n : 0) + i]);
+    scorer.score(st.rep, boff + nB, st.rep_s);
+    for (int i = tid; i < nB; i += NT) st.bkey[i] = make_key(st.rep_s[boff + i], st.rep[boff + i]);
     if (first)
-      for (int j = tid; j < n; j += NT) st.s[cur][j] = nan_to_ninf(st.rep_s[j]);
+      for (int j = tid; j < n; j += NT) st.key[cur][j] = make_key(st.rep_s[j], st.rep[j]);
     __syncthreads();
     // --- top-n (Alg. 1 lines 14-15)
-    if (first) bitonic_desc<NT>(st.s[cur], st.f[cur], st.l[cur], n);
-    bitonic_desc<NT>(st.bs, st.bf, st.bl, nB);
+    if (first) bitonic_desc<NMAX, NT>(st.key[cur], st.l[cur], n);
+    bitonic_desc<NMAX, NT>(st.bkey, st.bl, nB);
     const int nxt = cur ^ 1;
     for (int i = tid; i < n; i += NT) {
-      float s = st.s[cur][i];
-      int f = st.f[cur][i];
-      int r = i + count_greater(st.bs, st.bf, nB, s, f);
-      if (r < n) { st.s[nxt][r] = s; st.f[nxt][r] = f; st.l[nxt][r] = st.l[cur][i]; }
+      const uint64_t k = st.key[cur][i];
+      const int r = i + count_greater(st.bkey, nB, k);
+      if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.l[cur][i]; }
     }
     for (int i = tid; i < nB; i += NT) {
-      float s = st.bs[i];
-      int f = st.bf[i];
-      int r = i + count_greater(st.s[cur], st.f[cur], n, s, f);
-      if (r < n) { st.s[nxt][r] = s; st.f[nxt][r] = f; st.l[nxt][r] = st.bl[i]; }
+      const uint64_t k = st.bkey[i];
+      const int r = i + count_greater(st.key[cur], n, k);
+      if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.bl[i]; }
     }
     __syncthreads();
     cur = nxt;
     first = false;
   }
   // --- output (Alg. 1 line 17): first blocks of the final single-block nodes, ascending (G18)
-  bitonic_asc_int<NT>(st.f[cur], n);
-  for (int j = tid; j < n; j += NT) out_idx[j] = st.f[cur][j];
+  for (int j = tid; j < n; j += NT) {
+    st.bkey[j] = 0xFFFFFFFFull - (uint32_t)key_first(st.key[cur][j]);  // descending key = ascending block
+    st.bl[j] = 0;
+  }
+  __syncthreads();
+  bitonic_desc<NMAX, NT>(st.bkey, st.bl, n);
+  for (int j = tid; j < n; j += NT) out_idx[j] = (int)(0xFFFFFFFFull - st.bkey[j]);
   if (tid == 0) *out_cnt = n;
 }
 
