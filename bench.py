@@ -177,9 +177,9 @@ def bench_prefill(cfg, args, rank, world, device, pg):
     import torch.distributed as dist
     from paper_2406_09827_b200 import hipattn as HA
 
-    H = cfg["H"]
-    assert H % world == 0, f"{H} heads do not shard over {world} GPUs"
-    hs = list(range(rank * H // world, (rank + 1) * H // world))
+    from paper_2406_09827_b200 import dist as hd
+
+    hs = list(hd.head_range(cfg["H"], world, rank))  # heads shard (dist.py), no exchange in the hot loop
     Q, K, V = make_prefill_inputs(cfg, hs, args.seed, device)
     kw = dict(k_budget=cfg["k"], b_q=cfg["bq"], b_k=cfg["bk"], causal=True)
     O = torch.empty_like(Q)
@@ -187,7 +187,6 @@ def bench_prefill(cfg, args, rank, world, device, pg):
     n = cfg["k"] // cfg["bk"]
     idx = torch.empty(cfg["B"], len(hs), nqb, n, dtype=torch.int32, device=device)
     cnt = torch.empty(cfg["B"], len(hs), nqb, dtype=torch.int32, device=device)
-    gathered = torch.empty((world,) + tuple(O.shape), dtype=O.dtype, device=device) if world > 1 else None
     stream = torch.cuda.current_stream(device)
 
     def step(ev=None):
@@ -200,7 +199,7 @@ def bench_prefill(cfg, args, rank, world, device, pg):
         if ev is not None:
             ev[2].record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, O)
+            hd.gather_heads(O)  # the one collective: NCCL all-gather of the head shards over NVLink
 
     for _ in range(args.warmup):
         step()
@@ -251,7 +250,7 @@ def bench_prefill(cfg, args, rank, world, device, pg):
         Vd.copy_(Vh, non_blocking=True)
         o = HA.hip_attention(Qd, Kd, Vd, out=O, **kw)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, o)
+            hd.gather_heads(o)
         Oh.copy_(o, non_blocking=True)
 
     e2e_step()

@@ -50,6 +50,7 @@
 
 #define ORC_F32C 0
 #define ORC_F64 1
+#define ORC_F32L 2 /* reading G9b: 16 sequential segments + pairwise tree (d % 16 == 0) */
 
 typedef struct {
     int64_t f, l; /* first / last key-block index of the range, inclusive */
@@ -100,6 +101,22 @@ static double block_score(const float *Qh, const float *Kh, int64_t t0, int64_t 
                 float acc = 0.0f;
                 for (int c = 0; c < d; ++c) acc = fmaf(q[c], kk[c], acc);
                 v = (double)acc;
+                for (int c = 0; c < d; ++c) e += fabs((double)q[c] * (double)kk[c]);
+            } else if (mode == ORC_F32L) {
+                /* reading G9b: 16 segments of d/16 consecutive terms, each a sequential fmaf
+                 * chain, combined by the pairwise tree v[l] <- v[l] + v[l ^ o], o = 8, 4, 2, 1 */
+                float seg[16], nxt[16];
+                int w = d / 16;
+                for (int l = 0; l < 16; ++l) {
+                    float acc = 0.0f;
+                    for (int c = l * w; c < (l + 1) * w; ++c) acc = fmaf(q[c], kk[c], acc);
+                    seg[l] = acc;
+                }
+                for (int o = 8; o >= 1; o >>= 1) {
+                    for (int l = 0; l < 16; ++l) nxt[l] = seg[l] + seg[l ^ o];
+                    for (int l = 0; l < 16; ++l) seg[l] = nxt[l];
+                }
+                v = (double)seg[0];
                 for (int c = 0; c < d; ++c) e += fabs((double)q[c] * (double)kk[c]);
             } else {
                 double acc = 0.0;
@@ -163,6 +180,7 @@ static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, in
     int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
     int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
     orc_diag dg = {INFINITY, 0.0, 0, 0};
+    if (mode == ORC_F32L && d % 16) return ORC_EINVAL;
 
     if (Bq <= n) { /* exact case */
         for (int64_t j = 0; j < n; ++j) out_idx[j] = j < Bq ? (int32_t)j : -1;
@@ -309,6 +327,7 @@ int oracle_exact_block_topn(const float *Q, const float *K, int B, int Hq, int H
 {
     int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
     if (rc) return rc;
+    if (mode == ORC_F32L && d % 16) return ORC_EINVAL;
     int n = k / bk;
     int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
     int64_t units = (int64_t)B * Hq * nqb;
@@ -351,6 +370,7 @@ int oracle_block_scores(const float *Q, const float *K, int B, int Hq, int Hkv, 
                         double *scores, double *emax)
 {
     if (check_dims(B, Hq, Hkv, Tq, Tk, d, bk, bq, bk, causal)) return ORC_EINVAL;
+    if (mode == ORC_F32L && d % 16) return ORC_EINVAL;
     int err = ORC_OK;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < m; ++i) {

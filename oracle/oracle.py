@@ -21,6 +21,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 F32C = 0  # canonical fp32: acc = fmaf(q[c], k[c], acc), c = 0..d-1 (reading G9)
 F64 = 1   # fp64 dot products
+F32L = 2  # reading G9b: 16 sequential fmaf segments of d/16 terms + pairwise tree (o = 8, 4, 2, 1)
 
 _ERR = {1: "invalid value", 2: "out of memory", 3: "index out of range"}
 

@@ -182,7 +182,7 @@ hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_
   const bool exact = (params->flags & HIP_FLAG_EXACT_SCORES) != 0;
   if (dtype == HIP_DTYPE_BF16 && !exact && hip::mask_tc_supported(sh))
     e = hip::launch_mask_tc(sh, qs, ks, block_idx, block_cnt, st, sms);
-  else if (hip::mask_decode_supported(sh))
+  else if (!exact && hip::mask_decode_supported(sh))
     e = hip::launch_mask_decode(sh, qs, ks, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, st, sms);
   else
     e = hip::launch_mask_cc(sh, qs, ks, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, st, sms);
@@ -213,6 +213,9 @@ hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t 
   if (dtype == HIP_DTYPE_BF16 && hip::attn_tc_supported(sh))
     e = hip::launch_attn_tc(sh, qs, ks, vs, block_idx, block_cnt, scale, op, o.stride_b, o.stride_h, o.stride_t, lse,
                             st, sms);
+  else if (hip::attn_decode_supported(sh))
+    e = hip::launch_attn_decode(sh, qs, ks, vs, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, scale, op, o.stride_b,
+                                o.stride_h, o.stride_t, lse, st, sms);
   else
     e = hip::launch_attn_cc(sh, qs, ks, vs, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, scale, op, o.stride_b,
                             o.stride_h, o.stride_t, lse, st, sms);
@@ -241,10 +244,16 @@ hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H
   hip::RowSrc ks = make_paged(*paged, paged->k_pages, esz), vs = make_paged(*paged, paged->v_pages, esz);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* op = static_cast<char*>(const_cast<void*>(o.ptr));
-  cudaError_t e = hip::launch_attn_cc(sh, qs, ks, vs, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, scale, op,
-                                      o.stride_b, o.stride_h, o.stride_t, lse, st, sms);
+  cudaError_t e;
+  if (hip::attn_decode_supported(sh))
+    e = hip::launch_attn_decode(sh, qs, ks, vs, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, scale, op, o.stride_b,
+                                o.stride_h, o.stride_t, lse, st, sms);
+  else
+    e = hip::launch_attn_cc(sh, qs, ks, vs, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, scale, op, o.stride_b,
+                            o.stride_h, o.stride_t, lse, st, sms);
   if (e != cudaSuccess) return cuda_fail(e, "hip_sparse_attention_decode launch");
   return HIP_SUCCESS;
 }
 
 }  // extern "C"
+

@@ -87,6 +87,31 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Phase timers (profiling builds only: -DHIPATTN_PHASES, see profiles/phase_timers.py).  Thread 0
+// of each CTA accumulates clock64() deltas per phase into g_phase_cycles.
+#ifdef HIPATTN_PHASES
+__device__ unsigned long long g_phase_cycles[16];
+struct PhaseTimer {
+  unsigned long long acc[16];
+  long long t0;
+  __device__ PhaseTimer() { for (int i = 0; i < 16; ++i) acc[i] = 0; t0 = clock64(); }
+  __device__ __forceinline__ void mark(int p) {
+    long long t = clock64();
+    acc[p] += (unsigned long long)(t - t0);
+    t0 = t;
+  }
+  __device__ void flush() {
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 16; ++i) atomicAdd(&g_phase_cycles[i], acc[i]);
+  }
+};
+#define HIP_PT_MEMBER PhaseTimer* pt = nullptr;
+#define HIP_MARK(p) do { if (pt) pt->mark(p); } while (0)
+#else
+#define HIP_PT_MEMBER
+#define HIP_MARK(p) do { } while (0)
+#endif
+
 // 2^x with the SFU (relative error ~2^-22; the probabilities it feeds are rounded to bf16).
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

@@ -39,6 +39,7 @@ inline cudaError_t persistent_ctas(K kernel, int threads, size_t smem, int tmem_
   n = std::min(n, thr_sm / threads);
   if (tmem_cols > 0) n = std::min(n, 512 / tmem_cols);
   n = std::min(n, 32);
+  if (const char* cap = getenv("HIPATTN_CTAS_PER_SM")) n = std::min(n, atoi(cap));  // tuning aid
   *per_sm = std::max(n, 1);
   if (getenv("HIPATTN_VERBOSE"))
     fprintf(stderr, "[hipattn] launch: threads=%d smem=%zu regs=%d -> %d CTAs/SM\n", threads, smem, fa.numRegs,
@@ -64,6 +65,12 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
 cudaError_t launch_attn_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, bool bf16,
                            const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh,
                            int64_t ost, float* lse, cudaStream_t stream, int num_sms);
+
+// Short query blocks (decode, <= 4 rows): half-warp-per-key GEMV attention, online softmax.
+bool attn_decode_supported(const Shape& sh);
+cudaError_t launch_attn_decode(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, bool bf16,
+                               const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb,
+                               int64_t osh, int64_t ost, float* lse, cudaStream_t stream, int num_sms);
 
 // tcgen05 block-sparse attention prefill (bf16, d = 128, b_q <= 32, 128 % b_k == 0).
 bool attn_tc_supported(const Shape& sh);

@@ -29,6 +29,8 @@ struct CCScorer {
   RowSrc ks;
   int b, hk, Tk, d, bk, causal, rows_q, ch;  // ch = key blocks per chunk
   int64_t tpos0;     // key position of query row 0 of the block: q*bq + Tk - Tq
+  HIP_PT_MEMBER
+  __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
   __device__ void issue(const int* rep, int n_rep, int c) {
     const int blk0 = c * ch, nblk = min(ch, n_rep - blk0);

@@ -1,96 +1,117 @@
 // mask_decode.cu — HiP mask estimation for short query blocks (decode: one query row per sequence
 // against a paged KV cache; also T_q <= 4 multi-query).  With b_q = 1 the tile
-// score is a GEMV: there is nothing for tensor cores to do, and the kernel is bound by
-// HBM (the cache of a 128k sequence is far larger than L2).  Each thread owns one representative
-// key row per round, loads its 256 bytes straight from HBM with 16 independent 16-byte loads (the
-// whole round of a CTA, 32 KB, is in flight at once), and runs the canonical sequential fp32 chain
-// acc = fmaf(q[c], k[c], acc), c = 0..d-1 (reading G9) — so decode masks are bit-identical to the
-// oracle's F32C mode.  The max over the b_k rows of a block is a shuffle across adjacent lanes.
-// Many small CTAs (128 threads, ~15 KB of shared memory) keep every (sequence, head) unit of a
-// decode batch resident at once; the selection is select.cuh.
+// score is a GEMV: nothing for tensor cores to do, and the kernel is bound by HBM
+// (the cache of a 128k sequence is far larger than L2).
+//
+// Layout of the work: a half-warp (16 lanes) owns one representative key row at a time; lane l
+// loads the row's 16-byte slice l (a coalesced 256-byte row per half-warp), keeps its slice of the
+// query rows in registers, runs a sequential fmaf chain over its d/16 elements and the half-warp
+// sums the 16 partials with a fixed xor tree (o = 8, 4, 2, 1).  That order is the canonical fp32
+// order of this path, reading G9b ("F32L" in the oracle), so decode masks are bit-identical to the
+// oracle.  Each half-warp takes U = 16 consecutive rows per batch (all 16 loads in flight), so the
+// b_k <= 16 rows of a block stay in one half-warp and the block max needs no exchange.  Many small
+// CTAs (128 threads) keep every (sequence, head) unit of a decode batch resident; the selection is
+// select.cuh.
 #include "kernels.h"
 #include "select.cuh"
 
 namespace hip {
 
 constexpr int kMDThreads = 128;
-constexpr int kMDRows = 4;  // max query rows per block on this path
+constexpr int kMDRows = 4;   // max query rows per block on this path
+constexpr int kMDU = 16;     // rows per half-warp per batch (128 rows = 32 KB in flight per CTA)
 
 template <typename T, int D, bool kPaged>
-struct DirectScorer {
-  const float* qs;   // [rows_q][D] fp32 (smem, broadcast reads)
+struct LaneScorer {
+  static constexpr int E = D / 16;                 // elements per lane
+  static constexpr int NV = (E * (int)sizeof(T) + 15) / 16;  // 16-byte vectors per lane (1 or 2)
+  const float* qs;   // [rows_q][D] fp32 (smem)
   RowSrc ks;
   const char* kh;
-  int64_t row_bytes;
+  uint32_t row_bytes;
   int b, hk, Tk, lbk, causal, rows_q;
   int64_t tpos0;
+  HIP_PT_MEMBER
+  __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
-  __device__ __forceinline__ const char* row(int64_t s) const {
+  __device__ __forceinline__ const char* row(int s) const {
     if constexpr (kPaged) return row_ptr(ks, b, hk, s);
-    else return kh + s * row_bytes;
+    else return kh + (uint64_t)(uint32_t)s * row_bytes;
   }
 
   __device__ void score(const int* rep, int n_rep, float* out) {
-    constexpr int EPP = 16 / sizeof(T);          // elements per 16-byte piece
-    constexpr int NPIECE = D / EPP;              // pieces per row
-    constexpr int G = NPIECE < 16 ? NPIECE : 16; // pieces held in registers at once
+    const int lane16 = threadIdx.x & 15, hw = threadIdx.x >> 4;  // 8 half-warps
     const int bmask = (1 << lbk) - 1;
     const int rows_total = n_rep << lbk;
-    for (int base = 0; base < rows_total; base += kMDThreads) {
-      const int r = base + threadIdx.x;
-      float best = -INFINITY;
-      int64_t s = Tk;
-      if (r < rows_total) s = (int64_t)rep[r >> lbk] * (1 << lbk) + (r & bmask);
-      if (s < Tk) {
-        const uint4* src = reinterpret_cast<const uint4*>(row(s));
-        float acc[kMDRows];
+    // this lane's slice of every query row
+    float qv[kMDRows][E];
 #pragma unroll
-        for (int t = 0; t < kMDRows; ++t) acc[t] = 0.f;
+    for (int t = 0; t < kMDRows; ++t)
 #pragma unroll
-        for (int g0 = 0; g0 < NPIECE; g0 += G) {
-          uint4 buf[G];
+      for (int e = 0; e < E; ++e) qv[t][e] = t < rows_q ? qs[t * D + lane16 * E + e] : 0.f;
+
+    for (int base = 0; base < rows_total; base += 8 * kMDU) {
+      const int r0 = base + hw * kMDU;
+      uint4 buf[kMDU][NV];
+      int sv[kMDU];
 #pragma unroll
-          for (int i = 0; i < G; ++i) buf[i] = __ldg(src + g0 + i);
+      for (int i = 0; i < kMDU; ++i) {
+        const int r = r0 + i;
+        int s = Tk;
+        if (r < rows_total) s = (rep[r >> lbk] << lbk) + (r & bmask);
+        sv[i] = s;
+        if (s < Tk) {
+          const char* p = row(s) + lane16 * (E * (int)sizeof(T));
 #pragma unroll
-          for (int i = 0; i < G; ++i) {
-            float kv[EPP];
-            if constexpr (sizeof(T) == 4) {
-              kv[0] = __uint_as_float(buf[i].x); kv[1] = __uint_as_float(buf[i].y);
-              kv[2] = __uint_as_float(buf[i].z); kv[3] = __uint_as_float(buf[i].w);
-            } else {
-              kv[0] = bf16_lo(buf[i].x); kv[1] = bf16_hi(buf[i].x); kv[2] = bf16_lo(buf[i].y); kv[3] = bf16_hi(buf[i].y);
-              kv[4] = bf16_lo(buf[i].z); kv[5] = bf16_hi(buf[i].z); kv[6] = bf16_lo(buf[i].w); kv[7] = bf16_hi(buf[i].w);
-            }
-            const int c0 = (g0 + i) * EPP;
-#pragma unroll
-            for (int t = 0; t < kMDRows; ++t) {
-              if (t < rows_q) {
-                const float4* qv = reinterpret_cast<const float4*>(qs + t * D + c0);
-#pragma unroll
-                for (int e4 = 0; e4 < EPP / 4; ++e4) {
-                  const float4 qq = qv[e4];
-                  acc[t] = __fmaf_rn(qq.x, kv[4 * e4 + 0], acc[t]);
-                  acc[t] = __fmaf_rn(qq.y, kv[4 * e4 + 1], acc[t]);
-                  acc[t] = __fmaf_rn(qq.z, kv[4 * e4 + 2], acc[t]);
-                  acc[t] = __fmaf_rn(qq.w, kv[4 * e4 + 3], acc[t]);
-                }
-              }
+          for (int v = 0; v < NV; ++v) {
+            if constexpr (E * sizeof(T) >= 16) buf[i][v] = __ldg(reinterpret_cast<const uint4*>(p) + v);
+            else {
+              const uint2 h = __ldg(reinterpret_cast<const uint2*>(p));
+              buf[i][v] = make_uint4(h.x, h.y, 0u, 0u);
             }
           }
-        }
+        } else {
 #pragma unroll
-        for (int t = 0; t < kMDRows; ++t)
-          if (t < rows_q && (!causal || s <= tpos0 + t) && acc[t] > best) best = acc[t];
+          for (int v = 0; v < NV; ++v) buf[i][v] = make_uint4(0u, 0u, 0u, 0u);
+        }
       }
-      for (int off = 1; off <= bmask; off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-      if (r < rows_total && (r & bmask) == 0) out[r >> lbk] = best;
+      float blockbest = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kMDU; ++i) {
+        float kvv[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(&buf[i][0]);
+          if constexpr (sizeof(T) == 4) kvv[e] = __uint_as_float(w[e]);
+          else kvv[e] = (e & 1) ? bf16_hi(w[e >> 1]) : bf16_lo(w[e >> 1]);
+        }
+        float best = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < kMDRows; ++t) {
+          if (t < rows_q) {
+            float acc = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc = __fmaf_rn(qv[t][e], kvv[e], acc);
+#pragma unroll
+            for (int o = 8; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (sv[i] < Tk && (!causal || sv[i] <= tpos0 + t) && acc > best) best = acc;
+          }
+        }
+        // rows r0 + i of one block are consecutive inside this half-warp (b_k | U)
+        blockbest = fmaxf(blockbest, best);
+        const int r = r0 + i;
+        if ((r & bmask) == bmask) {
+          if (lane16 == 0 && r < rows_total) out[r >> lbk] = blockbest;
+          blockbest = -INFINITY;
+        }
+      }
     }
     __syncthreads();
   }
 };
 
 template <typename T, int D, int NMAX, bool kPaged>
-__global__ void __launch_bounds__(kMDThreads) mask_decode_kernel(Shape sh, QSrc qsrc, RowSrc ks,
+__global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                  int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) char smem[];
   SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
@@ -116,11 +137,11 @@ __global__ void __launch_bounds__(kMDThreads) mask_decode_kernel(Shape sh, QSrc 
       }
       __syncthreads();
     }
-    DirectScorer<T, D, kPaged> sc;
+    LaneScorer<T, D, kPaged> sc;
     sc.qs = qs;
     sc.ks = ks;
     sc.kh = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
-    sc.row_bytes = ks.st * (int64_t)ks.esize;
+    sc.row_bytes = (uint32_t)(ks.st * ks.esize);
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
     tree_search<NMAX, kMDThreads>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
@@ -128,8 +149,10 @@ __global__ void __launch_bounds__(kMDThreads) mask_decode_kernel(Shape sh, QSrc 
   }
 }
 
+// <= 4 query rows per block, b_k a power of two <= 16 (a block inside one half-warp batch).
 bool mask_decode_supported(const Shape& sh) {
-  return std::min(sh.bq, sh.Tq) <= kMDRows && sh.bk <= 32 && (sh.bk & (sh.bk - 1)) == 0 && (sh.d == 64 || sh.d == 128);
+  return std::min(sh.bq, sh.Tq) <= kMDRows && sh.bk <= kMDU && (sh.bk & (sh.bk - 1)) == 0 &&
+         (sh.d == 64 || sh.d == 128);
 }
 
 template <typename T, int D, int NMAX>

@@ -51,6 +51,8 @@ struct TCScorer {
   uint32_t row_bytes;    // contiguous: bytes between key rows
   int b, hk, Tk, lbk, causal, rows_q, bpt;
   int64_t tpos0;
+  HIP_PT_MEMBER
+  __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
   __device__ __forceinline__ const char* row(int s) const {
     if constexpr (kPaged) return row_ptr(ks, b, hk, s);
@@ -87,6 +89,7 @@ struct TCScorer {
       }
       fence_proxy_async_smem();
       __syncthreads();
+      mark(1);  // gather issue + wait
       if (threadIdx.x == 0) {
         tc_fence_after();
         const uint32_t kt = k_s0 + (c % NBUF) * kKTileBytes;
@@ -100,6 +103,7 @@ struct TCScorer {
       }
       mbar_wait(mbar, *phase);
       *phase ^= 1u;
+      mark(2);  // MMA
       if constexpr (NBUF == 1) {  // the tile has been consumed by the MMA: refill it now
         if (c + 1 < ntiles) issue(rep, n_rep, c + 1);
         cp_async_commit();
@@ -133,6 +137,7 @@ struct TCScorer {
         tc_fence_before();
       }
       __syncthreads();  // TMEM read before the next MMA; tile consumed before it is refilled
+      mark(3);  // epilogue
     }
   }
 };
@@ -162,6 +167,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
   const uint32_t tmem = *tmem_slot;
   uint32_t phase = 0;
   const int lbk = 31 - __clz(sh.bk);
+#ifdef HIPATTN_PHASES
+  PhaseTimer ptimer;
+#endif
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -194,11 +202,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.bpt = 128 >> lbk;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+#ifdef HIPATTN_PHASES
+    sc.pt = &ptimer;
+    ptimer.mark(7);  // unit setup / Q load / exact units
+#endif
     tree_search<kMTNmax, NT>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
     __syncthreads();
   }
   tc_fence_before();
   __syncthreads();
+#ifdef HIPATTN_PHASES
+  ptimer.flush();
+#endif
   if (warp == 0) tmem_dealloc<32>(tmem);
 }
 
@@ -235,3 +250,14 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
 }
 
 }  // namespace hip
+
+#ifdef HIPATTN_PHASES
+// Profiling builds only (profiles/phase_timers.py): read and clear this translation unit's
+// per-phase cycle counters.
+extern "C" int hip_debug_phase_cycles(unsigned long long* out16) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+  if (cudaMemcpyFromSymbol(out16, hip::g_phase_cycles, 16 * sizeof(unsigned long long)) != cudaSuccess) return 2;
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(hip::g_phase_cycles, z, sizeof(z)) == cudaSuccess ? 0 : 3;
+}
+#endif

@@ -229,6 +229,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
       }
     }
     __syncthreads();
+    scorer.mark(0);  // split + scan
     // --- representative scores (Alg. 1 lines 10-13)
     scorer.score(st.rep, boff + nB, st.rep_s);
     for (int i = tid; i < nB; i += NT) st.bkey[i] = make_key(st.rep_s[boff + i], st.rep[boff + i]);
@@ -238,6 +239,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     // --- top-n (Alg. 1 lines 14-15)
     if (first) bitonic_desc<NMAX, NT>(st.key[cur], st.l[cur], n);
     bitonic_desc<NMAX, NT>(st.bkey, st.bl, nB);
+    scorer.mark(4);  // keys + sorts
     const int nxt = cur ^ 1;
     for (int i = tid; i < n; i += NT) {
       const uint64_t k = st.key[cur][i];
@@ -250,6 +252,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
       if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.bl[i]; }
     }
     __syncthreads();
+    scorer.mark(5);  // rank merge
     cur = nxt;
     first = false;
   }
@@ -262,6 +265,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
   bitonic_desc<NMAX, NT>(st.bkey, st.bl, n);
   for (int j = tid; j < n; j += NT) out_idx[j] = (int)(0xFFFFFFFFull - st.bkey[j]);
   if (tid == 0) *out_cnt = n;
+  scorer.mark(6);  // output sort
 }
 
 }  // namespace hip

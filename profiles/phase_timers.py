@@ -1,0 +1,48 @@
+"""Per-phase cycle breakdown of the tcgen05 mask kernel (profiling aid).
+
+Builds a separate library with -DHIPATTN_PHASES (libhipattn_phases.so, never used by the product
+path), runs one C2-sized mask estimation and prints the share of CTA time per phase."""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+PHASES = ["split+scan", "gather issue+wait", "MMA", "epilogue", "keys+sort", "rank merge", "output sort",
+          "unit setup"]
+
+
+def build():
+    from paper_2406_09827_b200 import build as b
+    out = os.path.join(ROOT, "paper_2406_09827_b200", "libhipattn_phases.so")
+    cmd = [b.NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler",
+           "-fPIC", "-shared", "-cudart", "static", "-DHIPATTN_PHASES", "-I", os.path.join(ROOT, "include"), "-o", out,
+           *b.sources()]
+    subprocess.check_call(cmd)
+    return out
+
+
+def main():
+    import torch
+    from paper_2406_09827_b200 import hipattn as H, synth
+    lib_path = build() if "--build" in sys.argv else os.path.join(ROOT, "paper_2406_09827_b200", "libhipattn_phases.so")
+    H._lib = None
+    lib = H.load(lib_path)
+    fn = lib.hip_debug_phase_cycles
+    fn.argtypes = [ctypes.c_void_p]
+    T, Hh = int(os.environ.get("PT_T", 32768)), int(os.environ.get("PT_H", 32))
+    Q, K, _ = synth.gen_qkv(1, Hh, Hh, T, T, 128, "llm", seed=0, device="cuda", make_v=False)
+    H.mask_estimate(Q, K)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * 16)()
+    fn(buf)
+    H.mask_estimate(Q, K)
+    fn(buf)
+    tot = sum(buf[i] for i in range(8))
+    for i, nm in enumerate(PHASES):
+        print(f"{nm:22s} {100 * buf[i] / tot:5.1f}%   {buf[i] / 1e9:8.3f} Gcyc")
+
+
+if __name__ == "__main__":
+    main()

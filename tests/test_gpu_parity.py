@@ -2,8 +2,9 @@
 
 Bars (BASELINE.json north_star):
   * mask indices: bit-exact wherever both sides take the selection decisions in the same fp32
-    arithmetic — the fp32 / HIP_FLAG_EXACT_SCORES / decode kernels (sequential fmaf = oracle F32C)
-    on every input, and the tcgen05 kernel on integer-valued inputs (every sum exact).  For the
+    arithmetic — the fp32 / HIP_FLAG_EXACT_SCORES kernels (sequential fmaf = oracle F32C), the
+    decode GEMV kernel (16-segment fmaf + xor tree = oracle F32L, reading G9b) on every input, and
+    the tcgen05 kernel on integer-valued inputs (every sum exact).  For the
     tcgen05 kernel on Gaussian inputs the mismatching query blocks are reported as a fraction and
     every one must be certified as a near-tie by the oracle's fp64 selection margins.
   * attention outputs: max-abs <= 1e-4 (fp32) / 2e-2 (bf16) against the fp64 oracle on the same
@@ -197,8 +198,13 @@ def test_decode_paged_parity(orc, dt, dist, ps):
     o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T, idx, cnt, k_budget=k,
                                        b_q=1, b_k=bk, causal=True, return_lse=True)
     torch.cuda.synchronize()
-    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F32C)
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F32L)  # decode GEMV order (G9b)
     _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    # HIP_FLAG_EXACT_SCORES: the sequential chain, == oracle F32C
+    ie, ce = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk,
+                                   causal=True, exact=True)
+    oi2, oc2 = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F32C)
+    _assert_mask_equal(ie.cpu().numpy(), ce.cpu().numpy(), oi2, oc2)
     Oo, lo = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, oi, oc)
     assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
     assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
@@ -221,7 +227,7 @@ def test_paged_equals_contiguous_and_page_permutation():
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     for b in range(B):
         Kb, Vb = Kc[b:b + 1, :, : seq[b]].cuda(), Vc[b:b + 1, :, : seq[b]].cuda()
-        idx_c, cnt_c = H.mask_estimate(Q[b:b + 1], Kb, k_budget=k, b_q=1, b_k=bk, exact=True)
+        idx_c, cnt_c = H.mask_estimate(Q[b:b + 1], Kb, k_budget=k, b_q=1, b_k=bk)
         assert torch.equal(idx_c.cpu(), outs[0][0][b:b + 1])
 
 

@@ -434,3 +434,28 @@ def test_iteration_count_reading_g6(orc):
     need = np.array([0 if v <= 256 else math.ceil(math.log2(math.ceil(v / 256))) for v in vis])
     assert (dg["n_iter"][0, 0] <= need).all()
     assert (dg["n_iter"][0, 0][vis > 256] >= 1).all()
+
+
+# --------------------------------------------------------------------------------------------
+# F32L (reading G9b, the decode GEMV's fp32 order): exact on integer inputs, reduces to F32C when a
+# single segment is non-zero, and stays within the fp32 error bound of the exact (fp64) score.
+# --------------------------------------------------------------------------------------------
+def test_f32l_mode_pins(orc):
+    T, d, k, bq, bk = 1200, 128, 64, 1, 2
+    Qi, Ki, _ = synth.gen_qkv(1, 2, 1, T, T, d, "int", seed=13, dtype=torch.float32, make_v=False)
+    a = orc.mask(Qi, Ki, k, bq, bk, True, mode=orc.F32L)[0]
+    b = orc.mask(Qi, Ki, k, bq, bk, True, mode=orc.F64)[0]
+    assert np.array_equal(a, b)
+    Q, K, _ = synth.gen_qkv(1, 1, 1, 64, 64, d, "iid", seed=14, dtype=torch.float32, make_v=False)
+    Q1 = Q.clone()
+    Q1[..., 8:] = 0  # only segment 0 (elements 0..7) contributes: F32L == F32C bit-for-bit
+    tup = [(0, 0, q, j) for q in range(64) for j in range(0, 32, 3) if j <= q // 2]
+    s_l, _ = orc.block_scores(Q1, K, 1, 2, True, tup, mode=orc.F32L)
+    s_c, _ = orc.block_scores(Q1, K, 1, 2, True, tup, mode=orc.F32C)
+    assert np.array_equal(s_l, s_c)
+    s_l, em = orc.block_scores(Q, K, 1, 2, True, tup, mode=orc.F32L)
+    s_64, _ = orc.block_scores(Q, K, 1, 2, True, tup, mode=orc.F64)
+    gamma = (d // 16 + 4) * 2.0 ** -24 * 1.01
+    assert (np.abs(s_l - s_64) <= gamma * em).all()
+    with pytest.raises(ValueError):
+        orc.mask(Q[..., :24], K[..., :24], k, bq, bk, True, mode=orc.F32L)
