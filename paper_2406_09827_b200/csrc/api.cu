@@ -81,6 +81,8 @@ hip_status_t check_common(hip_dtype_t dt, int32_t B, int32_t Hq, int32_t Hkv, in
   if (p->k / p->b_k > 1024) return fail(HIP_ERROR_INVALID_VALUE, "n = k/b_k = %d > 1024", p->k / p->b_k);
   if (p->causal != 0 && p->causal != 1) return fail(HIP_ERROR_INVALID_VALUE, "causal must be 0 or 1");
   if (p->causal && Tq > Tk) return fail(HIP_ERROR_INVALID_VALUE, "causal with T_q=%d > T_k=%d", Tq, Tk);
+  if (((int64_t)Tk + p->b_k - 1) / p->b_k >= (1 << 22))
+    return fail(HIP_ERROR_NOT_SUPPORTED, "ceil(T_k / b_k) >= 2^22 key blocks (T_k=%d, b_k=%d)", Tk, p->b_k);
   if (std::min(p->b_q, Tq) > 64) return fail(HIP_ERROR_NOT_SUPPORTED, "query block of %d rows > 64", std::min(p->b_q, Tq));
   (void)dt;
   return HIP_SUCCESS;

@@ -68,11 +68,12 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
   using L = AttnTCSmem;
   float* red = reinterpret_cast<float*>(base + L::red);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(mbar, 1);
+    mbar_init(mbar, 1);  // one MMA-completion barrier per ring slot
+    mbar_init(mbar + 1, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<256>(tmem_slot);
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_lane = tmem + ((uint32_t)(32 * warp) << 16);
-  uint32_t phase = 0;
+  uint32_t phase[2] = {0u, 0u};
   const int lbk = 31 - __clz(sh.bk);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
@@ -150,13 +151,25 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
     // token of this thread's key in chunk ch (or -1): used for masking
     auto key_token = [&](int ch) -> int64_t { return tok[ch * 128 + 32 * warp + lane]; };
 
+    // Items stream through the 2-slot ring: item i < nch is K tile i, item nch + i is V tile i.  The
+    // MMA of an item is issued as soon as its bytes land and waited only to refill its slot with
+    // item + 2, so V0/V1 are already in flight while the softmax runs.
     const int nitems = 2 * nch;
+    bool pend[2] = {false, false};
+    auto wait_slot = [&](int sl) {
+      if (pend[sl]) {
+        mbar_wait(mbar + sl, phase[sl]);
+        phase[sl] ^= 1u;
+        pend[sl] = false;
+      }
+    };
     issue(0);
     cp_async_commit();
+    if (nitems > 1) issue(1);
+    cp_async_commit();
     for (int it = 0; it < nitems; ++it) {
-      if (it + 1 < nitems) issue(it + 1);
-      cp_async_commit();
-      cp_async_wait<1>();
+      if (it + 1 < nitems) cp_async_wait<1>();
+      else cp_async_wait<0>();
       fence_proxy_async_smem();
       __syncthreads();
       const uint32_t tile = (it & 1) ? sb + L::ring1 : sb + L::ring0;
@@ -169,12 +182,18 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
             uint64_t bq = smem_desc(sb + L::q + (s >> 2) * (32 * 128) + (s & 3) * 32, 16, 1024, kLayoutSw128);
             umma_bf16(tmem + 32 * it, a, bq, kIdescQK, s > 0 ? 1u : 0u);
           }
-          umma_commit(mbar);
+          umma_commit(mbar + (it & 1));
         }
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
+        pend[it & 1] = true;
+        if (it + 2 < nitems) {  // refill this slot (item it + 2) once its MMA has read it
+          wait_slot(it & 1);
+          issue(it + 2);
+          cp_async_commit();
+        }
         if (it == nch - 1) {
           // ---- softmax over all S tiles (two passes, S stays in TMEM)
+          wait_slot(0);
+          wait_slot(1);
           tc_fence_after();
           float mq;  // running max (log2 domain) of query `lane` over this warp's keys
           mq = -INFINITY;
@@ -252,13 +271,18 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
             uint64_t bp = smem_desc(pch + s * 256, 128, 2048, kLayoutNone);
             umma_bf16(tmem + 128, a, bp, kIdescPV, (ch > 0 || s > 0) ? 1u : 0u);
           }
-          umma_commit(mbar);
+          umma_commit(mbar + (it & 1));
         }
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
+        pend[it & 1] = true;
+        if (it + 2 < nitems) {
+          wait_slot(it & 1);
+          issue(it + 2);
+          cp_async_commit();
+        }
       }
-      __syncthreads();  // slot (it & 1) consumed before issue(it + 2)
     }
+    wait_slot(0);  // the last MMAs (O^T complete)
+    wait_slot(1);
     // ---- epilogue: O^T lanes = d, columns = queries -> normalise, stage [32 q][128 d] bf16 in the
     // (now free) P buffer, then 16-byte coalesced row stores
     float* invl = red + 384;

@@ -21,7 +21,7 @@ constexpr int kMDThreads = 128;
 constexpr int kMDRows = 4;   // max query rows per block on this path
 constexpr int kMDU = 16;     // rows per half-warp per batch (128 rows = 32 KB in flight per CTA)
 
-template <typename T, int D, bool kPaged>
+template <typename T, int D, int RM, bool kPaged>
 struct LaneScorer {
   static constexpr int E = D / 16;                 // elements per lane
   static constexpr int NV = (E * (int)sizeof(T) + 15) / 16;  // 16-byte vectors per lane (1 or 2)
@@ -44,9 +44,9 @@ struct LaneScorer {
     const int bmask = (1 << lbk) - 1;
     const int rows_total = n_rep << lbk;
     // this lane's slice of every query row
-    float qv[kMDRows][E];
+    float qv[RM][E];
 #pragma unroll
-    for (int t = 0; t < kMDRows; ++t)
+    for (int t = 0; t < RM; ++t)
 #pragma unroll
       for (int e = 0; e < E; ++e) qv[t][e] = t < rows_q ? qs[t * D + lane16 * E + e] : 0.f;
 
@@ -87,7 +87,7 @@ struct LaneScorer {
         }
         float best = -INFINITY;
 #pragma unroll
-        for (int t = 0; t < kMDRows; ++t) {
+        for (int t = 0; t < RM; ++t) {
           if (t < rows_q) {
             float acc = 0.f;
 #pragma unroll
@@ -110,7 +110,7 @@ struct LaneScorer {
   }
 };
 
-template <typename T, int D, int NMAX, bool kPaged>
+template <typename T, int D, int NMAX, int RM, bool kPaged>
 __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                  int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) char smem[];
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
       }
       __syncthreads();
     }
-    LaneScorer<T, D, kPaged> sc;
+    LaneScorer<T, D, RM, kPaged> sc;
     sc.qs = qs;
     sc.ks = ks;
     sc.kh = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
@@ -155,11 +155,11 @@ bool mask_decode_supported(const Shape& sh) {
          (sh.d == 64 || sh.d == 128);
 }
 
-template <typename T, int D, int NMAX>
+template <typename T, int D, int NMAX, int RM>
 static cudaError_t launch_md(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                              cudaStream_t stream, int num_sms) {
   const size_t smem = align_up(sizeof(SelState<NMAX>), 128) + kMDRows * D * 4;
-  auto kern = ks.paged ? mask_decode_kernel<T, D, NMAX, true> : mask_decode_kernel<T, D, NMAX, false>;
+  auto kern = ks.paged ? mask_decode_kernel<T, D, NMAX, RM, true> : mask_decode_kernel<T, D, NMAX, RM, false>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kMDThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
@@ -172,8 +172,12 @@ static cudaError_t launch_md(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
 template <typename T, int D>
 static cudaError_t launch_md_n(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                                cudaStream_t stream, int num_sms) {
-  if (sh.n <= 256) return launch_md<T, D, 256>(sh, qs, ks, idx, cnt, stream, num_sms);
-  return launch_md<T, D, 1024>(sh, qs, ks, idx, cnt, stream, num_sms);
+  const bool one = std::min(sh.bq, sh.Tq) == 1;  // plain decode: one query row
+  if (sh.n <= 256)
+    return one ? launch_md<T, D, 256, 1>(sh, qs, ks, idx, cnt, stream, num_sms)
+               : launch_md<T, D, 256, kMDRows>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return one ? launch_md<T, D, 1024, 1>(sh, qs, ks, idx, cnt, stream, num_sms)
+             : launch_md<T, D, 1024, kMDRows>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
 
 cudaError_t launch_mask_decode(const Shape& sh, const QSrc& qs, const RowSrc& ks, bool bf16, int32_t* idx,

@@ -4,21 +4,23 @@
 // Block approximation makes every representative score a small dense contraction:
 // the b_q x d query block against the b_k x d rows of each representative key block.  Per iteration
 // the CTA gathers the (up to 2n, then n) representative key blocks of its query block, 128 key rows
-// per tile, straight from L2/HBM into a 128-byte-swizzled K-major shared tile (coalesced 16-byte
-// cp.async: 16 threads per 256-byte key row, one 32x32->64-bit multiply-add per row address), and
-// one thread issues
-//     S^T[128 keys x 32 queries] = K_tile[128 x 128] . Q_block^T      (tcgen05.mma, M=128, N=32)
-// into 32 TMEM columns (with NBUF = 2 the next tile's gather is in flight meanwhile).
-// Four warps read their 32 TMEM lanes (one key per thread, 32 query columns) and take the max over
-// the valid query rows (a plain 32-way max unless the block touches the causal diagonal), then the
-// max over the b_k lanes of a block with shuffles -> one fp32 score per block in shared memory.
-// The selection (split, unrolled register bitonic sort, rank merge, tie toward the smaller block)
-// is select.cuh.
+// per tile, straight from L2/HBM into 128-byte-swizzled K-major shared memory (coalesced 16-byte
+// cp.async, 8 threads per 128-byte half row), and one thread issues
+//     S^T_c [128 keys x 32 queries] = K_tile_c [128 x 128] . Q_block^T   (tcgen05.mma, M=128, N=32)
+// into TMEM columns [32c, 32c+32) as two d-halves (4 x K16 each).  Half tiles stream through a ring
+// of SLOTS 16 KB shared slots: the MMA of a half tile is issued as soon as its bytes land and only
+// waited for when its slot is refilled, so tensor-core latency hides under the gathers.  After each
+// round of up to TT tiles ONE epilogue pass reads the accumulators: each thread of warps 0-3 owns a
+// TMEM lane (one key, 32 query columns), maxes over the valid query rows (a plain 32-way max unless
+// the block touches the causal diagonal), then over the b_k lanes of a block with shuffles -> one
+// fp32 score per representative block.  The selection (split, unrolled register bitonic sort of
+// packed keys, rank merge, tie toward the smaller block) is select.cuh.
 //
 // Why keys on M: b_q = 32 is below the smallest tcgen05 M (64), so the query block is the N=32
-// operand and the gathered keys fill M = 128.  The kernel is bound by the L2->SM
-// gather of representative rows (32 FLOP per gathered byte, far below the tensor-core ridge), so
-// the launch keeps several query blocks per SM in flight (persistent CTAs, NT x NBUF variants).
+// operand and the gathered keys fill M = 128.  Gathers are 32 FLOP per byte, far below
+// the tensor-core ridge.  Random 512-byte gathers from L2 sustain ~16 TB/s on B200 only with many
+// independent streams per SM (profiles/r01/gather_ceiling.json), so the default launch is small
+// CTAs (128 threads, 32 KB ring, 128 TMEM columns) with 4 query blocks in flight per SM.
 #include "kernels.h"
 #include "select.cuh"
 
@@ -26,25 +28,26 @@ namespace hip {
 
 constexpr int kMTNmax = 256;
 constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 rows x 128 B
-constexpr uint32_t kKRegion = 128 * 128;         // 128 rows x 128 B
-constexpr uint32_t kKTileBytes = 2 * kKRegion;   // d = 128 -> two regions
+constexpr uint32_t kKRegion = 128 * 128;         // 128 rows x 128 B = one half-tile slot
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
-template <int NBUF>
+template <int SLOTS>
 struct MaskTCSmemLayout {
   static constexpr uint32_t q = 0;
   static constexpr uint32_t k0 = kQTileBytes;
-  static constexpr uint32_t sel = k0 + NBUF * kKTileBytes;
-  static constexpr uint32_t misc = (uint32_t)align_up(sel + sizeof(SelState<kMTNmax>), 128);  // mbarrier: 8B
-  static constexpr uint32_t total = misc + 64;
+  static constexpr uint32_t sel = k0 + SLOTS * kKRegion;
+  static constexpr uint32_t misc = (uint32_t)align_up(sel + sizeof(SelState<kMTNmax>), 128);  // mbarriers
+  static constexpr uint32_t total = misc + 128;
 };
 
-template <int NT, int NBUF, bool kPaged>
+template <int NT, int SLOTS, int TT, bool kPaged>
 struct TCScorer {
-  static constexpr int RPP = NT / 16;  // key rows per pass of the CTA (16 threads per row)
+  static_assert(SLOTS >= 2 && (SLOTS & (SLOTS - 1)) == 0, "ring of 2^k half-tile slots");
+  static constexpr int RPT = NT / 8;  // half rows per pass (8 threads per 128-byte half row)
   uint32_t q_s, k_s0;
-  uint64_t* mbar;
-  uint32_t* phase;
+  uint64_t* mbar;     // [SLOTS], one per ring slot
+  uint32_t* phase;    // [SLOTS]
+  uint32_t pend = 0;  // slots whose MMA has been committed but not yet waited
   uint32_t tmem;
   RowSrc ks;
   const char* kh;        // contiguous: row 0 of this (b, kv head)
@@ -59,113 +62,138 @@ struct TCScorer {
     else return kh + (uint64_t)(uint32_t)s * row_bytes;
   }
 
-  __device__ __forceinline__ void issue(const int* rep, int n_rep, int c) {
+  // Item i of a round = (tile c0 + i/2, d-half i&1): 128 key rows x 128 bytes into slot i % SLOTS.
+  __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
+    const int c = c0 + (i >> 1), h = i & 1;
     const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
-    const int tid = threadIdx.x, c16 = tid & 15, r0 = tid >> 4;
+    const int tid = threadIdx.x, c8 = tid & 7, r0 = tid >> 3;
     const int bmask = (1 << lbk) - 1;
-    const uint32_t dst = k_s0 + (c % NBUF) * kKTileBytes + (c16 >> 3) * kKRegion + (r0 >> 3) * 1024 +
-                         (r0 & 7) * 128 + (((c16 & 7) ^ (r0 & 7)) << 4);
+    const uint32_t dst = k_s0 + (i & (SLOTS - 1)) * kKRegion + (r0 >> 3) * 1024 + (r0 & 7) * 128 +
+                         ((c8 ^ (r0 & 7)) << 4);
 #pragma unroll
-    for (int i = 0; i < 128 / RPP; ++i) {
-      const int r = r0 + RPP * i, lb = r >> lbk;
+    for (int j = 0; j < 128 / RPT; ++j) {
+      const int r = r0 + RPT * j, lb = r >> lbk;
       const int s = lb < nblk ? (rep[blk0 + lb] << lbk) + (r & bmask) : Tk;
       const bool ok = s < Tk;
-      cp_async16(dst + i * (RPP / 8) * 1024, row(ok ? s : 0) + c16 * 16, ok ? 16u : 0u);
+      cp_async16(dst + j * (RPT / 8) * 1024, row(ok ? s : 0) + h * 128 + c8 * 16, ok ? 16u : 0u);
+    }
+  }
+
+  __device__ __forceinline__ void wait_slot(int slot) {
+    if (pend & (1u << slot)) {
+      mbar_wait(mbar + slot, phase[slot]);
+      phase[slot] ^= 1u;
+      pend &= ~(1u << slot);
+    }
+  }
+
+  __device__ void epilogue(const int* rep, int n_rep, int c0, int nt, float* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= 4) return;
+    const int r = 32 * warp + lane, bm = (1 << lbk) - 1;
+    for (int cc = 0; cc < nt; ++cc) {
+      const int c = c0 + cc;
+      float v[32];
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * warp) << 16) + 32 * cc, v);
+      const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
+      const int lb = r >> lbk;
+      float best = -INFINITY;
+      if (lb < nblk) {
+        const int s = (rep[blk0 + lb] << lbk) + (r & bm);
+        if (s < Tk) {
+          if (rows_q == 32 && (!causal || s <= tpos0)) {  // every query row sees this key
+            float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]), m2 = fmaxf(v[4], v[5]), m3 = fmaxf(v[6], v[7]);
+#pragma unroll
+            for (int j = 8; j < 32; j += 4) {
+              m0 = fmaxf(m0, v[j]); m1 = fmaxf(m1, v[j + 1]); m2 = fmaxf(m2, v[j + 2]); m3 = fmaxf(m3, v[j + 3]);
+            }
+            best = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < rows_q && (!causal || s <= tpos0 + j)) best = fmaxf(best, v[j]);
+          }
+        }
+      }
+      for (int off = 1; off <= bm; off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
+      if (lb < nblk && (r & bm) == 0) out[blk0 + lb] = best;
     }
   }
 
   __device__ void score(const int* rep, int n_rep, float* out) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (n_rep + bpt - 1) / bpt;
-    issue(rep, n_rep, 0);
-    cp_async_commit();
-    for (int c = 0; c < ntiles; ++c) {
-      if constexpr (NBUF == 2) {
-        if (c + 1 < ntiles) issue(rep, n_rep, c + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      fence_proxy_async_smem();
-      __syncthreads();
-      mark(1);  // gather issue + wait
-      if (threadIdx.x == 0) {
-        tc_fence_after();
-        const uint32_t kt = k_s0 + (c % NBUF) * kKTileBytes;
+    for (int c0 = 0; c0 < ntiles; c0 += TT) {  // rounds of up to TT tiles (TMEM columns)
+      const int nt = min(TT, ntiles - c0), nitems = 2 * nt;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {  // d = 128 = 8 x K16
-          uint64_t a = smem_desc(kt + (s >> 2) * kKRegion + (s & 3) * 32, 16, 1024, kLayoutSw128);
-          uint64_t bq = smem_desc(q_s + (s >> 2) * (32 * 128) + (s & 3) * 32, 16, 1024, kLayoutSw128);
-          umma_bf16(tmem, a, bq, kIdescS, s > 0 ? 1u : 0u);
-        }
-        umma_commit(mbar);
-      }
-      mbar_wait(mbar, *phase);
-      *phase ^= 1u;
-      mark(2);  // MMA
-      if constexpr (NBUF == 1) {  // the tile has been consumed by the MMA: refill it now
-        if (c + 1 < ntiles) issue(rep, n_rep, c + 1);
+      for (int i = 0; i < SLOTS - 1; ++i) {  // prologue: SLOTS - 1 half tiles in flight
+        if (i < nitems) issue(rep, n_rep, c0, i);
         cp_async_commit();
       }
-      if (warp < 4) {
-        tc_fence_after();
-        float v[32];
-        tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * warp) << 16), v);
-        const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
-        const int r = 32 * warp + lane, lb = r >> lbk;
-        float best = -INFINITY;
-        if (lb < nblk) {
-          const int s = (rep[blk0 + lb] << lbk) + (r & ((1 << lbk) - 1));
-          if (s < Tk) {
-            if (rows_q == 32 && (!causal || s <= tpos0)) {  // every query row sees this key
-              float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]), m2 = fmaxf(v[4], v[5]), m3 = fmaxf(v[6], v[7]);
+      for (int i = 0; i < nitems; ++i) {
+        cp_async_wait<SLOTS - 2>();  // item i landed
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          tc_fence_after();
+          const int cc = i >> 1, h = i & 1;
+          const uint32_t kt = k_s0 + (i & (SLOTS - 1)) * kKRegion;
 #pragma unroll
-              for (int j = 8; j < 32; j += 4) {
-                m0 = fmaxf(m0, v[j]); m1 = fmaxf(m1, v[j + 1]); m2 = fmaxf(m2, v[j + 2]); m3 = fmaxf(m3, v[j + 3]);
-              }
-              best = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j < rows_q && (!causal || s <= tpos0 + j)) best = fmaxf(best, v[j]);
-            }
+          for (int s = 0; s < 4; ++s) {  // one d-half = 4 x K16
+            uint64_t a = smem_desc(kt + s * 32, 16, 1024, kLayoutSw128);
+            uint64_t bq = smem_desc(q_s + h * (32 * 128) + s * 32, 16, 1024, kLayoutSw128);
+            umma_bf16(tmem + 32 * cc, a, bq, kIdescS, (h | s) ? 1u : 0u);
           }
+          umma_commit(mbar + (i & (SLOTS - 1)));
         }
-        for (int off = 1; off < (1 << lbk); off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-        if (lb < nblk && (r & ((1 << lbk) - 1)) == 0) out[blk0 + lb] = best;
-        tc_fence_before();
+        pend |= 1u << (i & (SLOTS - 1));
+        // refill the slot of item i - 1 (the oldest one in the ring) with item i + SLOTS - 1 once
+        // item i - 1's MMA has read it
+        if (i + SLOTS - 1 < nitems) {
+          wait_slot((i + SLOTS - 1) & (SLOTS - 1));
+          issue(rep, n_rep, c0, i + SLOTS - 1);
+        }
+        cp_async_commit();
       }
-      __syncthreads();  // TMEM read before the next MMA; tile consumed before it is refilled
+      mark(1);  // gathers + MMA issue
+#pragma unroll
+      for (int sl = 0; sl < SLOTS; ++sl) wait_slot(sl);  // drain the round's MMAs
+      mark(2);  // MMA drain
+      tc_fence_after();
+      epilogue(rep, n_rep, c0, nt, out);
+      tc_fence_before();
+      __syncthreads();  // scores visible; TMEM reads done before the next round's MMAs
       mark(3);  // epilogue
     }
   }
 };
 
-template <int NT, int NBUF, bool kPaged>
-__global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
-                                                     int32_t* __restrict__ cnt) {
+template <int NT, int SLOTS, int TT, bool kPaged>
+__global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
+                                                              int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+  constexpr uint32_t kCols = 32 * TT;
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<NBUF>;
+  using L = MaskTCSmemLayout<SLOTS>;
   SelState<kMTNmax>& st = *reinterpret_cast<SelState<kMTNmax>*>(base + L::sel);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
   const int warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
-    mbar_init(mbar, 1);
+    for (int s = 0; s < SLOTS; ++s) mbar_init(mbar + s, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<32>(tmem_slot);
+  if (warp == 0) tmem_alloc<kCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  uint32_t phase = 0;
+  uint32_t phase[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) phase[s] = 0u;
   const int lbk = 31 - __clz(sh.bk);
 #ifdef HIPATTN_PHASES
   PhaseTimer ptimer;
@@ -190,11 +218,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
       }
       cp_async_commit();
     }
-    TCScorer<NT, NBUF, kPaged> sc;
+    TCScorer<NT, SLOTS, TT, kPaged> sc;
     sc.q_s = sbase + L::q;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = mbar;
-    sc.phase = &phase;
+    sc.phase = phase;
     sc.tmem = tmem;
     sc.ks = ks;
     sc.kh = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
@@ -214,23 +242,24 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
 #ifdef HIPATTN_PHASES
   ptimer.flush();
 #endif
-  if (warp == 0) tmem_dealloc<32>(tmem);
+  if (warp == 0) tmem_dealloc<kCols>(tmem);
 }
 
 // The tensor-core path needs a real query block on N (>= 8 rows); single-row decode scoring is a
-// GEMV and runs on CUDA cores (mask_decode.cu, HBM-bound).  b_k must be a power of two <= 32 so
-// that a block's rows sit in one warp's TMEM lanes.
+// GEMV (mask_decode.cu).  b_k must be a power of two <= 32 so that a block's rows sit in one warp's
+// TMEM lanes.
 bool mask_tc_supported(const Shape& sh) {
-  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && sh.bk <= 32 && (32 % sh.bk) == 0 && sh.n <= kMTNmax;
+  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && sh.bk >= 1 && sh.bk <= 32 && (32 % sh.bk) == 0 &&
+         sh.n <= kMTNmax;
 }
 
-template <int NT, int NBUF>
+template <int NT, int SLOTS, int TT>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
-  const size_t smem = MaskTCSmemLayout<NBUF>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<NT, NBUF, true> : mask_tc_kernel<NT, NBUF, false>;
+  const size_t smem = MaskTCSmemLayout<SLOTS>::total + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<NT, SLOTS, TT, true> : mask_tc_kernel<NT, SLOTS, TT, false>;
   int per_sm = 1;
-  cudaError_t e = persistent_ctas(kern, NT, smem, 32, &per_sm);
+  cudaError_t e = persistent_ctas(kern, NT, smem, 32 * TT, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
@@ -240,16 +269,14 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
-  // HIPATTN_MASK_TC=<threads>x<buffers> selects a variant (tuning aid).  Default 256x1: measured on
-  // C2 (profiles/r01): 256x1 6.07 ms, 128x1 6.89, 256x2 7.17, 128x2 11.8.
+  // HIPATTN_MASK_TC=<threads>x<slots>x<tiles> selects a variant (tuning aid, profiles/r01).
   const char* v = getenv("HIPATTN_MASK_TC");
-  if (v && !strcmp(v, "256x2")) return launch_v<256, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x1")) return launch_v<128, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x2")) return launch_v<128, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-  return launch_v<256, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "256x4x8")) return launch_v<256, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "256x2x4")) return launch_v<256, 2, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x4x4")) return launch_v<128, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x2x2")) return launch_v<128, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return launch_v<128, 2, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
-
-}  // namespace hip
 
 #ifdef HIPATTN_PHASES
 // Profiling builds only (profiles/phase_timers.py): read and clear this translation unit's
@@ -261,3 +288,5 @@ extern "C" int hip_debug_phase_cycles(unsigned long long* out16) {
   return cudaMemcpyToSymbol(hip::g_phase_cycles, z, sizeof(z)) == cudaSuccess ? 0 : 3;
 }
 #endif
+
+}  // namespace hip

@@ -1,11 +1,15 @@
 // select.cuh — the tree-search control of HiP mask estimation for one query block, run by one CTA
 // (Alg. 1 lines 4-17).  Scoring of the representative key blocks is delegated to a
-// Scorer (CUDA-core sequential fp32 in mask_cc.cu, tcgen05 in mask_tc.cu).
+// Scorer (CUDA-core sequential fp32 in mask_cc.cu, GEMV in mask_decode.cu, tcgen05 in mask_tc.cu).
 //
 // Ranking key (reading G10): larger score first, equal scores -> smaller first block.
-// It is packed into one 64-bit integer, key = orderable(score) << 32 | ~first, so ranking is a
-// plain unsigned compare (+0 and -0 are normalised to the same key; NaN, impossible for finite
-// inputs, is mapped to -inf so the order stays total).
+// It is packed into one 64-bit integer
+//     key = orderable(score) << 32 | (kFirstMax - first) << kSlotBits | slot
+// so ranking is a plain unsigned compare (+0 and -0 normalised to one key; NaN, impossible for
+// finite inputs, mapped to -inf so the order is total).  `slot` is the entry's position in the
+// unsorted array it was built from; first blocks are unique among candidates, so the slot never
+// decides an order — it only lets the sort move 64-bit keys alone (no payload) and the merge find
+// each entry's last block afterwards.
 //
 // The n current nodes are kept SORTED by key.  Splitting a node at m = floor((f + l + 1) / 2)
 // (reading G3) gives a left child (f, m - 1) that keeps the node's key (same first block => same
@@ -21,12 +25,18 @@
 
 namespace hip {
 
+constexpr int kFirstBits = 22;                       // first block < 2^22 (T_k <= 4M * b_k)
+constexpr uint32_t kFirstMax = (1u << kFirstBits) - 1;
+
 template <int NMAX>
 struct SelState {
+  static constexpr int kSlotBits = 32 - kFirstBits;  // 10 bits: NMAX <= 1024
+  static_assert(NMAX <= (1 << kSlotBits), "slot field too small");
   uint64_t key[2][NMAX];   // nodes, sorted by key (descending)
-  int l[2][NMAX];          // last block of each node (first block = ~low word of key)
+  int l[2][NMAX];          // last block of each node, aligned with key
   uint64_t bkey[NMAX];     // right children (B list)
-  int bl[NMAX];
+  int bl[NMAX];            // their last blocks, indexed by slot
+  int ltmp[NMAX];
   int rep[2 * NMAX];       // representative blocks to score this iteration
   float rep_s[2 * NMAX];   // their scores (written by the Scorer)
   int warp_tot[32];
@@ -39,10 +49,18 @@ __device__ __forceinline__ uint32_t ord_score(float s) {
   uint32_t u = __float_as_uint(s);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
-__device__ __forceinline__ uint64_t make_key(float s, int first) {
-  return ((uint64_t)ord_score(s) << 32) | (uint32_t)(~(uint32_t)first);
+__device__ __forceinline__ uint64_t make_key(float s, int first, int slot) {
+  constexpr int kSlotBits = 32 - kFirstBits;
+  return ((uint64_t)ord_score(s) << 32) | ((uint32_t)(kFirstMax - (uint32_t)first) << kSlotBits) | (uint32_t)slot;
 }
-__device__ __forceinline__ int key_first(uint64_t k) { return (int)(~(uint32_t)k); }
+__device__ __forceinline__ int key_first(uint64_t k) {
+  constexpr int kSlotBits = 32 - kFirstBits;
+  return (int)(kFirstMax - ((uint32_t)k >> kSlotBits));
+}
+__device__ __forceinline__ int key_slot(uint64_t k) {
+  constexpr int kSlotBits = 32 - kFirstBits;
+  return (int)((uint32_t)k & ((1u << kSlotBits) - 1));
+}
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total) {
@@ -71,22 +89,16 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total)
   return base + x - v;
 }
 
-__device__ __forceinline__ int next_pow2(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
-
-// One compare-exchange step of the network, element e against e ^ J inside blocks of K.
+// One compare-exchange of the network: element e against e ^ J inside blocks of K; the pair
+// ends descending inside blocks with (e & K) == 0, ascending otherwise.
 template <int K, int J>
-__device__ __forceinline__ void bitonic_step(uint64_t& key, int& pay, uint64_t pk, int pp, int e) {
+__device__ __forceinline__ uint64_t bitonic_pick(uint64_t key, uint64_t pk, int e) {
   const bool want_max = ((e & K) == 0) == ((e & J) == 0);
-  if (want_max ? (pk > key) : (pk < key)) { key = pk; pay = pp; }
+  return want_max ? (pk > key ? pk : key) : (pk < key ? pk : key);
 }
 
 template <int P, int NT, int K, int J>
-__device__ __forceinline__ void bitonic_stage(uint64_t (&key)[(P + NT - 1) / NT], int (&pay)[(P + NT - 1) / NT],
-                                              uint64_t* skey, int* spay) {
+__device__ __forceinline__ void bitonic_stage(uint64_t (&key)[(P + NT - 1) / NT], uint64_t* skey) {
   constexpr int E = P >= NT ? P / NT : 1;
   const int tid = threadIdx.x;
   const bool active = tid < P;
@@ -96,69 +108,65 @@ __device__ __forceinline__ void bitonic_stage(uint64_t (&key)[(P + NT - 1) / NT]
     for (int r = 0; r < E; ++r) {
       if ((r & JR) == 0) {
         const int e = r * NT + tid;
+        const uint64_t a = key[r], b = key[r | JR];
         const bool desc_seg = (e & K) == 0;  // e is the lower index of the pair
-        if (desc_seg ? (key[r | JR] > key[r]) : (key[r | JR] < key[r])) {
-          uint64_t tk = key[r]; key[r] = key[r | JR]; key[r | JR] = tk;
-          int tp = pay[r]; pay[r] = pay[r | JR]; pay[r | JR] = tp;
-        }
+        const bool swap = desc_seg ? (b > a) : (b < a);
+        key[r] = swap ? b : a;
+        key[r | JR] = swap ? a : b;
       }
     }
   } else if constexpr (J >= 32) {  // partner in another warp: through shared memory
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < E; ++r)
-      if (active) { skey[r * NT + tid] = key[r]; spay[r * NT + tid] = pay[r]; }
+      if (active) skey[r * NT + tid] = key[r];
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < E; ++r)
       if (active) {
         const int e = r * NT + tid;
-        bitonic_step<K, J>(key[r], pay[r], skey[e ^ J], spay[e ^ J], e);
+        key[r] = bitonic_pick<K, J>(key[r], skey[e ^ J], e);
       }
   } else if (active) {  // partner in the same warp
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)key[r], J);
       const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(key[r] >> 32), J);
-      const int pp = __shfl_xor_sync(0xffffffffu, pay[r], J);
-      bitonic_step<K, J>(key[r], pay[r], ((uint64_t)hi << 32) | lo, pp, r * NT + tid);
+      key[r] = bitonic_pick<K, J>(key[r], ((uint64_t)hi << 32) | lo, r * NT + tid);
     }
   }
 }
 
 template <int P, int NT, int K, int J>
-__device__ __forceinline__ void bitonic_stages(uint64_t (&key)[(P + NT - 1) / NT], int (&pay)[(P + NT - 1) / NT],
-                                               uint64_t* skey, int* spay) {
-  bitonic_stage<P, NT, K, J>(key, pay, skey, spay);
-  if constexpr (J > 1) bitonic_stages<P, NT, K, J / 2>(key, pay, skey, spay);
-  else if constexpr (K < P) bitonic_stages<P, NT, 2 * K, K>(key, pay, skey, spay);
+__device__ __forceinline__ void bitonic_stages(uint64_t (&key)[(P + NT - 1) / NT], uint64_t* skey) {
+  bitonic_stage<P, NT, K, J>(key, skey);
+  if constexpr (J > 1) bitonic_stages<P, NT, K, J / 2>(key, skey);
+  else if constexpr (K < P) bitonic_stages<P, NT, 2 * K, K>(key, skey);
 }
 
-// Bitonic sort, descending, of cnt <= P (key, payload) pairs held in shared memory (P a power of
-// two >= 32, compile-time: the whole network is unrolled); the result is written back to the
-// first cnt slots, entries past cnt are padded with key 0 (ranks below every real key).  Element
-// e = r * NT + threadIdx.x lives in register r of its thread: strides < 32 are warp shuffles,
-// strides >= NT in-thread, only strides in [32, NT) go through shared memory.  All NT threads call.
+// Bitonic sort, descending, of cnt <= P 64-bit keys held in shared memory (P a power of two >= 32,
+// compile-time: the whole network is unrolled); the result is written back to the first cnt slots,
+// entries past cnt are padded with key 0 (ranks below every real key).  Element e = r*NT + tid
+// lives in register r of its thread: strides < 32 are warp shuffles, strides >= NT in-thread,
+// only strides in [32, NT) go through shared memory.  All NT threads call it.
 template <int P, int NT>
-__device__ void bitonic_desc(uint64_t* skey, int* spay, int cnt) {
+__device__ void bitonic_desc(uint64_t* skey, int cnt) {
   static_assert(P >= 32 && (P & (P - 1)) == 0, "P must be a power of two >= 32");
   constexpr int E = P >= NT ? P / NT : 1;
   const int tid = threadIdx.x;
   const bool active = tid < P;
   uint64_t key[E];
-  int pay[E];
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const int e = r * NT + tid;
     key[r] = (active && e < cnt) ? skey[e] : 0ull;
-    pay[r] = (active && e < cnt) ? spay[e] : 0;
   }
-  bitonic_stages<P, NT, 2, 1>(key, pay, skey, spay);
+  bitonic_stages<P, NT, 2, 1>(key, skey);
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const int e = r * NT + tid;
-    if (active && e < cnt) { skey[e] = key[r]; spay[e] = pay[r]; }
+    if (active && e < cnt) skey[e] = key[r];
   }
   __syncthreads();
 }
@@ -176,7 +184,7 @@ __device__ __forceinline__ int count_greater(const uint64_t* key, int cnt, uint6
 // Runs the tree search of one query block with B_q visible key blocks and writes the n selected
 // blocks (ascending, -1 padded) to out_idx and the count to *out_cnt.  All NT threads call it.
 // Scorer::score(rep, n_rep, rep_s) must fill rep_s[i] = tile score of key block rep[i] and end
-// with a __syncthreads().
+// with a __syncthreads(); Scorer::mark(p) is a profiling hook (no-op in product builds).
 template <int NMAX, int NT, class Scorer>
 __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, int32_t* out_idx, int32_t* out_cnt) {
   constexpr int EMAX = (NMAX + NT - 1) / NT;
@@ -191,7 +199,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
   for (int j = tid; j < n; j += NT) {
     const int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
     const int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
-    st.key[0][j] = make_key(0.f, (int)fj);
+    st.key[0][j] = make_key(0.f, (int)fj, j);
     st.l[0][j] = (int)fj1 - 1;
   }
   __syncthreads();
@@ -232,13 +240,18 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     scorer.mark(0);  // split + scan
     // --- representative scores (Alg. 1 lines 10-13)
     scorer.score(st.rep, boff + nB, st.rep_s);
-    for (int i = tid; i < nB; i += NT) st.bkey[i] = make_key(st.rep_s[boff + i], st.rep[boff + i]);
+    for (int i = tid; i < nB; i += NT) st.bkey[i] = make_key(st.rep_s[boff + i], st.rep[boff + i], i);
     if (first)
-      for (int j = tid; j < n; j += NT) st.key[cur][j] = make_key(st.rep_s[j], st.rep[j]);
+      for (int j = tid; j < n; j += NT) st.key[cur][j] = make_key(st.rep_s[j], st.rep[j], j);
     __syncthreads();
     // --- top-n (Alg. 1 lines 14-15)
-    if (first) bitonic_desc<NMAX, NT>(st.key[cur], st.l[cur], n);
-    bitonic_desc<NMAX, NT>(st.bkey, st.bl, nB);
+    if (first) {  // A is unsorted on the first iteration: sort it, then realign its last blocks
+      bitonic_desc<NMAX, NT>(st.key[cur], n);
+      for (int i = tid; i < n; i += NT) st.ltmp[i] = st.l[cur][key_slot(st.key[cur][i])];
+      __syncthreads();
+      for (int i = tid; i < n; i += NT) st.l[cur][i] = st.ltmp[i];
+    }
+    bitonic_desc<NMAX, NT>(st.bkey, nB);
     scorer.mark(4);  // keys + sorts
     const int nxt = cur ^ 1;
     for (int i = tid; i < n; i += NT) {
@@ -249,7 +262,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     for (int i = tid; i < nB; i += NT) {
       const uint64_t k = st.bkey[i];
       const int r = i + count_greater(st.key[cur], n, k);
-      if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.bl[i]; }
+      if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.bl[key_slot(k)]; }
     }
     __syncthreads();
     scorer.mark(5);  // rank merge
@@ -257,12 +270,9 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     first = false;
   }
   // --- output (Alg. 1 line 17): first blocks of the final single-block nodes, ascending (G18)
-  for (int j = tid; j < n; j += NT) {
-    st.bkey[j] = 0xFFFFFFFFull - (uint32_t)key_first(st.key[cur][j]);  // descending key = ascending block
-    st.bl[j] = 0;
-  }
+  for (int j = tid; j < n; j += NT) st.bkey[j] = 0xFFFFFFFFull - (uint32_t)key_first(st.key[cur][j]);
   __syncthreads();
-  bitonic_desc<NMAX, NT>(st.bkey, st.bl, n);
+  bitonic_desc<NMAX, NT>(st.bkey, n);  // descending key = ascending block
   for (int j = tid; j < n; j += NT) out_idx[j] = (int)(0xFFFFFFFFull - st.bkey[j]);
   if (tid == 0) *out_cnt = n;
   scorer.mark(6);  // output sort
