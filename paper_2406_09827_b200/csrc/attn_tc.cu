@@ -1,40 +1,43 @@
 // attn_tc.cu — block-sparse flash-style attention prefill on tcgen05 (Eq. 2-3, P:116-123;
-// "Block Sparse Flash Attention"), bf16 in/out, fp32 scores/softmax in TMEM/registers.
+// "Block Sparse Flash Attention"), bf16 in/out, fp32 scores / online softmax.
 //
-// Per query block (b_q <= 32 rows) the selected key blocks give <= k = 512 keys (4 tiles of 128).
-// The CTA streams K tiles then V tiles through a 2-slot shared ring (gathered with 16-byte
-// cp.async into 128-byte-swizzled tiles: one key row = 256 B), and one thread issues
-//     S^T_c [128 keys x 32 q] = K_c . Q^T          (M=128, N=32, K=d=128; A K-major, B K-major)
-//     O^T  [128 d    x 32 q] += V_c^T . P_c^T       (M=128, N=32, K=128 keys; A, B MN-major)
-// with all S tiles resident in TMEM (128 columns) and O^T in 32 more.  Softmax is exact two-pass
-// over the on-chip S (the key count per query block is bounded by k, so no rescaling of O is ever
-// needed): each thread owns one key (a TMEM lane) and 32 query columns; row max / row sum over keys
-// are a 5-step shuffle reduce-scatter inside the warp plus a 4-warp exchange in shared memory.
-// P is rounded to bf16 into a no-swizzle MN-major operand tile.  Token-level causal masking and
-// the ragged tails (short last query block, keys past T_k, fewer than n selected blocks) are
-// applied to S before the max.
+// Per query block (b_q <= 32 rows) the selected key blocks give <= k keys, processed in chunks of
+// 128.  Each chunk streams four 16 KB items through a 2-slot shared ring (16-byte cp.async gathers
+// into 128-byte-swizzled layouts): the two d-halves of K_c and the two 64-key halves of V_c.  One
+// thread issues
+//     S^T_c [128 keys x 32 q]  = K_c . Q^T         (M=128, N=32, K=d; A, B K-major)
+//     O^T   [128 d x 32 q]    += V_c^T . P_c^T     (M=128, N=32, K=keys; A, B MN-major)
+// with S^T_c and O^T in 64 TMEM columns.  The softmax is online over chunks (flash style): each
+// thread owns one key (a TMEM lane) and 32 query columns; the row max over keys is a 5-step shuffle
+// reduce-scatter plus a 4-warp exchange.  The running max is updated lazily (only when a chunk's
+// max exceeds it by more than 8 in log2 units, so P <= 2^8 stays exact in bf16 range), and O^T is
+// rescaled in TMEM only then.  P is rounded to bf16 into a no-swizzle MN-major operand tile.
+// Token-level causal masking and the ragged tails (short last query block, keys past T_k, fewer
+// than n selected blocks) are applied to S before the max.  Small CTAs (128 threads, 64 TMEM
+// columns, ~53 KB shared) keep 4 query blocks per SM in flight: the gathers are L2-bound
+// (profiles/r01/gather_ceiling.json), and independent streams are what saturates L2.
 #include "kernels.h"
 
 namespace hip {
 
 constexpr int kATThreads = 128;
-constexpr uint32_t kATRegion = 128 * 128;              // 128 rows x 128 B
-constexpr uint32_t kATTile = 2 * kATRegion;           // d = 128
+constexpr uint32_t kATSlot = 128 * 128;               // one ring slot: 16 KB
 constexpr uint32_t kATQTile = 2 * 32 * 128;
 constexpr uint32_t kATPChunk = 128 * 32 * 2;          // 128 keys x 32 queries bf16
 constexpr uint32_t kIdescQK = idesc_bf16(128, 32, 0, 0);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32, 1, 1);
 constexpr float kATLog2e = 1.4426950408889634f;
 constexpr float kATLn2 = 0.6931471805599453f;
+constexpr float kATRescale = 8.f;                     // lazy rescale threshold (log2 units)
 
 struct AttnTCSmem {
   static constexpr uint32_t q = 0;
-  static constexpr uint32_t ring0 = kATQTile;
-  static constexpr uint32_t ring1 = ring0 + kATTile;
-  static constexpr uint32_t p = ring1 + kATTile;                 // 4 chunks
-  static constexpr uint32_t red = p + 4 * kATPChunk;             // [3][4][32] floats
-  static constexpr uint32_t tok = red + (3 * 4 * 32 + 32) * 4;   // [512] int token per key slot
-  static constexpr uint32_t misc = tok + 512 * 4;
+  static constexpr uint32_t ring = kATQTile;                      // 2 slots
+  static constexpr uint32_t p = ring + 2 * kATSlot;               // one P chunk
+  static constexpr uint32_t red = p + kATPChunk;                  // floats, see below
+  static constexpr int kRedFloats = 3 * 4 * 32 + 6 * 32 + 32;     // [3][4][32] + m, l, lu, corr, invl, pad + flag
+  static constexpr uint32_t tok = red + kRedFloats * 4;           // [512] int token per key slot
+  static constexpr uint32_t misc = (uint32_t)align_up(tok + 512 * 4, 64);
   static constexpr uint32_t total = misc + 64;
 };
 
@@ -55,18 +58,25 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   return v[0];
 }
 
-__global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
-                                                             const int32_t* __restrict__ idx,
-                                                             const int32_t* __restrict__ cnt, float scale_log2,
-                                                             char* __restrict__ o, int64_t osb, int64_t osh,
-                                                             int64_t ost, float* __restrict__ lse) {
+__global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
+                                                                const int32_t* __restrict__ idx,
+                                                                const int32_t* __restrict__ cnt, float scale_log2,
+                                                                char* __restrict__ o, int64_t osb, int64_t osh,
+                                                                int64_t ost, float* __restrict__ lse) {
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sb = raw + pad;
   using L = AttnTCSmem;
-  float* red = reinterpret_cast<float*>(base + L::red);
+  float* red = reinterpret_cast<float*>(base + L::red);   // [0,384): per-warp max / sum / unrounded sum
+  float* mrun = red + 384;                                 // running max per query (log2 units)
+  float* lrun = red + 416;                                 // running sum of bf16-rounded p
+  float* lurun = red + 448;                                // running sum of unrounded p (lse)
+  float* corr = red + 480;                                 // rescale factor of this chunk
+  float* invl = red + 512;
+  int* flag = reinterpret_cast<int*>(red + 576);
+  int* tok = reinterpret_cast<int*>(base + L::tok);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -76,11 +86,11 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
     mbar_init(mbar + 1, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  if (warp == 0) tmem_alloc<64>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot;  // S^T at columns [0, 32), O^T at [32, 64)
   const uint32_t tmem_lane = tmem + ((uint32_t)(32 * warp) << 16);
   uint32_t phase[2] = {0u, 0u};
   const int lbk = 31 - __clz(sh.bk);
@@ -101,10 +111,10 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
     const int32_t* blk = idx + lin * sh.n;
 
     if (nch == 0) {  // no selected block: O = 0, lse = -inf (G13)
-      for (int i = threadIdx.x; i < rows_q * 128; i += kATThreads) {
-        int t = i >> 7, d = i & 127;
-        reinterpret_cast<__nv_bfloat16*>(o)[b * osb + h * osh + ((int64_t)q * sh.bq + t) * ost + d] =
-            __float2bfloat16_rn(0.f);
+      for (int i = threadIdx.x; i < rows_q * 16; i += kATThreads) {
+        const int t = i >> 4, c16 = i & 15;
+        *reinterpret_cast<uint4*>(o + (b * osb + h * osh + ((int64_t)q * sh.bq + t) * ost) * 2 + c16 * 16) =
+            make_uint4(0u, 0u, 0u, 0u);
       }
       if (lse && threadIdx.x < rows_q) lse[((int64_t)b * sh.Hq + h) * sh.Tq + (int64_t)q * sh.bq + threadIdx.x] = -INFINITY;
       continue;
@@ -118,7 +128,6 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
       cp_async16(sb + L::q + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
     }
     // token of every selected key slot (or -1 past T_k / past cnt), staged once per unit
-    int* tok = reinterpret_cast<int*>(base + L::tok);
     for (int k = threadIdx.x; k < nch * 128; k += kATThreads) {
       int s = -1;
       if (k < nkeys) {
@@ -128,33 +137,38 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
       }
       tok[k] = s;
     }
+    if (threadIdx.x < 32) {
+      mrun[threadIdx.x] = -INFINITY;
+      lrun[threadIdx.x] = 0.f;
+      lurun[threadIdx.x] = 0.f;
+    }
     __syncthreads();
     const char* kbase = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
     const char* vbase = vs.base + (b * vs.sb + hk * vs.sh) * (int64_t)vs.esize;
     const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
-    // item i < nch: K tile i; item nch + i: V tile i; slot = i & 1.  16 threads per 256-B row.
-    auto issue = [&](int item) {
-      const bool isv = item >= nch;
-      const int ch = isv ? item - nch : item;
-      const char* g0 = isv ? vbase : kbase;
-      const uint32_t rb = isv ? vrow : krow;
-      const int c16 = threadIdx.x & 15, r0 = threadIdx.x >> 4;  // r0 < 8
-      const uint32_t dst = ((item & 1) ? sb + L::ring1 : sb + L::ring0) + (c16 >> 3) * kATRegion + r0 * 128 +
-                           (((c16 & 7) ^ r0) << 4);
-      const int* tk = tok + ch * 128 + r0;
+
+    // item i: chunk ch = i >> 2; (i & 3) = 0, 1: K_ch d-half 0 / 1; 2, 3: V_ch keys [0,64) / [64,128)
+    auto issue = [&](int i) {
+      const int ch = i >> 2, kind = i & 3;
+      const uint32_t slot = sb + L::ring + (i & 1) * kATSlot;
+      const int c8 = threadIdx.x & 7, r0 = threadIdx.x >> 3;  // r0 < 16
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int s = tk[8 * i];
-        cp_async16(dst + i * 1024, g0 + (uint64_t)(uint32_t)(s >= 0 ? s : 0) * rb + c16 * 16, s >= 0 ? 16u : 0u);
+      for (int j = 0; j < 8; ++j) {
+        const int x = r0 + 16 * j;  // 0..127
+        int r, dh, key;
+        const char* g0;
+        uint32_t rb, dst;
+        if (kind < 2) {  // K: 128 keys x this d-half
+          r = x; dh = kind; key = ch * 128 + r; g0 = kbase; rb = krow;
+          dst = slot + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4);
+        } else {         // V: 64 keys x both d-halves, d-half regions 8 KB apart
+          r = x & 63; dh = x >> 6; key = ch * 128 + (kind - 2) * 64 + r; g0 = vbase; rb = vrow;
+          dst = slot + dh * 8192 + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4);
+        }
+        const int s = tok[key];
+        cp_async16(dst, g0 + (uint64_t)(uint32_t)(s >= 0 ? s : 0) * rb + dh * 128 + c8 * 16, s >= 0 ? 16u : 0u);
       }
     };
-    // token of this thread's key in chunk ch (or -1): used for masking
-    auto key_token = [&](int ch) -> int64_t { return tok[ch * 128 + 32 * warp + lane]; };
-
-    // Items stream through the 2-slot ring: item i < nch is K tile i, item nch + i is V tile i.  The
-    // MMA of an item is issued as soon as its bytes land and waited only to refill its slot with
-    // item + 2, so V0/V1 are already in flight while the softmax runs.
-    const int nitems = 2 * nch;
     bool pend[2] = {false, false};
     auto wait_slot = [&](int sl) {
       if (pend[sl]) {
@@ -163,140 +177,148 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
         pend[sl] = false;
       }
     };
+
+    const int nitems = 4 * nch;
     issue(0);
     cp_async_commit();
-    if (nitems > 1) issue(1);
-    cp_async_commit();
     for (int it = 0; it < nitems; ++it) {
-      if (it + 1 < nitems) cp_async_wait<1>();
-      else cp_async_wait<0>();
+      cp_async_wait<0>();  // item it landed
       fence_proxy_async_smem();
       __syncthreads();
-      const uint32_t tile = (it & 1) ? sb + L::ring1 : sb + L::ring0;
-      if (it < nch) {
-        if (threadIdx.x == 0) {
-          tc_fence_after();
+      // refill the other slot (item it - 1's) with item it + 1 once item it - 1's MMA has read it.
+      // tcgen05 MMAs of one thread complete in order, so this wait also retires every earlier MMA
+      // (S of this chunk before its softmax, and the previous chunk's PV before P is rewritten).
+      wait_slot((it + 1) & 1);
+      if (it + 1 < nitems) issue(it + 1);
+      cp_async_commit();
+      const int ch = it >> 2, kind = it & 3;
+      const uint32_t slot = sb + L::ring + (it & 1) * kATSlot;
+      if (kind == 2) {
+        // ---- online softmax of chunk ch (S^T_ch complete: its last MMA was item it - 1)
+        tc_fence_after();
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_lane, v);
+        const int s = tok[ch * 128 + 32 * warp + lane];
+        const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0);
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            uint64_t a = smem_desc(tile + (s >> 2) * kATRegion + (s & 3) * 32, 16, 1024, kLayoutSw128);
-            uint64_t bq = smem_desc(sb + L::q + (s >> 2) * (32 * 128) + (s & 3) * 32, 16, 1024, kLayoutSw128);
-            umma_bf16(tmem + 32 * it, a, bq, kIdescQK, s > 0 ? 1u : 0u);
-          }
-          umma_commit(mbar + (it & 1));
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = all_vis || (s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j));
+          v[j] = ok ? v[j] * scale_log2 : -INFINITY;
         }
-        pend[it & 1] = true;
-        if (it + 2 < nitems) {  // refill this slot (item it + 2) once its MMA has read it
-          wait_slot(it & 1);
-          issue(it + 2);
-          cp_async_commit();
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = v[j];
+        red[warp * 32 + lane] = reduce_scatter32<true>(v, lane);
+        __syncthreads();
+        if (threadIdx.x < 32) {  // new running max per query (lazy), rescale factor, rescale flag
+          const int j = threadIdx.x;
+          const float mc = fmaxf(fmaxf(red[j], red[32 + j]), fmaxf(red[64 + j], red[96 + j]));
+          const float mo = mrun[j];
+          const float mn = (mc > mo + kATRescale || (mo == -INFINITY && mc != -INFINITY)) ? mc : mo;
+          const float cf = (mn == mo) ? 1.f : (mo == -INFINITY ? 0.f : ex2_approx(mo - mn));
+          corr[j] = cf;
+          mrun[j] = mn;
+          lrun[j] *= cf;
+          lurun[j] *= cf;
+          const unsigned any = __ballot_sync(0xffffffffu, cf != 1.f);
+          if (j == 0) *flag = (any != 0u) && ch > 0;
         }
-        if (it == nch - 1) {
-          // ---- softmax over all S tiles (two passes, S stays in TMEM)
-          wait_slot(0);
-          wait_slot(1);
-          tc_fence_after();
-          float mq;  // running max (log2 domain) of query `lane` over this warp's keys
-          mq = -INFINITY;
-          for (int ch = 0; ch < nch; ++ch) {
-            float v[32];
-            tmem_ld_32x32b_x32(tmem_lane + 32 * ch, v);
-            const int64_t s = key_token(ch);
-            if (s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0)) {  // visible to every row
+        __syncthreads();
+        float lq = 0.f, lu = 0.f;
+        {
+          uint32_t pk[16];
+          float w[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] *= scale_log2;
-            } else {
+          for (int j = 0; j < 32; j += 2) {
+            float p2[2];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const bool ok = s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j);
-                v[j] = ok ? v[j] * scale_log2 : -INFINITY;
-              }
+            for (int e = 0; e < 2; ++e) {
+              const float m = mrun[j + e];
+              p2[e] = (x[j + e] == -INFINITY || m == -INFINITY) ? 0.f : ex2_approx(x[j + e] - m);
             }
-            mq = fmaxf(mq, reduce_scatter32<true>(v, lane));
+            w[j] = p2[0];
+            w[j + 1] = p2[1];
+            __nv_bfloat162 pb = __floats2bfloat162_rn(p2[0], p2[1]);
+            pk[j >> 1] = *reinterpret_cast<uint32_t*>(&pb);
+            const float2 pr = __bfloat1622float2(pb);
+            v[j] = pr.x;
+            v[j + 1] = pr.y;
           }
-          red[warp * 32 + lane] = mq;
-          __syncthreads();
-          float mrow[32];
+          // P^T chunk: MN-major, no swizzle: 8-query piece cp at cp*2048, key group r/8 at (r/8)*128,
+          // key r%8 at 16 B stride.
+          const int r = 32 * warp + lane;
+          char* pc = base + L::p + (r >> 3) * 128 + (r & 7) * 16;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            mrow[j] = fmaxf(fmaxf(red[j], red[32 + j]), fmaxf(red[64 + j], red[96 + j]));
-          float lq = 0.f, lu = 0.f;  // sums of the bf16-rounded p (normalises O) / unrounded p (lse)
-          for (int ch = 0; ch < nch; ++ch) {
-            float v[32], w[32];
-            tmem_ld_32x32b_x32(tmem_lane + 32 * ch, v);
-            const int64_t s = key_token(ch);
-            const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0);  // => every m finite
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              float p2[2];
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int jj = j + e;
-                const bool ok = all_vis || (s >= 0 && jj < rows_q && (!sh.causal || s <= tpos0 + jj) &&
-                                            mrow[jj] != -INFINITY);
-                p2[e] = ok ? ex2_approx(fmaf(v[jj], scale_log2, -mrow[jj])) : 0.f;
-              }
-              w[j] = p2[0];
-              w[j + 1] = p2[1];
-              __nv_bfloat162 pb = __floats2bfloat162_rn(p2[0], p2[1]);
-              pk[j >> 1] = *reinterpret_cast<uint32_t*>(&pb);
-              float2 pr = __bfloat1622float2(pb);
-              v[j] = pr.x;
-              v[j + 1] = pr.y;
-            }
-            // P^T chunk: MN-major, no swizzle: piece (8 queries) cp at cp*2048, key group r/8 at
-            // (r/8)*128, key r%8 at 16 B stride.
-            const int r = 32 * warp + lane;
-            char* pc = base + L::p + ch * kATPChunk + (r >> 3) * 128 + (r & 7) * 16;
-#pragma unroll
-            for (int cp = 0; cp < 4; ++cp)
-              *reinterpret_cast<uint4*>(pc + cp * 2048) = make_uint4(pk[4 * cp], pk[4 * cp + 1], pk[4 * cp + 2], pk[4 * cp + 3]);
-            lq += reduce_scatter32<false>(v, lane);
-            if (lse) lu += reduce_scatter32<false>(w, lane);
-          }
-          red[128 + warp * 32 + lane] = lq;
-          red[256 + warp * 32 + lane] = lu;
-          tc_fence_before();
-          fence_proxy_async_smem();
-          __syncthreads();
+          for (int cp = 0; cp < 4; ++cp)
+            *reinterpret_cast<uint4*>(pc + cp * 2048) =
+                make_uint4(pk[4 * cp], pk[4 * cp + 1], pk[4 * cp + 2], pk[4 * cp + 3]);
+          lq = reduce_scatter32<false>(v, lane);
+          if (lse) lu = reduce_scatter32<false>(w, lane);
         }
-      } else {
-        const int ch = it - nch;
-        if (threadIdx.x == 0) {
-          tc_fence_after();
-          const uint32_t pch = sb + L::p + ch * kATPChunk;
+        red[128 + warp * 32 + lane] = lq;
+        red[256 + warp * 32 + lane] = lu;
+        if (*flag) {  // rescale O^T columns (queries) whose running max moved; all PV MMAs retired
+          float ov[32];
+          tmem_ld_32x32b_x32(tmem_lane + 32, ov);
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {  // 128 keys = 8 x K16
-            uint64_t a = smem_desc(tile + s * 2048, kATRegion, 1024, kLayoutSw128);
-            uint64_t bp = smem_desc(pch + s * 256, 128, 2048, kLayoutNone);
-            umma_bf16(tmem + 128, a, bp, kIdescPV, (ch > 0 || s > 0) ? 1u : 0u);
-          }
-          umma_commit(mbar + (it & 1));
+          for (int j = 0; j < 32; ++j) ov[j] *= corr[j];
+          uint32_t* ou = reinterpret_cast<uint32_t*>(ov);
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+              "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+              "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(tmem_lane + 32),
+              "r"(ou[0]), "r"(ou[1]), "r"(ou[2]), "r"(ou[3]), "r"(ou[4]), "r"(ou[5]), "r"(ou[6]), "r"(ou[7]),
+              "r"(ou[8]), "r"(ou[9]), "r"(ou[10]), "r"(ou[11]), "r"(ou[12]), "r"(ou[13]), "r"(ou[14]), "r"(ou[15]),
+              "r"(ou[16]), "r"(ou[17]), "r"(ou[18]), "r"(ou[19]), "r"(ou[20]), "r"(ou[21]), "r"(ou[22]), "r"(ou[23]),
+              "r"(ou[24]), "r"(ou[25]), "r"(ou[26]), "r"(ou[27]), "r"(ou[28]), "r"(ou[29]), "r"(ou[30]), "r"(ou[31])
+              : "memory");
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         }
-        pend[it & 1] = true;
-        if (it + 2 < nitems) {
-          wait_slot(it & 1);
-          issue(it + 2);
-          cp_async_commit();
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          const int j = threadIdx.x;
+          lrun[j] += red[128 + j] + red[160 + j] + red[192 + j] + red[224 + j];
+          lurun[j] += red[256 + j] + red[288 + j] + red[320 + j] + red[352 + j];
         }
       }
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+        if (kind < 2) {  // S^T_ch (+)= K_ch(d-half) . Q^T(d-half)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const uint64_t a = smem_desc(slot + s * 32, 16, 1024, kLayoutSw128);
+            const uint64_t bq = smem_desc(sb + L::q + kind * (32 * 128) + s * 32, 16, 1024, kLayoutSw128);
+            umma_bf16(tmem, a, bq, kIdescQK, (kind | s) ? 1u : 0u);
+          }
+        } else {         // O^T += V_ch(64 keys)^T . P_ch(those keys)^T
+          const int hk2 = kind - 2;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {  // 64 keys = 4 x K16
+            const uint64_t a = smem_desc(slot + s * 2048, 8192, 1024, kLayoutSw128);
+            const uint64_t bp = smem_desc(sb + L::p + hk2 * 1024 + s * 256, 128, 2048, kLayoutNone);
+            umma_bf16(tmem + 32, a, bp, kIdescPV, (ch > 0 || hk2 > 0 || s > 0) ? 1u : 0u);
+          }
+        }
+        umma_commit(mbar + (it & 1));
+      }
+      pend[it & 1] = true;
     }
     wait_slot(0);  // the last MMAs (O^T complete)
     wait_slot(1);
     // ---- epilogue: O^T lanes = d, columns = queries -> normalise, stage [32 q][128 d] bf16 in the
-    // (now free) P buffer, then 16-byte coalesced row stores
-    float* invl = red + 384;
+    // (now free) ring, then 16-byte coalesced row stores
     if (threadIdx.x < 32) {
       const int j = threadIdx.x;
-      const float l = red[128 + j] + red[160 + j] + red[192 + j] + red[224 + j];
-      invl[j] = l > 0.f ? 1.f / l : 0.f;
+      invl[j] = lrun[j] > 0.f ? 1.f / lrun[j] : 0.f;
     }
     tc_fence_after();
     float v[32];
-    tmem_ld_32x32b_x32(tmem_lane + 128, v);
+    tmem_ld_32x32b_x32(tmem_lane + 32, v);
     __syncthreads();
     const int d = 32 * warp + lane;
-    __nv_bfloat16* ostage = reinterpret_cast<__nv_bfloat16*>(base + L::p);
+    __nv_bfloat16* ostage = reinterpret_cast<__nv_bfloat16*>(base + L::ring);
 #pragma unroll
     for (int j = 0; j < 32; ++j) ostage[j * 128 + d] = __float2bfloat16_rn(v[j] * invl[j]);
     __syncthreads();
@@ -305,13 +327,12 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
       const int p = threadIdx.x + kATThreads * i, j = p >> 4, c16 = p & 15;
       if (j < rows_q) {
         char* dst = o + (b * osb + h * osh + ((int64_t)q * sh.bq + j) * ost) * 2 + c16 * 16;
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(base + L::p + j * 256 + c16 * 16);
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(base + L::ring + j * 256 + c16 * 16);
       }
     }
     if (lse && threadIdx.x < rows_q) {
       const int j = threadIdx.x;
-      const float l = red[256 + j] + red[288 + j] + red[320 + j] + red[352 + j];
-      const float m = fmaxf(fmaxf(red[j], red[32 + j]), fmaxf(red[64 + j], red[96 + j]));
+      const float l = lurun[j], m = mrun[j];
       lse[((int64_t)b * sh.Hq + h) * sh.Tq + (int64_t)q * sh.bq + j] = l > 0.f ? m * kATLn2 + logf(l) : -INFINITY;
     }
     tc_fence_before();
@@ -319,11 +340,12 @@ __global__ void __launch_bounds__(kATThreads) attn_tc_kernel(Shape sh, QSrc qsrc
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<256>(tmem);
+  if (warp == 0) tmem_dealloc<64>(tmem);
 }
 
 bool attn_tc_supported(const Shape& sh) {
-  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 && (int64_t)sh.n * sh.bk <= 512;
+  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 &&
+         (int64_t)sh.n * sh.bk <= 512;
 }
 
 cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
@@ -331,7 +353,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, co
                            float* lse, cudaStream_t stream, int num_sms) {
   const size_t smem = AttnTCSmem::total + 1024;
   int per_sm = 1;
-  cudaError_t e = persistent_ctas(attn_tc_kernel, kATThreads, smem, 256, &per_sm);
+  cudaError_t e = persistent_ctas(attn_tc_kernel, kATThreads, smem, 64, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
