@@ -13,8 +13,8 @@
 // round of up to TT tiles ONE epilogue pass reads the accumulators: each thread of warps 0-3 owns a
 // TMEM lane (one key, 32 query columns), maxes over the valid query rows (a plain 32-way max unless
 // the block touches the causal diagonal), then over the b_k lanes of a block with shuffles -> one
-// fp32 score per representative block.  The selection (split, unrolled register bitonic sort of
-// packed keys, rank merge, tie toward the smaller block) is select.cuh.
+// fp32 score per representative block.  The selection (position-ordered split, radix select of
+// the n best packed keys, tie toward the smaller block, stable compaction) is select.cuh.
 //
 // Why keys on M: b_q = 32 is below the smallest tcgen05 M (64), so the query block is the N=32
 // operand and the gathered keys fill M = 128.  Gathers are 32 FLOP per byte, far below
@@ -40,9 +40,12 @@ struct MaskTCSmemLayout {
   static constexpr uint32_t total = misc + 128;
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged>
+// LAG = 1: item i - 1's slot is refilled after MMA(i) is issued (its MMA is usually done by then),
+// SLOTS - 1 half tiles in flight; LAG = 0: item i's own slot is refilled as soon as MMA(i)
+// completes, SLOTS half tiles in flight at the cost of waiting for each MMA.
+template <int NT, int SLOTS, int TT, int LAG, bool kPaged>
 struct TCScorer {
-  static_assert(SLOTS >= 2 && (SLOTS & (SLOTS - 1)) == 0, "ring of 2^k half-tile slots");
+  static_assert(SLOTS >= 2 && SLOTS <= 8 && (LAG == 0 || LAG == 1), "ring of 2..8 half-tile slots");
   static constexpr int RPT = NT / 8;  // half rows per pass (8 threads per 128-byte half row)
   uint32_t q_s, k_s0;
   uint64_t* mbar;     // [SLOTS], one per ring slot
@@ -68,7 +71,7 @@ struct TCScorer {
     const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
     const int tid = threadIdx.x, c8 = tid & 7, r0 = tid >> 3;
     const int bmask = (1 << lbk) - 1;
-    const uint32_t dst = k_s0 + (i & (SLOTS - 1)) * kKRegion + (r0 >> 3) * 1024 + (r0 & 7) * 128 +
+    const uint32_t dst = k_s0 + (i % SLOTS) * kKRegion + (r0 >> 3) * 1024 + (r0 & 7) * 128 +
                          ((c8 ^ (r0 & 7)) << 4);
 #pragma unroll
     for (int j = 0; j < 128 / RPT; ++j) {
@@ -124,33 +127,33 @@ struct TCScorer {
     const int ntiles = (n_rep + bpt - 1) / bpt;
     for (int c0 = 0; c0 < ntiles; c0 += TT) {  // rounds of up to TT tiles (TMEM columns)
       const int nt = min(TT, ntiles - c0), nitems = 2 * nt;
+      constexpr int P = SLOTS - LAG;  // half tiles in flight
 #pragma unroll
-      for (int i = 0; i < SLOTS - 1; ++i) {  // prologue: SLOTS - 1 half tiles in flight
+      for (int i = 0; i < P; ++i) {  // prologue
         if (i < nitems) issue(rep, n_rep, c0, i);
         cp_async_commit();
       }
       for (int i = 0; i < nitems; ++i) {
-        cp_async_wait<SLOTS - 2>();  // item i landed
+        cp_async_wait<P - 1>();  // item i landed
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0) {
           tc_fence_after();
           const int cc = i >> 1, h = i & 1;
-          const uint32_t kt = k_s0 + (i & (SLOTS - 1)) * kKRegion;
+          const uint32_t kt = k_s0 + (i % SLOTS) * kKRegion;
 #pragma unroll
           for (int s = 0; s < 4; ++s) {  // one d-half = 4 x K16
             uint64_t a = smem_desc(kt + s * 32, 16, 1024, kLayoutSw128);
             uint64_t bq = smem_desc(q_s + h * (32 * 128) + s * 32, 16, 1024, kLayoutSw128);
             umma_bf16(tmem + 32 * cc, a, bq, kIdescS, (h | s) ? 1u : 0u);
           }
-          umma_commit(mbar + (i & (SLOTS - 1)));
+          umma_commit(mbar + (i % SLOTS));
         }
-        pend |= 1u << (i & (SLOTS - 1));
-        // refill the slot of item i - 1 (the oldest one in the ring) with item i + SLOTS - 1 once
-        // item i - 1's MMA has read it
-        if (i + SLOTS - 1 < nitems) {
-          wait_slot((i + SLOTS - 1) & (SLOTS - 1));
-          issue(rep, n_rep, c0, i + SLOTS - 1);
+        pend |= 1u << (i % SLOTS);
+        // refill the slot of item i - LAG with item i - LAG + SLOTS once that item's MMA has read it
+        if (i + P < nitems) {
+          wait_slot((i + P) % SLOTS);
+          issue(rep, n_rep, c0, i + P);
         }
         cp_async_commit();
       }
@@ -167,7 +170,7 @@ struct TCScorer {
   }
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged>
+template <int NT, int SLOTS, int TT, int LAG, bool kPaged>
 __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                               int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
   constexpr uint32_t kCols = 32 * TT;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged> sc;
+    TCScorer<NT, SLOTS, TT, LAG, kPaged> sc;
     sc.q_s = sbase + L::q;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = mbar;
@@ -253,11 +256,11 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int NT, int SLOTS, int TT>
+template <int NT, int SLOTS, int TT, int LAG = 1>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
   const size_t smem = MaskTCSmemLayout<SLOTS>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<NT, SLOTS, TT, true> : mask_tc_kernel<NT, SLOTS, TT, false>;
+  auto kern = ks.paged ? mask_tc_kernel<NT, SLOTS, TT, LAG, true> : mask_tc_kernel<NT, SLOTS, TT, LAG, false>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, NT, smem, 32 * TT, &per_sm);
   if (e != cudaSuccess) return e;
@@ -275,7 +278,10 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
   if (v && !strcmp(v, "256x2x4")) return launch_v<256, 2, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "128x4x4")) return launch_v<128, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "128x2x2")) return launch_v<128, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-  return launch_v<128, 2, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x3x4")) return launch_v<128, 3, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x3x4e")) return launch_v<128, 3, 4, 0>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "128x2x4l")) return launch_v<128, 2, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return launch_v<128, 2, 4, 0>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
 
 #ifdef HIPATTN_PHASES

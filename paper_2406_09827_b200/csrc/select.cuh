@@ -2,23 +2,21 @@
 // (Alg. 1 lines 4-17).  Scoring of the representative key blocks is delegated to a
 // Scorer (CUDA-core sequential fp32 in mask_cc.cu, GEMV in mask_decode.cu, tcgen05 in mask_tc.cu).
 //
-// Ranking key (reading G10): larger score first, equal scores -> smaller first block.
-// It is packed into one 64-bit integer
-//     key = orderable(score) << 32 | (kFirstMax - first) << kSlotBits | slot
-// so ranking is a plain unsigned compare (+0 and -0 normalised to one key; NaN, impossible for
-// finite inputs, mapped to -inf so the order is total).  `slot` is the entry's position in the
-// unsorted array it was built from; first blocks are unique among candidates, so the slot never
-// decides an order — it only lets the sort move 64-bit keys alone (no payload) and the merge find
-// each entry's last block afterwards.
+// The nodes are kept in POSITION order (ascending first block), not in score order.  Splitting a
+// node (f, l) at m = floor((f + l + 1) / 2) (reading G3) gives two adjacent children (f, m - 1) and
+// (m, l), so the children of the position-ordered nodes are again position ordered: one block-wide
+// exclusive scan places them.  The left child keeps its parent's score (same first block => same
+// representative => same score, exact); only the right children are scored (all 2n children on
+// the first iteration, PIN-7).  The n best children are then found by a block-wide
+// radix select over their ranking keys and compacted in place by a second scan, which keeps the
+// position order — so the final nodes are already the ascending block list Alg. 1 line 17 returns
+// (G18) and no sort is ever needed.
 //
-// The n current nodes are kept SORTED by key.  Splitting a node at m = floor((f + l + 1) / 2)
-// (reading G3) gives a left child (f, m - 1) that keeps the node's key (same first block => same
-// representative => same score, exact) and a right child (m, l) that needs a fresh score.  So
-// each iteration the left children form a list A that is already sorted and the right children a
-// list B of <= n fresh keys: B is sorted with a register/shuffle bitonic network (only the strides
-// that cross warps go through shared memory), then A and B are merged by rank (binary search) and
-// the first n kept.  On the first iteration A's scores are fresh too (2n scored
-// blocks, PIN-7) and A is sorted the same way.
+// Ranking key (reading G10): larger score first, equal scores -> smaller first block:
+//     key = orderable(score) << 22 | (kFirstMax - first)
+// a plain unsigned compare (+0 and -0 normalised to one key; NaN, impossible for finite inputs,
+// mapped to -inf so the order is total).  First blocks are unique among candidates, so keys are
+// unique and "the n largest keys" is exactly one set.
 #pragma once
 
 #include "common.cuh"
@@ -27,18 +25,20 @@ namespace hip {
 
 constexpr int kFirstBits = 22;                       // first block < 2^22 (T_k <= 4M * b_k)
 constexpr uint32_t kFirstMax = (1u << kFirstBits) - 1;
+constexpr int kNeedScore = 1 << 30;                  // candidate flag (in its last block): score is rep_s[cs]
 
 template <int NMAX>
 struct SelState {
-  static constexpr int kSlotBits = 32 - kFirstBits;  // 10 bits: NMAX <= 1024
-  static_assert(NMAX <= (1 << kSlotBits), "slot field too small");
-  uint64_t key[2][NMAX];   // nodes, sorted by key (descending)
-  int l[2][NMAX];          // last block of each node, aligned with key
-  uint64_t bkey[NMAX];     // right children (B list)
-  int bl[NMAX];            // their last blocks, indexed by slot
-  int ltmp[NMAX];
-  int rep[2 * NMAX];       // representative blocks to score this iteration
-  float rep_s[2 * NMAX];   // their scores (written by the Scorer)
+  static constexpr int kRep = 2 * NMAX > 512 ? 2 * NMAX : 512;
+  int nf[NMAX], nl[NMAX];            // nodes (first, last block), position order
+  uint32_t ns[NMAX];                 // their orderable scores
+  int cf[2 * NMAX], cl[2 * NMAX];    // candidates (children), position order; cl may carry kNeedScore
+  uint32_t cs[2 * NMAX];             // orderable score, or index into rep_s when kNeedScore
+  int rep[kRep];                     // representative blocks to score; radix histograms after scoring
+  float rep_s[2 * NMAX];             // their scores (written by the Scorer)
+  unsigned long long red[64];        // per-warp OR / AND of the keys
+  unsigned long long rprefix, rmask;
+  int rneed, rdone;
   int warp_tot[32];
   int total;
 };
@@ -49,17 +49,8 @@ __device__ __forceinline__ uint32_t ord_score(float s) {
   uint32_t u = __float_as_uint(s);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
-__device__ __forceinline__ uint64_t make_key(float s, int first, int slot) {
-  constexpr int kSlotBits = 32 - kFirstBits;
-  return ((uint64_t)ord_score(s) << 32) | ((uint32_t)(kFirstMax - (uint32_t)first) << kSlotBits) | (uint32_t)slot;
-}
-__device__ __forceinline__ int key_first(uint64_t k) {
-  constexpr int kSlotBits = 32 - kFirstBits;
-  return (int)(kFirstMax - ((uint32_t)k >> kSlotBits));
-}
-__device__ __forceinline__ int key_slot(uint64_t k) {
-  constexpr int kSlotBits = 32 - kFirstBits;
-  return (int)((uint32_t)k & ((1u << kSlotBits) - 1));
+__device__ __forceinline__ uint64_t make_key(uint32_t ord, int first) {
+  return ((uint64_t)ord << kFirstBits) | (uint64_t)(kFirstMax - (uint32_t)first);
 }
 
 template <int NT>
@@ -89,96 +80,106 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total)
   return base + x - v;
 }
 
-// One compare-exchange of the network: element e against e ^ J inside blocks of K; the pair
-// ends descending inside blocks with (e & K) == 0, ascending otherwise.
-template <int K, int J>
-__device__ __forceinline__ uint64_t bitonic_pick(uint64_t key, uint64_t pk, int e) {
-  const bool want_max = ((e & K) == 0) == ((e & J) == 0);
-  return want_max ? (pk > key ? pk : key) : (pk < key ? pk : key);
-}
-
-template <int P, int NT, int K, int J>
-__device__ __forceinline__ void bitonic_stage(uint64_t (&key)[(P + NT - 1) / NT], uint64_t* skey) {
-  constexpr int E = P >= NT ? P / NT : 1;
-  const int tid = threadIdx.x;
-  const bool active = tid < P;
-  if constexpr (J >= NT) {  // partner in the same thread
-    constexpr int JR = J / NT;
+// Block-wide radix select over unique 64-bit keys, EC per thread (bit k of `valid` marks key[k]):
+// on return exactly the `need` largest valid keys satisfy (key & mask) >= prefix.  Digits of 8 bits
+// starting at the highest bit on which the keys differ; each pass histograms the keys that match
+// the prefix so far (shared atomics), one warp finds the digit where the count from the top reaches
+// `need`, and the search stops as soon as that digit's whole bin is selected.  Requires
+// 1 <= need <= number of valid keys.  hist: 512 ints of scratch (aliases SelState::rep).
+template <int NT, int EC, int NMAX>
+__device__ __forceinline__ void radix_top(const uint64_t (&key)[EC], uint32_t valid, int need, SelState<NMAX>& st,
+                                          uint64_t& prefix, uint64_t& mask) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  int* hist = st.rep;
+  unsigned long long o = 0ull, a = ~0ull;
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-      if ((r & JR) == 0) {
-        const int e = r * NT + tid;
-        const uint64_t a = key[r], b = key[r | JR];
-        const bool desc_seg = (e & K) == 0;  // e is the lower index of the pair
-        const bool swap = desc_seg ? (b > a) : (b < a);
-        key[r] = swap ? b : a;
-        key[r | JR] = swap ? a : b;
-      }
+  for (int k = 0; k < EC; ++k)
+    if (valid & (1u << k)) {
+      o |= key[k];
+      a &= key[k];
     }
-  } else if constexpr (J >= 32) {  // partner in another warp: through shared memory
-    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < E; ++r)
-      if (active) skey[r * NT + tid] = key[r];
-    __syncthreads();
+  for (int w = 16; w >= 1; w >>= 1) {
+    o |= __shfl_xor_sync(0xffffffffu, o, w);
+    a &= __shfl_xor_sync(0xffffffffu, a, w);
+  }
+  if (lane == 0) {
+    st.red[warp] = o;
+    st.red[32 + warp] = a;
+  }
+  for (int i = tid; i < 512; i += NT) hist[i] = 0;
+  __syncthreads();
+  o = 0ull;
+  a = ~0ull;
 #pragma unroll
-    for (int r = 0; r < E; ++r)
-      if (active) {
-        const int e = r * NT + tid;
-        key[r] = bitonic_pick<K, J>(key[r], skey[e ^ J], e);
+  for (int w = 0; w < NW; ++w) {
+    o |= st.red[w];
+    a &= st.red[32 + w];
+  }
+  const uint64_t diff = o ^ a;
+  if (diff == 0ull) {  // a single distinct key
+    prefix = a;
+    mask = ~0ull;
+    return;
+  }
+  const int hb = 63 - __clzll((long long)diff);
+  mask = hb == 63 ? 0ull : (~0ull << (hb + 1));
+  prefix = a & mask;
+  int top = hb;
+  for (int pass = 0;; ++pass) {
+    const int s = top >= 7 ? top - 7 : 0;
+    const uint32_t dmask = (1u << (top - s + 1)) - 1u;
+    int* h = hist + (pass & 1) * 256;
+#pragma unroll
+    for (int k = 0; k < EC; ++k)
+      if ((valid & (1u << k)) && (key[k] & mask) == prefix) atomicAdd(h + (uint32_t)((key[k] >> s) & dmask), 1);
+    __syncthreads();
+    if (warp == 0) {
+      // lane L owns bins [248 - 8L, 255 - 8L], walked from the top
+      const int b0 = 248 - 8 * lane;
+      const int4 v0 = *reinterpret_cast<const int4*>(h + b0);
+      const int4 v1 = *reinterpret_cast<const int4*>(h + b0 + 4);
+      const int c[8] = {v1.w, v1.z, v1.y, v1.x, v0.w, v0.z, v0.y, v0.x};
+      int sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += c[i];
+      int incl = sum;
+#pragma unroll
+      for (int w = 1; w < 32; w <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, w);
+        if (lane >= w) incl += y;
       }
-  } else if (active) {  // partner in the same warp
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
+      if (lane == __ffs(hit) - 1) {
+        int acc = incl - sum, d = -1, cb = 0, above = 0;
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)key[r], J);
-      const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(key[r] >> 32), J);
-      key[r] = bitonic_pick<K, J>(key[r], ((uint64_t)hi << 32) | lo, r * NT + tid);
+        for (int i = 0; i < 8; ++i)
+          if (d < 0) {
+            if (acc + c[i] >= need) {
+              d = b0 + 7 - i;
+              cb = c[i];
+              above = acc;
+            } else {
+              acc += c[i];
+            }
+          }
+        st.rprefix = prefix | ((uint64_t)d << s);
+        st.rmask = mask | ((uint64_t)dmask << s);
+        st.rneed = need - above;
+        st.rdone = (cb == need - above) || s == 0;
+      }
+    } else {
+      int* hn = hist + ((pass + 1) & 1) * 256;  // clear the next pass's histogram
+      for (int i = tid - 32; i < 256; i += NT - 32) hn[i] = 0;
     }
+    __syncthreads();
+    prefix = st.rprefix;
+    mask = st.rmask;
+    need = st.rneed;
+    if (st.rdone) return;
+    top = s - 1;
   }
-}
-
-template <int P, int NT, int K, int J>
-__device__ __forceinline__ void bitonic_stages(uint64_t (&key)[(P + NT - 1) / NT], uint64_t* skey) {
-  bitonic_stage<P, NT, K, J>(key, skey);
-  if constexpr (J > 1) bitonic_stages<P, NT, K, J / 2>(key, skey);
-  else if constexpr (K < P) bitonic_stages<P, NT, 2 * K, K>(key, skey);
-}
-
-// Bitonic sort, descending, of cnt <= P 64-bit keys held in shared memory (P a power of two >= 32,
-// compile-time: the whole network is unrolled); the result is written back to the first cnt slots,
-// entries past cnt are padded with key 0 (ranks below every real key).  Element e = r*NT + tid
-// lives in register r of its thread: strides < 32 are warp shuffles, strides >= NT in-thread,
-// only strides in [32, NT) go through shared memory.  All NT threads call it.
-template <int P, int NT>
-__device__ void bitonic_desc(uint64_t* skey, int cnt) {
-  static_assert(P >= 32 && (P & (P - 1)) == 0, "P must be a power of two >= 32");
-  constexpr int E = P >= NT ? P / NT : 1;
-  const int tid = threadIdx.x;
-  const bool active = tid < P;
-  uint64_t key[E];
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int e = r * NT + tid;
-    key[r] = (active && e < cnt) ? skey[e] : 0ull;
-  }
-  bitonic_stages<P, NT, 2, 1>(key, skey);
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int e = r * NT + tid;
-    if (active && e < cnt) skey[e] = key[r];
-  }
-  __syncthreads();
-}
-
-// Number of entries of the descending list key[0, cnt) strictly greater than x.
-__device__ __forceinline__ int count_greater(const uint64_t* key, int cnt, uint64_t x) {
-  int lo = 0, hi = cnt;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (key[mid] > x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
 }
 
 // Runs the tree search of one query block with B_q visible key blocks and writes the n selected
@@ -187,8 +188,10 @@ __device__ __forceinline__ int count_greater(const uint64_t* key, int cnt, uint6
 // with a __syncthreads(); Scorer::mark(p) is a profiling hook (no-op in product builds).
 template <int NMAX, int NT, class Scorer>
 __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, int32_t* out_idx, int32_t* out_cnt) {
-  constexpr int EMAX = (NMAX + NT - 1) / NT;
-  static_assert(NMAX >= 32 && (NMAX & (NMAX - 1)) == 0, "NMAX must be a power of two >= 32");
+  static_assert(NMAX % NT == 0 || NT % NMAX == 0, "NMAX and NT must nest");
+  constexpr int E = NMAX >= NT ? NMAX / NT : 1;  // nodes per thread (contiguous)
+  constexpr int EC = 2 * E;                      // candidates per thread (contiguous)
+  static_assert(EC <= 32, "valid mask");
   const int tid = threadIdx.x;
   if (Bq <= n) {  // exact case (G1): every visible block
     for (int j = tid; j < n; j += NT) out_idx[j] = j < Bq ? j : -1;
@@ -199,83 +202,101 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
   for (int j = tid; j < n; j += NT) {
     const int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
     const int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
-    st.key[0][j] = make_key(0.f, (int)fj, j);
-    st.l[0][j] = (int)fj1 - 1;
+    st.nf[j] = (int)fj;
+    st.nl[j] = (int)fj1 - 1;
+    st.ns[j] = 0u;
   }
   __syncthreads();
-  constexpr int PER = EMAX;
-  int cur = 0;
   bool first = true;
   // Every iteration at least halves the largest node, so <= 31 iterations end the search; the cap
   // only guards against non-finite inputs.
   for (int iter = 0; iter < 40; ++iter) {
-    // --- branching (Alg. 1 lines 6-9): count the nodes that split, compact the right children
-    const int j0 = tid * PER;
-    int mine = 0;
+    // --- branching (Alg. 1 lines 6-9): place the children of every node by one scan of
+    //     (children count | splits << 16)
+    int f[E], l[E];
+    uint32_t s[E];
+    int packed = 0;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int j = j0 + i;
-      if (j < n && st.l[cur][j] > key_first(st.key[cur][j])) ++mine;
-    }
-    int pos = block_excl_scan<NT>(mine, st.warp_tot, &st.total);
-    const int nB = st.total;
-    if (nB == 0) break;  // every node is a single block (P:155, G5/G6)
-    const int boff = first ? n : 0;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int j = j0 + i;
+    for (int i = 0; i < E; ++i) {
+      const int j = E * tid + i;
       if (j < n) {
-        const int f = key_first(st.key[cur][j]), l = st.l[cur][j];
-        if (l > f) {
-          const int m = (f + l + 1) >> 1;
-          st.bl[pos] = l;
-          st.rep[boff + pos] = m;
-          ++pos;
-          st.l[cur][j] = m - 1;  // left child keeps (score, first)
+        f[i] = st.nf[j];
+        l[i] = st.nl[j];
+        s[i] = st.ns[j];
+        packed += l[i] > f[i] ? 2 + (1 << 16) : 1;
+      }
+    }
+    const int pre = block_excl_scan<NT>(packed, st.warp_tot, &st.total);
+    const int C = st.total & 0xffff, nB = st.total >> 16;
+    if (nB == 0) break;  // every node is a single block (P:155, G5/G6)
+    int p = pre & 0xffff, S = pre >> 16;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int j = E * tid + i;
+      if (j < n) {
+        const bool split = l[i] > f[i];
+        const int m = (f[i] + l[i] + 1) >> 1;
+        st.cf[p] = f[i];
+        st.cl[p] = (split ? m - 1 : l[i]) | (first ? kNeedScore : 0);
+        st.cs[p] = first ? (uint32_t)p : s[i];
+        if (first) st.rep[p] = f[i];
+        if (split) {
+          const int r = first ? p + 1 : S;
+          st.cf[p + 1] = m;
+          st.cl[p + 1] = l[i] | kNeedScore;
+          st.cs[p + 1] = (uint32_t)r;
+          st.rep[r] = m;
+          ++S;
         }
-        if (first) st.rep[j] = f;
+        p += split ? 2 : 1;
       }
     }
     __syncthreads();
     scorer.mark(0);  // split + scan
     // --- representative scores (Alg. 1 lines 10-13)
-    scorer.score(st.rep, boff + nB, st.rep_s);
-    for (int i = tid; i < nB; i += NT) st.bkey[i] = make_key(st.rep_s[boff + i], st.rep[boff + i], i);
-    if (first)
-      for (int j = tid; j < n; j += NT) st.key[cur][j] = make_key(st.rep_s[j], st.rep[j], j);
-    __syncthreads();
+    scorer.score(st.rep, first ? C : nB, st.rep_s);
     // --- top-n (Alg. 1 lines 14-15)
-    if (first) {  // A is unsorted on the first iteration: sort it, then realign its last blocks
-      bitonic_desc<NMAX, NT>(st.key[cur], n);
-      for (int i = tid; i < n; i += NT) st.ltmp[i] = st.l[cur][key_slot(st.key[cur][i])];
-      __syncthreads();
-      for (int i = tid; i < n; i += NT) st.l[cur][i] = st.ltmp[i];
+    uint64_t key[EC];
+    int kf[EC], kl[EC];
+    uint32_t valid = 0;
+#pragma unroll
+    for (int k = 0; k < EC; ++k) {
+      const int c = EC * tid + k;
+      key[k] = 0ull;
+      kf[k] = 0;
+      kl[k] = 0;
+      if (c < C) {
+        const int cl = st.cl[c];
+        const uint32_t cs = st.cs[c];
+        kf[k] = st.cf[c];
+        kl[k] = cl & ~kNeedScore;
+        key[k] = make_key((cl & kNeedScore) ? ord_score(st.rep_s[cs]) : cs, kf[k]);
+        valid |= 1u << k;
+      }
     }
-    bitonic_desc<NMAX, NT>(st.bkey, nB);
-    scorer.mark(4);  // keys + sorts
-    const int nxt = cur ^ 1;
-    for (int i = tid; i < n; i += NT) {
-      const uint64_t k = st.key[cur][i];
-      const int r = i + count_greater(st.bkey, nB, k);
-      if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.l[cur][i]; }
-    }
-    for (int i = tid; i < nB; i += NT) {
-      const uint64_t k = st.bkey[i];
-      const int r = i + count_greater(st.key[cur], n, k);
-      if (r < n) { st.key[nxt][r] = k; st.l[nxt][r] = st.bl[key_slot(k)]; }
-    }
+    uint64_t prefix, mask;
+    radix_top<NT, EC>(key, valid, n, st, prefix, mask);
+    scorer.mark(4);  // keys + radix select
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < EC; ++k) cnt += ((valid >> k) & 1u) && (key[k] & mask) >= prefix;
+    int pos = block_excl_scan<NT>(cnt, st.warp_tot, &st.total);
+#pragma unroll
+    for (int k = 0; k < EC; ++k)
+      if (((valid >> k) & 1u) && (key[k] & mask) >= prefix) {
+        st.nf[pos] = kf[k];
+        st.nl[pos] = kl[k];
+        st.ns[pos] = (uint32_t)(key[k] >> kFirstBits);
+        ++pos;
+      }
     __syncthreads();
-    scorer.mark(5);  // rank merge
-    cur = nxt;
+    scorer.mark(5);  // compaction
     first = false;
   }
-  // --- output (Alg. 1 line 17): first blocks of the final single-block nodes, ascending (G18)
-  for (int j = tid; j < n; j += NT) st.bkey[j] = 0xFFFFFFFFull - (uint32_t)key_first(st.key[cur][j]);
-  __syncthreads();
-  bitonic_desc<NMAX, NT>(st.bkey, n);  // descending key = ascending block
-  for (int j = tid; j < n; j += NT) out_idx[j] = (int)(0xFFFFFFFFull - st.bkey[j]);
+  // --- output (Alg. 1 line 17): first blocks of the final single-block nodes, already ascending (G18)
+  for (int j = tid; j < n; j += NT) out_idx[j] = st.nf[j];
   if (tid == 0) *out_cnt = n;
-  scorer.mark(6);  // output sort
+  scorer.mark(6);  // output
 }
 
 }  // namespace hip
