@@ -4,23 +4,26 @@
 // Block approximation makes every representative score a small dense contraction:
 // the b_q x d query block against the b_k x d rows of each representative key block.  Per iteration
 // the CTA gathers the (up to 2n, then n) representative key blocks of its query block, 128 key rows
-// per tile, straight from L2/HBM into 128-byte-swizzled K-major shared memory (coalesced 16-byte
-// cp.async, 8 threads per 128-byte half row), and one thread issues
+// per tile, straight from L2/HBM into swizzled K-major shared memory (coalesced 16-byte cp.async,
+// KW/8 threads per KW-column row piece, so every warp instruction moves whole 32-byte sectors), and
+// one thread issues
 //     S^T_c [128 keys x 32 queries] = K_tile_c [128 x 128] . Q_block^T   (tcgen05.mma, M=128, N=32)
-// into TMEM columns [32c, 32c+32) as two d-halves (4 x K16 each).  Half tiles stream through a ring
-// of SLOTS 16 KB shared slots: the MMA of a half tile is issued as soon as its bytes land and only
-// waited for when its slot is refilled, so tensor-core latency hides under the gathers.  After each
-// round of up to TT tiles ONE epilogue pass reads the accumulators: each thread of warps 0-3 owns a
-// TMEM lane (one key, 32 query columns), maxes over the valid query rows (a plain 32-way max unless
-// the block touches the causal diagonal), then over the b_k lanes of a block with shuffles -> one
-// fp32 score per representative block.  The selection (position-ordered split, radix select of
-// the n best packed keys, tie toward the smaller block, stable compaction) is select.cuh.
+// into TMEM columns [32c, 32c+32) as 128/KW column pieces ("items", KW/16 x K16 each).  Items
+// stream through a ring of SLOTS shared slots (128 x KW bf16 each; 128-byte swizzle for KW = 64,
+// 64-byte swizzle for KW = 32): the MMA of an item is issued as soon as its bytes land and the slot
+// is refilled as soon as that MMA completes, so SLOTS items are in flight.  After each round of up
+// to TT tiles ONE epilogue pass reads the accumulators: each thread of warps 0-3 owns a TMEM lane
+// (one key, 32 query columns), maxes over the valid query rows (a plain 32-way max unless the block
+// touches the causal diagonal), then over the b_k lanes of a block with shuffles -> one fp32 score
+// per representative block.  The selection (position-ordered split, radix select of the n best
+// packed keys, tie toward the smaller block, stable compaction) is select.cuh.
 //
 // Why keys on M: b_q = 32 is below the smallest tcgen05 M (64), so the query block is the N=32
 // operand and the gathered keys fill M = 128.  Gathers are 32 FLOP per byte, far below
-// the tensor-core ridge.  Random 512-byte gathers from L2 sustain ~16 TB/s on B200 only with many
-// independent streams per SM (profiles/r01/gather_ceiling.json), so the default launch is small
-// CTAs (128 threads, 32 KB ring, 128 TMEM columns) with 4 query blocks in flight per SM.
+// the tensor-core ridge; the kernel is bound by L2 gather latency x concurrency and by the
+// selection's instruction stream, so the launch favours many small CTAs per SM (128 threads).
+// TMA was measured and rejected for these gathers: one {64 x b_k} box per block (the only box shape
+// that lands in a UMMA layout) runs at ~half the cp.async rate (profiles/r01/notes.md).
 #include "kernels.h"
 #include "select.cuh"
 
@@ -28,27 +31,31 @@ namespace hip {
 
 constexpr int kMTNmax = 256;
 constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 rows x 128 B
-constexpr uint32_t kKRegion = 128 * 128;         // 128 rows x 128 B = one half-tile slot
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
-template <int SLOTS>
+template <int SLOTS, int KW>
 struct MaskTCSmemLayout {
+  static constexpr uint32_t slot = 128 * KW * 2;  // one item: 128 rows x KW bf16
   static constexpr uint32_t q = 0;
   static constexpr uint32_t k0 = kQTileBytes;
-  static constexpr uint32_t sel = k0 + SLOTS * kKRegion;
+  static constexpr uint32_t sel = k0 + SLOTS * slot;
   static constexpr uint32_t misc = (uint32_t)align_up(sel + sizeof(SelState<kMTNmax>), 128);  // mbarriers
   static constexpr uint32_t total = misc + 128;
 };
 
-// LAG = 1: item i - 1's slot is refilled after MMA(i) is issued (its MMA is usually done by then),
-// SLOTS - 1 half tiles in flight; LAG = 0: item i's own slot is refilled as soon as MMA(i)
-// completes, SLOTS half tiles in flight at the cost of waiting for each MMA.
-template <int NT, int SLOTS, int TT, int LAG, bool kPaged>
+template <int NT, int SLOTS, int TT, int KW, bool kPaged>
 struct TCScorer {
-  static_assert(SLOTS >= 2 && SLOTS <= 8 && (LAG == 0 || LAG == 1), "ring of 2..8 half-tile slots");
-  static constexpr int RPT = NT / 8;  // half rows per pass (8 threads per 128-byte half row)
+  static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
+  static_assert(KW == 64 || KW == 32, "item width: 64 (SW128) or 32 (SW64) columns");
+  static constexpr int IPT = 128 / KW;        // items per tile
+  static constexpr int TPR = KW / 8;          // threads per row piece (16 B each)
+  static constexpr int RPP = NT / TPR;        // rows per pass
+  static constexpr int RJ = 128 / RPP;        // rows per thread per tile
+  static constexpr uint32_t kSlot = 128 * KW * 2;
+  static constexpr uint32_t kAtom = KW * 16;  // 8-row swizzle atom (bytes) = SBO
+  static constexpr uint32_t kLayout = KW == 64 ? kLayoutSw128 : kLayoutSw64;
   uint32_t q_s, k_s0;
-  uint64_t* mbar;     // [SLOTS], one per ring slot
+  uint64_t* mbar;     // [SLOTS], MMA-completion barrier of each ring slot
   uint32_t* phase;    // [SLOTS]
   uint32_t pend = 0;  // slots whose MMA has been committed but not yet waited
   uint32_t tmem;
@@ -57,6 +64,8 @@ struct TCScorer {
   uint32_t row_bytes;    // contiguous: bytes between key rows
   int b, hk, Tk, lbk, causal, rows_q, bpt;
   int64_t tpos0;
+  const char* rp[RJ];    // this thread's source rows of the tile being issued
+  uint32_t rok;          // bit j: rp[j] is a real row (< T_k, block < n_rep)
   HIP_PT_MEMBER
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
@@ -65,21 +74,34 @@ struct TCScorer {
     else return kh + (uint64_t)(uint32_t)s * row_bytes;
   }
 
-  // Item i of a round = (tile c0 + i/2, d-half i&1): 128 key rows x 128 bytes into slot i % SLOTS.
+  // Byte offset of 16-byte chunk c of row r inside a slot (K-major, KW-column rows, swizzled).
+  static __device__ __forceinline__ uint32_t sw_off(int r, int c) {
+    if constexpr (KW == 64) return sw128_off(r, c);
+    else return (r >> 3) * 512u + (r & 7) * 64u + ((c ^ ((r & 7) >> 1)) << 4);
+  }
+
+  // Item i of a round = (tile c0 + i / IPT, column piece i % IPT) into slot i % SLOTS.  The row
+  // pointers are computed once per tile (at its first piece).
   __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
-    const int c = c0 + (i >> 1), h = i & 1;
-    const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
-    const int tid = threadIdx.x, c8 = tid & 7, r0 = tid >> 3;
-    const int bmask = (1 << lbk) - 1;
-    const uint32_t dst = k_s0 + (i % SLOTS) * kKRegion + (r0 >> 3) * 1024 + (r0 & 7) * 128 +
-                         ((c8 ^ (r0 & 7)) << 4);
+    const int c = c0 + i / IPT, h = i % IPT;
+    const int cq = threadIdx.x % TPR, r0 = threadIdx.x / TPR;
+    if (h == 0) {
+      const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
+      const int bmask = (1 << lbk) - 1;
+      rok = 0;
 #pragma unroll
-    for (int j = 0; j < 128 / RPT; ++j) {
-      const int r = r0 + RPT * j, lb = r >> lbk;
-      const int s = lb < nblk ? (rep[blk0 + lb] << lbk) + (r & bmask) : Tk;
-      const bool ok = s < Tk;
-      cp_async16(dst + j * (RPT / 8) * 1024, row(ok ? s : 0) + h * 128 + c8 * 16, ok ? 16u : 0u);
+      for (int j = 0; j < RJ; ++j) {
+        const int r = r0 + RPP * j, lb = r >> lbk;
+        const int s = lb < nblk ? (rep[blk0 + lb] << lbk) + (r & bmask) : Tk;
+        const bool ok = s < Tk;
+        rp[j] = row(ok ? s : 0) + cq * 16;
+        rok |= (uint32_t)ok << j;
+      }
     }
+    const uint32_t dst = k_s0 + (i % SLOTS) * kSlot + sw_off(r0, cq);
+#pragma unroll
+    for (int j = 0; j < RJ; ++j)  // rows r0 + RPP j share r0's swizzle phase (RPP % 8 == 0)
+      cp_async16(dst + j * (RPP / 8) * kAtom, rp[j] + h * (KW * 2), ((rok >> j) & 1u) ? 16u : 0u);
   }
 
   __device__ __forceinline__ void wait_slot(int slot) {
@@ -126,34 +148,36 @@ struct TCScorer {
   __device__ void score(const int* rep, int n_rep, float* out) {
     const int ntiles = (n_rep + bpt - 1) / bpt;
     for (int c0 = 0; c0 < ntiles; c0 += TT) {  // rounds of up to TT tiles (TMEM columns)
-      const int nt = min(TT, ntiles - c0), nitems = 2 * nt;
-      constexpr int P = SLOTS - LAG;  // half tiles in flight
+      const int nt = min(TT, ntiles - c0), nitems = IPT * nt;
 #pragma unroll
-      for (int i = 0; i < P; ++i) {  // prologue
+      for (int i = 0; i < SLOTS; ++i) {  // prologue: SLOTS items in flight
         if (i < nitems) issue(rep, n_rep, c0, i);
         cp_async_commit();
       }
       for (int i = 0; i < nitems; ++i) {
-        cp_async_wait<P - 1>();  // item i landed
+        cp_async_wait<SLOTS - 1>();  // item i landed
         fence_proxy_async_smem();
         __syncthreads();
+        const int slot = i % SLOTS;
         if (threadIdx.x == 0) {
           tc_fence_after();
-          const int cc = i >> 1, h = i & 1;
-          const uint32_t kt = k_s0 + (i % SLOTS) * kKRegion;
+          const int cc = i / IPT, h = i % IPT;
+          const uint32_t kt = k_s0 + slot * kSlot;
+          // Q columns [h*KW, h*KW + KW): SW128 region h*KW/64, byte offset (h*KW % 64) * 2 in the row
+          const uint32_t qb = q_s + (h * KW / 64) * (32 * 128) + (h * KW % 64) * 2;
 #pragma unroll
-          for (int s = 0; s < 4; ++s) {  // one d-half = 4 x K16
-            uint64_t a = smem_desc(kt + s * 32, 16, 1024, kLayoutSw128);
-            uint64_t bq = smem_desc(q_s + h * (32 * 128) + s * 32, 16, 1024, kLayoutSw128);
+          for (int s = 0; s < KW / 16; ++s) {
+            uint64_t a = smem_desc(kt + s * 32, 16, kAtom, kLayout);
+            uint64_t bq = smem_desc(qb + s * 32, 16, 1024, kLayoutSw128);
             umma_bf16(tmem + 32 * cc, a, bq, kIdescS, (h | s) ? 1u : 0u);
           }
-          umma_commit(mbar + (i % SLOTS));
+          umma_commit(mbar + slot);
         }
-        pend |= 1u << (i % SLOTS);
-        // refill the slot of item i - LAG with item i - LAG + SLOTS once that item's MMA has read it
-        if (i + P < nitems) {
-          wait_slot((i + P) % SLOTS);
-          issue(rep, n_rep, c0, i + P);
+        pend |= 1u << slot;
+        // refill this slot with item i + SLOTS as soon as MMA(i) has read it
+        if (i + SLOTS < nitems) {
+          wait_slot(slot);
+          issue(rep, n_rep, c0, i + SLOTS);
         }
         cp_async_commit();
       }
@@ -170,16 +194,16 @@ struct TCScorer {
   }
 };
 
-template <int NT, int SLOTS, int TT, int LAG, bool kPaged>
-__global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
-                                                              int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+template <int NT, int SLOTS, int TT, int KW, bool kPaged, int MINB>
+__global__ void __launch_bounds__(NT, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
+                                                          int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
   constexpr uint32_t kCols = 32 * TT;
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<SLOTS>;
+  using L = MaskTCSmemLayout<SLOTS, KW>;
   SelState<kMTNmax>& st = *reinterpret_cast<SelState<kMTNmax>*>(base + L::sel);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
@@ -212,7 +236,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
     const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
     if (Bq > sh.n) {
-      // query block -> K-major SW128 tile (B operand, N = 32 rows, rows >= rows_q zero)
+      // query block -> K-major SW128 tile (B operand, N = 32 rows, rows >= rows_q zero); waited for
+      // together with the first item of the first round
       for (int p = threadIdx.x; p < 32 * 16; p += NT) {
         const int r = p >> 4, c16 = p & 15;
         const bool ok = r < rows_q;
@@ -221,7 +246,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mask_tc_kernel(Shape sh, QSrc qs
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, LAG, kPaged> sc;
+    TCScorer<NT, SLOTS, TT, KW, kPaged> sc;
     sc.q_s = sbase + L::q;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = mbar;
@@ -256,11 +281,11 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int NT, int SLOTS, int TT, int LAG = 1>
+template <int NT, int SLOTS, int TT, int KW, int MINB>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
-  const size_t smem = MaskTCSmemLayout<SLOTS>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<NT, SLOTS, TT, LAG, true> : mask_tc_kernel<NT, SLOTS, TT, LAG, false>;
+  const size_t smem = MaskTCSmemLayout<SLOTS, KW>::total + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<NT, SLOTS, TT, KW, true, MINB> : mask_tc_kernel<NT, SLOTS, TT, KW, false, MINB>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, NT, smem, 32 * TT, &per_sm);
   if (e != cudaSuccess) return e;
@@ -272,16 +297,13 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
-  // HIPATTN_MASK_TC=<threads>x<slots>x<tiles> selects a variant (tuning aid, profiles/r01).
+  // HIPATTN_MASK_TC=<KW>x<SLOTS>[bM] selects a variant (tuning aid, profiles/r01).
   const char* v = getenv("HIPATTN_MASK_TC");
-  if (v && !strcmp(v, "256x4x8")) return launch_v<256, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "256x2x4")) return launch_v<256, 2, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x4x4")) return launch_v<128, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x2x2")) return launch_v<128, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x3x4")) return launch_v<128, 3, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x3x4e")) return launch_v<128, 3, 4, 0>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "128x2x4l")) return launch_v<128, 2, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
-  return launch_v<128, 2, 4, 0>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "32x2b5")) return launch_v<128, 2, 4, 32, 5>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "32x2b6")) return launch_v<128, 2, 2, 32, 6>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "32x3")) return launch_v<128, 3, 4, 32, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "32x4")) return launch_v<128, 4, 4, 32, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return launch_v<128, 2, 4, 64, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
 
 #ifdef HIPATTN_PHASES
