@@ -282,6 +282,16 @@ def dense_ms(Q, K, V, reps=3):
     return t0.elapsed_time(t1) / reps
 
 
+def l2_gather_peak() -> float:
+    """Best measured random 512-byte L2->SMEM gather rate (GB/s) on this B200 pool
+    (profiles/gather_bench.py); 16500 if the committed measurement is missing."""
+    try:
+        rows = json.load(open(os.path.join(ROOT, "profiles", "r01", "gather_ceiling.json")))
+        return max(r["gbs"] for r in rows if r["source_mb"] <= 32)
+    except (OSError, ValueError, KeyError):
+        return 16500.0
+
+
 def roofline_obj(cfg, heads, mask_ms, attn_ms, pk, traffic=None):
     w = work_model(cfg, heads)
     dom = "mask_estimate" if mask_ms >= attn_ms else "sparse_attention_prefill"
@@ -293,6 +303,8 @@ def roofline_obj(cfg, heads, mask_ms, attn_ms, pk, traffic=None):
             "unit": "TFLOP/s", "frac": round(ach / pk["bf16_tflops"], 4), "traffic": traffic,
             "peak_source": pk["source"],
             "gather": {"achieved_gbs": round(gbytes / t / 1e9, 1), "bytes_per_launch": gbytes,
+                       "peak_gbs": l2_gather_peak(), "frac": round(gbytes / t / 1e9 / l2_gather_peak(), 4),
+                       "peak_source": "measured L2 random 512-B gather ceiling, profiles/r01/gather_ceiling.json",
                        "note": "algorithmic L2->SM gather of representative / selected key blocks; the "
                                "kernel's real bound (32 FLOP per gathered byte, DESIGN.md)"},
             "flops_per_launch": flops}
