@@ -25,22 +25,16 @@ namespace hip {
 
 constexpr int kFirstBits = 22;                       // first block < 2^22 (T_k <= 4M * b_k)
 constexpr uint32_t kFirstMax = (1u << kFirstBits) - 1;
-constexpr int kNeedScore = 1 << 30;                  // candidate flag (in its last block): score is rep_s[cs]
 
 template <int NMAX>
 struct SelState {
-  static constexpr int kRep = 2 * NMAX > 512 ? 2 * NMAX : 512;
+  static constexpr int kRep = 2 * NMAX > 768 ? 2 * NMAX : 768;
   int nf[NMAX], nl[NMAX];            // nodes (first, last block), position order
   uint32_t ns[NMAX];                 // their orderable scores
-  int cf[2 * NMAX], cl[2 * NMAX];    // candidates (children), position order; cl may carry kNeedScore
-  uint32_t cs[2 * NMAX];             // orderable score, or index into rep_s when kNeedScore
-  int rep[kRep];                     // representative blocks to score; radix histograms after scoring
+  int rep[kRep];                     // representative blocks to score; 3 radix histograms after scoring
   float rep_s[2 * NMAX];             // their scores (written by the Scorer)
   unsigned long long red[64];        // per-warp OR / AND of the keys
-  unsigned long long rprefix, rmask;
-  int rneed, rdone;
   int warp_tot[32];
-  int total;
 };
 
 __device__ __forceinline__ uint32_t ord_score(float s) {
@@ -53,8 +47,12 @@ __device__ __forceinline__ uint64_t make_key(uint32_t ord, int first) {
   return ((uint64_t)ord << kFirstBits) | (uint64_t)(kFirstMax - (uint32_t)first);
 }
 
+// Block-wide exclusive scan of one int per thread, ONE barrier: every warp scans itself, publishes
+// its total, and after the barrier each thread adds the totals of the warps before it (and of all
+// warps for *total).  The caller must separate two uses of warp_tot by a barrier.
 template <int NT>
-__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total) {
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
@@ -64,54 +62,52 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total)
   }
   if (lane == 31) warp_tot[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    constexpr int NW = NT / 32;
-    int t = lane < NW ? warp_tot[lane] : 0;
+  int base = 0, tot = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < NW) warp_tot[lane] = t;  // inclusive
-    if (lane == NW - 1) *total = t;
+  for (int w = 0; w < NW; ++w) {
+    const int t = warp_tot[w];
+    base += w < warp ? t : 0;
+    tot += t;
   }
-  __syncthreads();
-  int base = warp ? warp_tot[warp - 1] : 0;
+  total = tot;
   return base + x - v;
 }
 
 // Block-wide radix select over unique 64-bit keys, EC per thread (bit k of `valid` marks key[k]):
 // on return exactly the `need` largest valid keys satisfy (key & mask) >= prefix.  Digits of 8 bits
 // starting at the highest bit on which the keys differ; each pass histograms the keys that match
-// the prefix so far (shared atomics), one warp finds the digit where the count from the top reaches
-// `need`, and the search stops as soon as that digit's whole bin is selected.  Requires
-// 1 <= need <= number of valid keys.  hist: 512 ints of scratch (aliases SelState::rep).
+// the prefix so far (shared atomics), then EVERY warp scans the histogram for the digit where the
+// count from the top reaches `need` (redundantly, so the result needs no second barrier), and the
+// search stops as soon as that digit's whole bin is selected.  Three histograms rotate so one
+// barrier per pass suffices: pass p fills H[p % 3] and clears H[(p + 2) % 3], whose last readers
+// (pass p - 1's scans) are behind pass p's barrier.  Requires 1 <= need <= number of valid keys.
+// Returns the number of histogram passes.
 template <int NT, int EC, int NMAX>
-__device__ __forceinline__ void radix_top(const uint64_t (&key)[EC], uint32_t valid, int need, SelState<NMAX>& st,
-                                          uint64_t& prefix, uint64_t& mask) {
+__device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t valid, int need, SelState<NMAX>& st,
+                                         uint64_t& prefix, uint64_t& mask) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   int* hist = st.rep;
-  unsigned long long o = 0ull, a = ~0ull;
+  uint32_t olo = 0u, ohi = 0u, alo = ~0u, ahi = ~0u;
 #pragma unroll
   for (int k = 0; k < EC; ++k)
     if (valid & (1u << k)) {
-      o |= key[k];
-      a &= key[k];
+      olo |= (uint32_t)key[k];
+      ohi |= (uint32_t)(key[k] >> 32);
+      alo &= (uint32_t)key[k];
+      ahi &= (uint32_t)(key[k] >> 32);
     }
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    o |= __shfl_xor_sync(0xffffffffu, o, w);
-    a &= __shfl_xor_sync(0xffffffffu, a, w);
-  }
+  olo = __reduce_or_sync(0xffffffffu, olo);
+  ohi = __reduce_or_sync(0xffffffffu, ohi);
+  alo = __reduce_and_sync(0xffffffffu, alo);
+  ahi = __reduce_and_sync(0xffffffffu, ahi);
   if (lane == 0) {
-    st.red[warp] = o;
-    st.red[32 + warp] = a;
+    st.red[warp] = ((uint64_t)ohi << 32) | olo;
+    st.red[32 + warp] = ((uint64_t)ahi << 32) | alo;
   }
-  for (int i = tid; i < 512; i += NT) hist[i] = 0;
+  for (int i = tid; i < 512; i += NT) hist[i] = 0;  // H[0], H[1]
   __syncthreads();
-  o = 0ull;
-  a = ~0ull;
+  uint64_t o = 0ull, a = ~0ull;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     o |= st.red[w];
@@ -121,7 +117,7 @@ __device__ __forceinline__ void radix_top(const uint64_t (&key)[EC], uint32_t va
   if (diff == 0ull) {  // a single distinct key
     prefix = a;
     mask = ~0ull;
-    return;
+    return 0;
   }
   const int hb = 63 - __clzll((long long)diff);
   mask = hb == 63 ? 0ull : (~0ull << (hb + 1));
@@ -130,54 +126,50 @@ __device__ __forceinline__ void radix_top(const uint64_t (&key)[EC], uint32_t va
   for (int pass = 0;; ++pass) {
     const int s = top >= 7 ? top - 7 : 0;
     const uint32_t dmask = (1u << (top - s + 1)) - 1u;
-    int* h = hist + (pass & 1) * 256;
+    int* h = hist + (pass % 3) * 256;
 #pragma unroll
     for (int k = 0; k < EC; ++k)
       if ((valid & (1u << k)) && (key[k] & mask) == prefix) atomicAdd(h + (uint32_t)((key[k] >> s) & dmask), 1);
     __syncthreads();
-    if (warp == 0) {
-      // lane L owns bins [248 - 8L, 255 - 8L], walked from the top
-      const int b0 = 248 - 8 * lane;
-      const int4 v0 = *reinterpret_cast<const int4*>(h + b0);
-      const int4 v1 = *reinterpret_cast<const int4*>(h + b0 + 4);
-      const int c[8] = {v1.w, v1.z, v1.y, v1.x, v0.w, v0.z, v0.y, v0.x};
-      int sum = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) sum += c[i];
-      int incl = sum;
-#pragma unroll
-      for (int w = 1; w < 32; w <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, w);
-        if (lane >= w) incl += y;
-      }
-      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
-      if (lane == __ffs(hit) - 1) {
-        int acc = incl - sum, d = -1, cb = 0, above = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (d < 0) {
-            if (acc + c[i] >= need) {
-              d = b0 + 7 - i;
-              cb = c[i];
-              above = acc;
-            } else {
-              acc += c[i];
-            }
-          }
-        st.rprefix = prefix | ((uint64_t)d << s);
-        st.rmask = mask | ((uint64_t)dmask << s);
-        st.rneed = need - above;
-        st.rdone = (cb == need - above) || s == 0;
-      }
-    } else {
-      int* hn = hist + ((pass + 1) & 1) * 256;  // clear the next pass's histogram
-      for (int i = tid - 32; i < 256; i += NT - 32) hn[i] = 0;
+    {
+      int* hz = hist + ((pass + 2) % 3) * 256;  // clear the histogram of pass + 2
+      for (int i = tid; i < 256; i += NT) hz[i] = 0;
     }
-    __syncthreads();
-    prefix = st.rprefix;
-    mask = st.rmask;
-    need = st.rneed;
-    if (st.rdone) return;
+    // lane L owns bins [248 - 8L, 255 - 8L], walked from the top (every warp, same result)
+    const int b0 = 248 - 8 * lane;
+    const int4 v0 = *reinterpret_cast<const int4*>(h + b0);
+    const int4 v1 = *reinterpret_cast<const int4*>(h + b0 + 4);
+    const int c[8] = {v1.w, v1.z, v1.y, v1.x, v0.w, v0.z, v0.y, v0.x};
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += c[i];
+    int incl = sum;
+#pragma unroll
+    for (int w = 1; w < 32; w <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, w);
+      if (lane >= w) incl += y;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
+    const int fl = __ffs(hit) - 1;
+    int acc = incl - sum, d = -1, cb = 0, above = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (d < 0) {
+        if (acc + c[i] >= need) {
+          d = b0 + 7 - i;
+          cb = c[i];
+          above = acc;
+        } else {
+          acc += c[i];
+        }
+      }
+    d = __shfl_sync(0xffffffffu, d, fl);
+    cb = __shfl_sync(0xffffffffu, cb, fl);
+    above = __shfl_sync(0xffffffffu, above, fl);
+    prefix |= (uint64_t)d << s;
+    mask |= (uint64_t)dmask << s;
+    need -= above;
+    if (cb == need || s == 0) return pass + 1;
     top = s - 1;
   }
 }
@@ -190,7 +182,7 @@ template <int NMAX, int NT, class Scorer>
 __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, int32_t* out_idx, int32_t* out_cnt) {
   static_assert(NMAX % NT == 0 || NT % NMAX == 0, "NMAX and NT must nest");
   constexpr int E = NMAX >= NT ? NMAX / NT : 1;  // nodes per thread (contiguous)
-  constexpr int EC = 2 * E;                      // candidates per thread (contiguous)
+  constexpr int EC = 2 * E;                      // candidates per thread (their children)
   static_assert(EC <= 32, "valid mask");
   const int tid = threadIdx.x;
   if (Bq <= n) {  // exact case (G1): every visible block
@@ -226,26 +218,42 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
         packed += l[i] > f[i] ? 2 + (1 << 16) : 1;
       }
     }
-    const int pre = block_excl_scan<NT>(packed, st.warp_tot, &st.total);
-    const int C = st.total & 0xffff, nB = st.total >> 16;
+    int tot;
+    const int pre = block_excl_scan<NT>(packed, st.warp_tot, tot);
+    const int C = tot & 0xffff, nB = tot >> 16;
     if (nB == 0) break;  // every node is a single block (G5/G6)
+    // This thread's children stay in registers: candidate 2i = left child (or the unsplit node),
+    // 2i + 1 = right child of node i.  Those needing a score get a unique slot r in the rep list:
+    // the candidate position on the first iteration (all 2n scored), the split rank afterwards.
     int p = pre & 0xffff, S = pre >> 16;
+    int kf[EC], kl[EC], kr[EC];  // first, last, rep slot (-1: inherited score in ks)
+    uint32_t ks[EC];
+    uint32_t valid = 0;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int j = E * tid + i;
+      kf[2 * i] = kf[2 * i + 1] = 0;
+      kl[2 * i] = kl[2 * i + 1] = 0;
+      kr[2 * i] = kr[2 * i + 1] = -1;
+      ks[2 * i] = ks[2 * i + 1] = 0u;
       if (j < n) {
         const bool split = l[i] > f[i];
         const int m = (f[i] + l[i] + 1) >> 1;
-        st.cf[p] = f[i];
-        st.cl[p] = (split ? m - 1 : l[i]) | (first ? kNeedScore : 0);
-        st.cs[p] = first ? (uint32_t)p : s[i];
-        if (first) st.rep[p] = f[i];
+        kf[2 * i] = f[i];
+        kl[2 * i] = split ? m - 1 : l[i];
+        ks[2 * i] = s[i];
+        valid |= 1u << (2 * i);
+        if (first) {
+          kr[2 * i] = p;
+          st.rep[p] = f[i];
+        }
         if (split) {
           const int r = first ? p + 1 : S;
-          st.cf[p + 1] = m;
-          st.cl[p + 1] = l[i] | kNeedScore;
-          st.cs[p + 1] = (uint32_t)r;
+          kf[2 * i + 1] = m;
+          kl[2 * i + 1] = l[i];
+          kr[2 * i + 1] = r;
           st.rep[r] = m;
+          valid |= 1u << (2 * i + 1);
           ++S;
         }
         p += split ? 2 : 1;
@@ -257,30 +265,26 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     scorer.score(st.rep, first ? C : nB, st.rep_s);
     // --- top-n (Alg. 1 lines 14-15)
     uint64_t key[EC];
-    int kf[EC], kl[EC];
-    uint32_t valid = 0;
 #pragma unroll
-    for (int k = 0; k < EC; ++k) {
-      const int c = EC * tid + k;
-      key[k] = 0ull;
-      kf[k] = 0;
-      kl[k] = 0;
-      if (c < C) {
-        const int cl = st.cl[c];
-        const uint32_t cs = st.cs[c];
-        kf[k] = st.cf[c];
-        kl[k] = cl & ~kNeedScore;
-        key[k] = make_key((cl & kNeedScore) ? ord_score(st.rep_s[cs]) : cs, kf[k]);
-        valid |= 1u << k;
-      }
-    }
+    for (int k = 0; k < EC; ++k)
+      key[k] = make_key(kr[k] >= 0 ? ord_score(st.rep_s[kr[k]]) : ks[k], kf[k]);
     uint64_t prefix, mask;
-    radix_top<NT, EC>(key, valid, n, st, prefix, mask);
-    scorer.mark(4);  // keys + radix select
+    scorer.mark(8);  // keys
+    const int passes = radix_top<NT, EC>(key, valid, n, st, prefix, mask);
+    scorer.mark(4);  // radix select
+#ifdef HIPATTN_PHASES
+    if (tid == 0) {
+      atomicAdd(&g_phase_cycles[9], (unsigned long long)passes);
+      atomicAdd(&g_phase_cycles[10], 1ull);
+    }
+#else
+    (void)passes;
+#endif
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < EC; ++k) cnt += ((valid >> k) & 1u) && (key[k] & mask) >= prefix;
-    int pos = block_excl_scan<NT>(cnt, st.warp_tot, &st.total);
+    int ctot;
+    int pos = block_excl_scan<NT>(cnt, st.warp_tot, ctot);
 #pragma unroll
     for (int k = 0; k < EC; ++k)
       if (((valid >> k) & 1u) && (key[k] & mask) >= prefix) {

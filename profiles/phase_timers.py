@@ -9,8 +9,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-PHASES = ["split+scan", "gather issue+wait", "MMA", "epilogue", "keys+sort", "rank merge", "output sort",
-          "unit setup"]
+PHASES = ["split+scan", "gather+MMA issue", "MMA drain", "epilogue", "radix select", "compaction",
+          "output", "unit setup", "keys"]
 
 
 def build():
@@ -39,9 +39,11 @@ def main():
     fn(buf)
     H.mask_estimate(Q, K)
     fn(buf)
-    tot = sum(buf[i] for i in range(8))
+    tot = sum(buf[i] for i in range(9))
     for i, nm in enumerate(PHASES):
         print(f"{nm:22s} {100 * buf[i] / tot:5.1f}%   {buf[i] / 1e9:8.3f} Gcyc")
+    if buf[10]:
+        print(f"radix passes per select: {buf[9] / buf[10]:.2f} over {buf[10]} selections")
 
 
 if __name__ == "__main__":
