@@ -3,27 +3,35 @@
 //
 // Block approximation makes every representative score a small dense contraction:
 // the b_q x d query block against the b_k x d rows of each representative key block.  Per iteration
-// the CTA gathers the (up to 2n, then n) representative key blocks of its query block, 128 key rows
-// per tile, straight from L2/HBM into swizzled K-major shared memory (coalesced 16-byte cp.async,
-// KW/8 threads per KW-column row piece, so every warp instruction moves whole 32-byte sectors), and
-// one thread issues
+// a team of 128 threads gathers the (up to 2n, then n) representative key blocks of its query block,
+// 128 key rows per tile, straight from L2/HBM into 128-byte-swizzled K-major shared memory
+// (coalesced 16-byte cp.async, 8 threads per 128-byte half row, so every warp instruction moves
+// whole 32-byte sectors), and one thread issues
 //     S^T_c [128 keys x 32 queries] = K_tile_c [128 x 128] . Q_block^T   (tcgen05.mma, M=128, N=32)
-// into TMEM columns [32c, 32c+32) as 128/KW column pieces ("items", KW/16 x K16 each).  Items
-// stream through a ring of SLOTS shared slots (128 x KW bf16 each; 128-byte swizzle for KW = 64,
-// 64-byte swizzle for KW = 32): the MMA of an item is issued as soon as its bytes land and the slot
-// is refilled as soon as that MMA completes, so SLOTS items are in flight.  After each round of up
-// to TT tiles ONE epilogue pass reads the accumulators: each thread of warps 0-3 owns a TMEM lane
-// (one key, 32 query columns), maxes over the valid query rows (a plain 32-way max unless the block
-// touches the causal diagonal), then over the b_k lanes of a block with shuffles -> one fp32 score
-// per representative block.  The selection (position-ordered split, radix select of the n best
-// packed keys, tie toward the smaller block, stable compaction) is select.cuh.
+// into TMEM columns [32c, 32c+32) as two d-halves ("items", 4 x K16 each).  Items stream through a
+// ring of SLOTS 16 KB shared slots: the MMA of an item is issued as soon as its bytes land and the
+// slot is refilled as soon as that MMA completes, so SLOTS items are in flight.  After each round
+// of up to TT tiles ONE epilogue pass reads the accumulators: each thread owns a TMEM lane (one key,
+// 32 query columns), maxes over the valid query rows (a plain 32-way max unless the block touches
+// the causal diagonal), then over the b_k lanes of a block with shuffles -> one fp32 score per
+// representative block.  The selection (position-ordered split, radix select of the n best packed
+// keys, tie toward the smaller block, stable compaction) is select.cuh.
 //
 // Why keys on M: b_q = 32 is below the smallest tcgen05 M (64), so the query block is the N=32
 // operand and the gathered keys fill M = 128.  Gathers are 32 FLOP per byte, far below
-// the tensor-core ridge; the kernel is bound by L2 gather latency x concurrency and by the
-// selection's instruction stream, so the launch favours many small CTAs per SM (128 threads).
+// the tensor-core ridge; the kernel is bound by L2 gather latency (~1.2 us loaded, so ~128 KB must
+// be in flight per SM for the ~15 TB/s L2 gather ceiling) and by the selection's serial chain.
+//
+// Two launch shapes:
+//  * TEAMS = 1: one unit per 128-thread CTA, private 2-slot ring, 4 CTAs per SM.
+//  * TEAMS = 2 ("ping-pong"): a 256-thread CTA runs two units side by side, one per 128-thread team
+//    (named barriers), sharing ONE ring of SLOTS slots under a lock: a team holds the ring only while
+//    it gathers and scores, so while one team selects the other gathers with the whole ring — twice
+//    the bytes in flight per gathering unit at the same shared memory per SM.
 // TMA was measured and rejected for these gathers: one {64 x b_k} box per block (the only box shape
 // that lands in a UMMA layout) runs at ~half the cp.async rate (profiles/r01/notes.md).
+#include <type_traits>
+
 #include "kernels.h"
 #include "select.cuh"
 
@@ -31,34 +39,36 @@ namespace hip {
 
 constexpr int kMTNmax = 256;
 constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 rows x 128 B
+constexpr uint32_t kMTSlot = 128 * 128;          // one item: 128 rows x 64 bf16
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
-template <int SLOTS, int KW>
+template <int SLOTS, int TEAMS>
 struct MaskTCSmemLayout {
-  static constexpr uint32_t slot = 128 * KW * 2;  // one item: 128 rows x KW bf16
-  static constexpr uint32_t q = 0;
-  static constexpr uint32_t k0 = kQTileBytes;
-  static constexpr uint32_t sel = k0 + SLOTS * slot;
-  static constexpr uint32_t misc = (uint32_t)align_up(sel + sizeof(SelState<kMTNmax>), 128);  // mbarriers
+  static constexpr uint32_t k0 = 0;                                        // ring (1024-aligned)
+  static constexpr uint32_t q = k0 + SLOTS * kMTSlot;                      // [TEAMS] Q tiles
+  static constexpr uint32_t sel = q + TEAMS * kQTileBytes;                 // [TEAMS] SelState
+  static constexpr uint32_t sel_stride = (uint32_t)align_up(sizeof(SelState<kMTNmax>), 128);
+  static constexpr uint32_t misc = sel + TEAMS * sel_stride;               // mbarriers, lock, ...
   static constexpr uint32_t total = misc + 128;
 };
 
-template <int NT, int SLOTS, int TT, int KW, bool kPaged>
+// Shared ring state for TEAMS = 2 (lock word + the slots' mbarrier phase bits between owners).
+struct RingShare {
+  int* lock;         // -1 free, else owning team
+  uint32_t* phases;  // bit s = parity to wait for on slot s's MMA barrier
+};
+
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
-  static_assert(KW == 64 || KW == 32, "item width: 64 (SW128) or 32 (SW64) columns");
-  static constexpr int IPT = 128 / KW;        // items per tile
-  static constexpr int TPR = KW / 8;          // threads per row piece (16 B each)
-  static constexpr int RPP = NT / TPR;        // rows per pass
-  static constexpr int RJ = 128 / RPP;        // rows per thread per tile
-  static constexpr uint32_t kSlot = 128 * KW * 2;
-  static constexpr uint32_t kAtom = KW * 16;  // 8-row swizzle atom (bytes) = SBO
-  static constexpr uint32_t kLayout = KW == 64 ? kLayoutSw128 : kLayoutSw64;
+  static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
+  static constexpr int RJ = 128 / RPP;      // rows per thread per tile
   uint32_t q_s, k_s0;
   uint64_t* mbar;     // [SLOTS], MMA-completion barrier of each ring slot
-  uint32_t* phase;    // [SLOTS]
+  uint32_t* phase;    // [SLOTS], this thread's copy
   uint32_t pend = 0;  // slots whose MMA has been committed but not yet waited
-  uint32_t tmem;
+  uint32_t tmem;      // this team's first accumulator column
+  RingShare ring;
   RowSrc ks;
   const char* kh;        // contiguous: row 0 of this (b, kv head)
   uint32_t row_bytes;    // contiguous: bytes between key rows
@@ -74,17 +84,11 @@ struct TCScorer {
     else return kh + (uint64_t)(uint32_t)s * row_bytes;
   }
 
-  // Byte offset of 16-byte chunk c of row r inside a slot (K-major, KW-column rows, swizzled).
-  static __device__ __forceinline__ uint32_t sw_off(int r, int c) {
-    if constexpr (KW == 64) return sw128_off(r, c);
-    else return (r >> 3) * 512u + (r & 7) * 64u + ((c ^ ((r & 7) >> 1)) << 4);
-  }
-
-  // Item i of a round = (tile c0 + i / IPT, column piece i % IPT) into slot i % SLOTS.  The row
-  // pointers are computed once per tile (at its first piece).
+  // Item i of a round = (tile c0 + i / 2, d-half i % 2) into slot i % SLOTS.  The row pointers are
+  // computed once per tile (at its first half).
   __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
-    const int c = c0 + i / IPT, h = i % IPT;
-    const int cq = threadIdx.x % TPR, r0 = threadIdx.x / TPR;
+    const int c = c0 + (i >> 1), h = i & 1;
+    const int tid = Sync::tid(), c8 = tid & 7, r0 = tid >> 3;
     if (h == 0) {
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int bmask = (1 << lbk) - 1;
@@ -94,14 +98,14 @@ struct TCScorer {
         const int r = r0 + RPP * j, lb = r >> lbk;
         const int s = lb < nblk ? (rep[blk0 + lb] << lbk) + (r & bmask) : Tk;
         const bool ok = s < Tk;
-        rp[j] = row(ok ? s : 0) + cq * 16;
+        rp[j] = row(ok ? s : 0) + c8 * 16;
         rok |= (uint32_t)ok << j;
       }
     }
-    const uint32_t dst = k_s0 + (i % SLOTS) * kSlot + sw_off(r0, cq);
+    const uint32_t dst = k_s0 + (i % SLOTS) * kMTSlot + sw128_off(r0, c8);
 #pragma unroll
     for (int j = 0; j < RJ; ++j)  // rows r0 + RPP j share r0's swizzle phase (RPP % 8 == 0)
-      cp_async16(dst + j * (RPP / 8) * kAtom, rp[j] + h * (KW * 2), ((rok >> j) & 1u) ? 16u : 0u);
+      cp_async16(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & 1u) ? 16u : 0u);
   }
 
   __device__ __forceinline__ void wait_slot(int slot) {
@@ -112,9 +116,37 @@ struct TCScorer {
     }
   }
 
+  // TEAMS = 2: take the ring (spin on the lock word) and the slots' barrier parities.
+  __device__ __forceinline__ void acquire() {
+    if constexpr (kShared) {
+      if (Sync::tid() == 0) {
+        while (atomicCAS(ring.lock, -1, 0) != -1) __nanosleep(64);
+        __threadfence_block();
+      }
+      Sync::sync();
+      const uint32_t bits = *reinterpret_cast<volatile uint32_t*>(ring.phases);
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) phase[s] = (bits >> s) & 1u;
+    }
+  }
+  // Give the ring back once every MMA that read it has completed (pend == 0) and every thread of
+  // the team is past its last cp.async wait.
+  __device__ __forceinline__ void release() {
+    if constexpr (kShared) {
+      Sync::sync();
+      if (Sync::tid() == 0) {
+        uint32_t bits = 0;
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) bits |= phase[s] << s;
+        *reinterpret_cast<volatile uint32_t*>(ring.phases) = bits;
+        __threadfence_block();
+        atomicExch(ring.lock, -1);
+      }
+    }
+  }
+
   __device__ void epilogue(const int* rep, int n_rep, int c0, int nt, float* out) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp >= 4) return;
+    const int warp = Sync::tid() >> 5, lane = threadIdx.x & 31;
     const int r = 32 * warp + lane, bm = (1 << lbk) - 1;
     for (int cc = 0; cc < nt; ++cc) {
       const int c = c0 + cc;
@@ -147,8 +179,9 @@ struct TCScorer {
 
   __device__ void score(const int* rep, int n_rep, float* out) {
     const int ntiles = (n_rep + bpt - 1) / bpt;
+    acquire();
     for (int c0 = 0; c0 < ntiles; c0 += TT) {  // rounds of up to TT tiles (TMEM columns)
-      const int nt = min(TT, ntiles - c0), nitems = IPT * nt;
+      const int nt = min(TT, ntiles - c0), nitems = 2 * nt;
 #pragma unroll
       for (int i = 0; i < SLOTS; ++i) {  // prologue: SLOTS items in flight
         if (i < nitems) issue(rep, n_rep, c0, i);
@@ -157,18 +190,16 @@ struct TCScorer {
       for (int i = 0; i < nitems; ++i) {
         cp_async_wait<SLOTS - 1>();  // item i landed
         fence_proxy_async_smem();
-        __syncthreads();
+        Sync::sync();
         const int slot = i % SLOTS;
-        if (threadIdx.x == 0) {
+        if (Sync::tid() == 0) {
           tc_fence_after();
-          const int cc = i / IPT, h = i % IPT;
-          const uint32_t kt = k_s0 + slot * kSlot;
-          // Q columns [h*KW, h*KW + KW): SW128 region h*KW/64, byte offset (h*KW % 64) * 2 in the row
-          const uint32_t qb = q_s + (h * KW / 64) * (32 * 128) + (h * KW % 64) * 2;
+          const int cc = i >> 1, h = i & 1;
+          const uint32_t kt = k_s0 + slot * kMTSlot;
 #pragma unroll
-          for (int s = 0; s < KW / 16; ++s) {
-            uint64_t a = smem_desc(kt + s * 32, 16, kAtom, kLayout);
-            uint64_t bq = smem_desc(qb + s * 32, 16, 1024, kLayoutSw128);
+          for (int s = 0; s < 4; ++s) {  // one d-half = 4 x K16
+            uint64_t a = smem_desc(kt + s * 32, 16, 1024, kLayoutSw128);
+            uint64_t bq = smem_desc(q_s + h * (32 * 128) + s * 32, 16, 1024, kLayoutSw128);
             umma_bf16(tmem + 32 * cc, a, bq, kIdescS, (h | s) ? 1u : 0u);
           }
           umma_commit(mbar + slot);
@@ -184,40 +215,50 @@ struct TCScorer {
       mark(1);  // gathers + MMA issue
 #pragma unroll
       for (int sl = 0; sl < SLOTS; ++sl) wait_slot(sl);  // drain the round's MMAs
+      if (c0 + TT >= ntiles) release();  // last round: the ring is free for the other team
       mark(2);  // MMA drain
       tc_fence_after();
       epilogue(rep, n_rep, c0, nt, out);
       tc_fence_before();
-      __syncthreads();  // scores visible; TMEM reads done before the next round's MMAs
+      Sync::sync();  // scores visible; TMEM reads done before the next round's MMAs
       mark(3);  // epilogue
     }
   }
 };
 
-template <int NT, int SLOTS, int TT, int KW, bool kPaged, int MINB>
-__global__ void __launch_bounds__(NT, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
-                                                          int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
-  constexpr uint32_t kCols = 32 * TT;
+// TEAMS units per CTA (NT = 128 threads each); TEAMS = 2 shares the ring (see the header).
+template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB>
+__global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
+                                                                   int32_t* __restrict__ idx,
+                                                                   int32_t* __restrict__ cnt) {
+  constexpr int NT = 128;
+  constexpr uint32_t kCols = 32 * TT * TEAMS;
+  using Sync = typename std::conditional<TEAMS == 1, CtaSync, TeamSync<NT>>::type;
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<SLOTS, KW>;
-  SelState<kMTNmax>& st = *reinterpret_cast<SelState<kMTNmax>*>(base + L::sel);
+  using L = MaskTCSmemLayout<SLOTS, TEAMS>;
+  const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / NT);
+  SelState<kMTNmax>& st = *reinterpret_cast<SelState<kMTNmax>*>(base + L::sel + team * L::sel_stride);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
+  int* lock = reinterpret_cast<int*>(tmem_slot + 1);
+  uint32_t* ring_phases = tmem_slot + 2;
   const int warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SLOTS; ++s) mbar_init(mbar + s, 1);
+    *lock = -1;
+    *ring_phases = 0u;
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<kCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot + 32 * TT * team;
   uint32_t phase[SLOTS];
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) phase[s] = 0u;
@@ -227,7 +268,7 @@ __global__ void __launch_bounds__(NT, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, 
 #endif
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  for (int64_t u = (int64_t)blockIdx.x * TEAMS + team; u < units; u += (int64_t)gridDim.x * TEAMS) {
     int b, h, q;
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
@@ -235,23 +276,25 @@ __global__ void __launch_bounds__(NT, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, 
     const int Bq = visible_blocks(sh, q, Tk);
     const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    const uint32_t q_s = sbase + L::q + team * kQTileBytes;
     if (Bq > sh.n) {
       // query block -> K-major SW128 tile (B operand, N = 32 rows, rows >= rows_q zero); waited for
       // together with the first item of the first round
-      for (int p = threadIdx.x; p < 32 * 16; p += NT) {
+      for (int p = Sync::tid(); p < 32 * 16; p += NT) {
         const int r = p >> 4, c16 = p & 15;
         const bool ok = r < rows_q;
         const char* src = q_ptr(qsrc, b, h, (int64_t)q * sh.bq + (ok ? r : 0)) + c16 * 16;
-        cp_async16(sbase + L::q + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
+        cp_async16(q_s + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, KW, kPaged> sc;
-    sc.q_s = sbase + L::q;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, (TEAMS > 1)> sc;
+    sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = mbar;
     sc.phase = phase;
     sc.tmem = tmem;
+    sc.ring = RingShare{lock, ring_phases};
     sc.ks = ks;
     sc.kh = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
     sc.row_bytes = (uint32_t)(ks.st * ks.esize);
@@ -262,15 +305,15 @@ __global__ void __launch_bounds__(NT, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, 
     sc.pt = &ptimer;
     ptimer.mark(7);  // unit setup / Q load / exact units
 #endif
-    tree_search<kMTNmax, NT>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
-    __syncthreads();
+    tree_search<kMTNmax, NT, decltype(sc), Sync>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
+    Sync::sync();
   }
   tc_fence_before();
   __syncthreads();
 #ifdef HIPATTN_PHASES
   ptimer.flush();
 #endif
-  if (warp == 0) tmem_dealloc<kCols>(tmem);
+  if (warp == 0) tmem_dealloc<kCols>(*tmem_slot);
 }
 
 // The tensor-core path needs a real query block on N (>= 8 rows); single-row decode scoring is a
@@ -281,29 +324,27 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int NT, int SLOTS, int TT, int KW, int MINB>
+template <int SLOTS, int TT, int TEAMS, int MINB>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
-  const size_t smem = MaskTCSmemLayout<SLOTS, KW>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<NT, SLOTS, TT, KW, true, MINB> : mask_tc_kernel<NT, SLOTS, TT, KW, false, MINB>;
+  const size_t smem = MaskTCSmemLayout<SLOTS, TEAMS>::total + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB> : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB>;
   int per_sm = 1;
-  cudaError_t e = persistent_ctas(kern, NT, smem, 32 * TT, &per_sm);
+  cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
-  kern<<<(unsigned)grid, NT, smem, stream>>>(sh, qs, ks, idx, cnt);
+  int64_t grid = std::min<int64_t>((units + TEAMS - 1) / TEAMS, (int64_t)num_sms * per_sm);
+  kern<<<(unsigned)grid, 128 * TEAMS, smem, stream>>>(sh, qs, ks, idx, cnt);
   return cudaGetLastError();
 }
 
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
-  // HIPATTN_MASK_TC=<KW>x<SLOTS>[bM] selects a variant (tuning aid, profiles/r01).
+  // HIPATTN_MASK_TC selects a variant (tuning aid, profiles/r01).
   const char* v = getenv("HIPATTN_MASK_TC");
-  if (v && !strcmp(v, "32x2b5")) return launch_v<128, 2, 4, 32, 5>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "32x2b6")) return launch_v<128, 2, 2, 32, 6>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "32x3")) return launch_v<128, 3, 4, 32, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "32x4")) return launch_v<128, 4, 4, 32, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
-  return launch_v<128, 2, 4, 64, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+  return launch_v<2, 4, 1, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
 
 #ifdef HIPATTN_PHASES

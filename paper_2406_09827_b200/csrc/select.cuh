@@ -37,6 +37,20 @@ struct SelState {
   int warp_tot[32];
 };
 
+// Barrier scope of the selection: the whole CTA (one unit per CTA), or one 128-thread team of a
+// CTA that runs two units side by side (named barrier 1 + team; mask_tc.cu ping-pong).
+struct CtaSync {
+  static __device__ __forceinline__ void sync() { __syncthreads(); }
+  static __device__ __forceinline__ int tid() { return threadIdx.x; }
+};
+template <int NT>
+struct TeamSync {
+  static __device__ __forceinline__ void sync() {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (int)(threadIdx.x / NT)), "n"(NT) : "memory");
+  }
+  static __device__ __forceinline__ int tid() { return threadIdx.x % NT; }
+};
+
 __device__ __forceinline__ uint32_t ord_score(float s) {
   s = (s != s) ? -INFINITY : s;  // NaN -> -inf
   s = (s == 0.f) ? 0.f : s;      // -0 -> +0
@@ -50,10 +64,10 @@ __device__ __forceinline__ uint64_t make_key(uint32_t ord, int first) {
 // Block-wide exclusive scan of one int per thread, ONE barrier: every warp scans itself, publishes
 // its total, and after the barrier each thread adds the totals of the warps before it (and of all
 // warps for *total).  The caller must separate two uses of warp_tot by a barrier.
-template <int NT>
+template <int NT, class Sync>
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
   constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = Sync::tid() >> 5;
   int x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -61,7 +75,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
     if (lane >= o) x += y;
   }
   if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
+  Sync::sync();
   int base = 0, tot = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -82,10 +96,10 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
 // barrier per pass suffices: pass p fills H[p % 3] and clears H[(p + 2) % 3], whose last readers
 // (pass p - 1's scans) are behind pass p's barrier.  Requires 1 <= need <= number of valid keys.
 // Returns the number of histogram passes.
-template <int NT, int EC, int NMAX>
+template <int NT, int EC, int NMAX, class Sync>
 __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t valid, int need, SelState<NMAX>& st,
                                          uint64_t& prefix, uint64_t& mask) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Sync::tid(), lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   int* hist = st.rep;
   uint32_t olo = 0u, ohi = 0u, alo = ~0u, ahi = ~0u;
@@ -106,7 +120,7 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
     st.red[32 + warp] = ((uint64_t)ahi << 32) | alo;
   }
   for (int i = tid; i < 512; i += NT) hist[i] = 0;  // H[0], H[1]
-  __syncthreads();
+  Sync::sync();
   uint64_t o = 0ull, a = ~0ull;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -130,7 +144,7 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
 #pragma unroll
     for (int k = 0; k < EC; ++k)
       if ((valid & (1u << k)) && (key[k] & mask) == prefix) atomicAdd(h + (uint32_t)((key[k] >> s) & dmask), 1);
-    __syncthreads();
+    Sync::sync();
     {
       int* hz = hist + ((pass + 2) % 3) * 256;  // clear the histogram of pass + 2
       for (int i = tid; i < 256; i += NT) hz[i] = 0;
@@ -177,14 +191,14 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
 // Runs the tree search of one query block with B_q visible key blocks and writes the n selected
 // blocks (ascending, -1 padded) to out_idx and the count to *out_cnt.  All NT threads call it.
 // Scorer::score(rep, n_rep, rep_s) must fill rep_s[i] = tile score of key block rep[i] and end
-// with a __syncthreads(); Scorer::mark(p) is a profiling hook (no-op in product builds).
-template <int NMAX, int NT, class Scorer>
+// with a Sync::sync(); Scorer::mark(p) is a profiling hook (no-op in product builds).
+template <int NMAX, int NT, class Scorer, class Sync = CtaSync>
 __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, int32_t* out_idx, int32_t* out_cnt) {
   static_assert(NMAX % NT == 0 || NT % NMAX == 0, "NMAX and NT must nest");
   constexpr int E = NMAX >= NT ? NMAX / NT : 1;  // nodes per thread (contiguous)
   constexpr int EC = 2 * E;                      // candidates per thread (their children)
   static_assert(EC <= 32, "valid mask");
-  const int tid = threadIdx.x;
+  const int tid = Sync::tid();
   if (Bq <= n) {  // exact case (G1): every visible block
     for (int j = tid; j < n; j += NT) out_idx[j] = j < Bq ? j : -1;
     if (tid == 0) *out_cnt = Bq;
@@ -198,7 +212,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
     st.nl[j] = (int)fj1 - 1;
     st.ns[j] = 0u;
   }
-  __syncthreads();
+  Sync::sync();
   bool first = true;
   // Every iteration at least halves the largest node, so <= 31 iterations end the search; the cap
   // only guards against non-finite inputs.
@@ -219,7 +233,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
       }
     }
     int tot;
-    const int pre = block_excl_scan<NT>(packed, st.warp_tot, tot);
+    const int pre = block_excl_scan<NT, Sync>(packed, st.warp_tot, tot);
     const int C = tot & 0xffff, nB = tot >> 16;
     if (nB == 0) break;  // every node is a single block (G5/G6)
     // This thread's children stay in registers: candidate 2i = left child (or the unsplit node),
@@ -259,7 +273,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
         p += split ? 2 : 1;
       }
     }
-    __syncthreads();
+    Sync::sync();
     scorer.mark(0);  // split + scan
     // --- representative scores (Alg. 1 lines 10-13)
     scorer.score(st.rep, first ? C : nB, st.rep_s);
@@ -270,7 +284,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
       key[k] = make_key(kr[k] >= 0 ? ord_score(st.rep_s[kr[k]]) : ks[k], kf[k]);
     uint64_t prefix, mask;
     scorer.mark(8);  // keys
-    const int passes = radix_top<NT, EC>(key, valid, n, st, prefix, mask);
+    const int passes = radix_top<NT, EC, NMAX, Sync>(key, valid, n, st, prefix, mask);
     scorer.mark(4);  // radix select
 #ifdef HIPATTN_PHASES
     if (tid == 0) {
@@ -284,7 +298,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
 #pragma unroll
     for (int k = 0; k < EC; ++k) cnt += ((valid >> k) & 1u) && (key[k] & mask) >= prefix;
     int ctot;
-    int pos = block_excl_scan<NT>(cnt, st.warp_tot, ctot);
+    int pos = block_excl_scan<NT, Sync>(cnt, st.warp_tot, ctot);
 #pragma unroll
     for (int k = 0; k < EC; ++k)
       if (((valid >> k) & 1u) && (key[k] & mask) >= prefix) {
@@ -293,7 +307,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
         st.ns[pos] = (uint32_t)(key[k] >> kFirstBits);
         ++pos;
       }
-    __syncthreads();
+    Sync::sync();
     scorer.mark(5);  // compaction
     first = false;
   }
