@@ -135,6 +135,9 @@ hip::RowSrc make_paged(const hip_paged_kv_t& pg, const void* pages, int esz) {
   r.base = static_cast<const char*>(pages);
   r.sp = pg.stride_page; r.sh = pg.stride_h; r.st = pg.stride_t; r.esize = esz; r.paged = 1;
   r.block_table = pg.block_table; r.page_size = pg.page_size; r.max_pages = pg.max_pages_per_seq;
+  r.page_shift = -1;
+  for (int sh = 0; sh < 31; ++sh)
+    if ((1 << sh) == pg.page_size) r.page_shift = sh;
   return r;
 }
 

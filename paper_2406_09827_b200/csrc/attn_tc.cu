@@ -3,7 +3,8 @@
 //
 // Per query block (b_q <= 32 rows) the selected key blocks give <= k keys, processed in chunks of
 // 128.  Each chunk streams four 16 KB items through a 2-slot shared ring (16-byte cp.async gathers
-// into 128-byte-swizzled layouts): the two d-halves of K_c and the two 64-key halves of V_c.  One
+// into 128-byte-swizzled layouts; a slot is refilled as soon as the MMA that read it completes, so
+// two items are in flight): the two d-halves of K_c and the two 64-key halves of V_c.  One
 // thread issues
 //     S^T_c [128 keys x 32 q]  = K_c . Q^T         (M=128, N=32, K=d; A, B K-major)
 //     O^T   [128 d x 32 q]    += V_c^T . P_c^T     (M=128, N=32, K=keys; A, B MN-major)
@@ -181,16 +182,15 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     const int nitems = 4 * nch;
     issue(0);
     cp_async_commit();
+    issue(1);  // nitems >= 4
+    cp_async_commit();
     for (int it = 0; it < nitems; ++it) {
-      cp_async_wait<0>();  // item it landed
+      cp_async_wait<1>();  // item it landed (item it + 1 may still be in flight)
       fence_proxy_async_smem();
       __syncthreads();
-      // refill the other slot (item it - 1's) with item it + 1 once item it - 1's MMA has read it.
-      // tcgen05 MMAs of one thread complete in order, so this wait also retires every earlier MMA
-      // (S of this chunk before its softmax, and the previous chunk's PV before P is rewritten).
-      wait_slot((it + 1) & 1);
-      if (it + 1 < nitems) issue(it + 1);
-      cp_async_commit();
+      // Every MMA up to item it - 1 has completed here (each slot is refilled only after its MMA is
+      // waited for, and tcgen05 MMAs of one thread complete in order): S of this chunk is final
+      // before its softmax, and the previous chunk's PV is done before P is rewritten.
       const int ch = it >> 2, kind = it & 3;
       const uint32_t slot = sb + L::ring + (it & 1) * kATSlot;
       if (kind == 2) {
@@ -304,6 +304,12 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         umma_commit(mbar + (it & 1));
       }
       pend[it & 1] = true;
+      // refill this slot with item it + 2 as soon as MMA(it) has read it (two items in flight)
+      if (it + 2 < nitems) {
+        wait_slot(it & 1);
+        issue(it + 2);
+      }
+      cp_async_commit();
     }
     wait_slot(0);  // the last MMAs (O^T complete)
     wait_slot(1);

@@ -26,15 +26,24 @@ struct RowSrc {
   int64_t sp;                // paged: page stride (elements)
   const int32_t* block_table;
   int32_t page_size, max_pages;
+  int32_t page_shift;        // paged: log2(page_size) if a power of two, else -1
   int32_t paged;
   int32_t esize;             // bytes per element
 };
 
 __device__ __forceinline__ const char* row_ptr(const RowSrc& r, int b, int hk, int64_t s) {
   if (!r.paged) return r.base + (b * r.sb + hk * r.sh + s * r.st) * r.esize;
-  int64_t pi = s / r.page_size;
-  int64_t page = __ldg(r.block_table + (int64_t)b * r.max_pages + pi);
-  return r.base + (page * r.sp + hk * r.sh + (s - pi * r.page_size) * r.st) * r.esize;
+  const uint32_t us = (uint32_t)s;  // token index < 2^31
+  uint32_t pi, off;
+  if (r.page_shift >= 0) {
+    pi = us >> r.page_shift;
+    off = us & ((1u << r.page_shift) - 1u);
+  } else {
+    pi = us / (uint32_t)r.page_size;
+    off = us - pi * (uint32_t)r.page_size;
+  }
+  const int64_t page = __ldg(r.block_table + (int64_t)b * r.max_pages + pi);
+  return r.base + (page * r.sp + hk * r.sh + (int64_t)off * r.st) * r.esize;
 }
 
 struct QSrc {
