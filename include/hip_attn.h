@@ -123,10 +123,11 @@ size_t hip_workspace_bytes(hip_op_t op, hip_dtype_t dtype, int32_t B, int32_t H_
  *   q_t . k_s over the tile of the branch's first block (causal pairs only), keep the n best by
  *   (score desc, first block asc), until all nodes are single blocks.  Scores are fp32; the
  *   summation order of each dot product depends on the path (readings G9/G9b):
- *     - query blocks of <= 4 rows (decode), b_k a power of two <= 8: 16 sequential fmaf segments
- *       of d/16 terms combined by the xor tree o = 8, 4, 2, 1 ("F32L");
- *     - bf16, 8 <= b_q <= 32, d = 128, b_k | 32: tcgen05 fp32 accumulation, whose rounding can flip
- *       near-tied selections (reported as a fraction by the tests);
+ *     - bf16, b_q <= 32 (decode included), d = 128, b_k | 32, n <= 256: tcgen05 fp32 accumulation,
+ *       whose rounding can flip near-tied selections (reported as a fraction by the tests,
+ *       DESIGN.md "Parity");
+ *     - other query blocks of <= 4 rows (fp32 or d = 64 decode), b_k a power of two <= 16: 16
+ *       sequential fmaf segments of d/16 terms combined by the xor tree o = 8, 4, 2, 1 ("F32L");
  *     - otherwise, and always with HIP_FLAG_EXACT_SCORES: the sequential chain c = 0..d-1 ("F32C").
  *   Errors: INVALID_VALUE for NULL pointers, dims < 1, T_k = 0 ("empty K"), k < b_k or
  *   k % b_k != 0, H_q % H_kv != 0, causal with T_q > T_k, page_size % b_k != 0, n > 1024,

@@ -74,14 +74,18 @@ struct TCScorer {
   uint32_t row_bytes;    // contiguous: bytes between key rows
   int b, hk, Tk, lbk, causal, rows_q, bpt;
   int64_t tpos0;
+  const int* pg;         // paged: page of each representative block (aliases the score output)
   const char* rp[RJ];    // this thread's source rows of the tile being issued
   uint32_t rok;          // bit j: rp[j] is a real row (< T_k, block < n_rep)
   HIP_PT_MEMBER
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
-  __device__ __forceinline__ const char* row(int s) const {
-    if constexpr (kPaged) return row_ptr(ks, b, hk, s);
-    else return kh + (uint64_t)(uint32_t)s * row_bytes;
+  __device__ __forceinline__ const char* row(int s) const { return kh + (uint64_t)(uint32_t)s * row_bytes; }
+  // Paged: key row s of a block whose page was looked up once per call (pg).
+  __device__ __forceinline__ const char* paged_row(int page, int s) const {
+    const uint32_t off = ks.page_shift >= 0 ? ((uint32_t)s & ((1u << ks.page_shift) - 1u))
+                                            : ((uint32_t)s % (uint32_t)ks.page_size);
+    return ks.base + ((int64_t)page * ks.sp + (int64_t)hk * ks.sh + (int64_t)off * ks.st) * ks.esize;
   }
 
   // Item i of a round = (tile c0 + i / 2, d-half i % 2) into slot i % SLOTS.  The row pointers are
@@ -98,7 +102,8 @@ struct TCScorer {
         const int r = r0 + RPP * j, lb = r >> lbk;
         const int s = lb < nblk ? (rep[blk0 + lb] << lbk) + (r & bmask) : Tk;
         const bool ok = s < Tk;
-        rp[j] = row(ok ? s : 0) + c8 * 16;
+        if constexpr (kPaged) rp[j] = (ok ? paged_row(pg[blk0 + lb], s) : ks.base) + c8 * 16;
+        else rp[j] = row(ok ? s : 0) + c8 * 16;
         rok |= (uint32_t)ok << j;
       }
     }
@@ -180,6 +185,20 @@ struct TCScorer {
   __device__ void score(const int* rep, int n_rep, float* out) {
     const int ntiles = (n_rep + bpt - 1) / bpt;
     acquire();
+    if constexpr (kPaged) {
+      // one block-table lookup per representative block for the whole call (a block never straddles
+      // a page), so the gathers below carry no dependent global load.  pg[i] is read only before
+      // the epilogue that overwrites out[i].
+      int* pgw = reinterpret_cast<int*>(out);
+      const int32_t* bt = ks.block_table + (int64_t)b * ks.max_pages;
+      for (int i = Sync::tid(); i < n_rep; i += NT) {
+        const uint32_t s0 = (uint32_t)rep[i] << lbk;
+        const uint32_t pi = ks.page_shift >= 0 ? (s0 >> ks.page_shift) : (s0 / (uint32_t)ks.page_size);
+        pgw[i] = __ldg(bt + pi);
+      }
+      Sync::sync();
+      pg = pgw;
+    }
     for (int c0 = 0; c0 < ntiles; c0 += TT) {  // rounds of up to TT tiles (TMEM columns)
       const int nt = min(TT, ntiles - c0), nitems = 2 * nt;
 #pragma unroll
@@ -316,11 +335,12 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
   if (warp == 0) tmem_dealloc<kCols>(*tmem_slot);
 }
 
-// The tensor-core path needs a real query block on N (>= 8 rows); single-row decode scoring is a
-// GEMV (mask_decode.cu).  b_k must be a power of two <= 32 so that a block's rows sit in one warp's
-// TMEM lanes.
+// Any query block of <= 32 rows (the N = 32 operand is zero-padded): decode (b_q = 1) too — the
+// tensor cores are idle in this gather-bound kernel, so padding costs nothing, and the ring of
+// swizzled half tiles keeps more bytes in flight than the register-staged GEMV (C3: 229 vs 404 us).
+// b_k must be a power of two <= 32 so that a block's rows sit in one warp's TMEM lanes.
 bool mask_tc_supported(const Shape& sh) {
-  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && sh.bk >= 1 && sh.bk <= 32 && (32 % sh.bk) == 0 &&
+  return sh.d == 128 && sh.bq >= 1 && sh.bq <= 32 && sh.bk >= 1 && sh.bk <= 32 && (32 % sh.bk) == 0 &&
          sh.n <= kMTNmax;
 }
 
