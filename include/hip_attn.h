@@ -86,7 +86,8 @@ typedef struct {
     const int32_t* seq_lens;          /* [B] device, T_k of each sequence, 1 <= T_k <= max_seq_len */
     int32_t page_size;
     int32_t max_pages_per_seq;
-    int32_t num_pages;                /* physical pages (for documentation / sanitizer runs)     */
+    int32_t num_pages;                /* physical pages; 0 = unknown (the decode attention then  */
+                                      /* avoids the tcgen05 path, which indexes rows in int32)   */
     int32_t max_seq_len;              /* host-side upper bound of seq_lens (sizes the launch)    */
 } hip_paged_kv_t;
 

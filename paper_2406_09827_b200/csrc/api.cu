@@ -136,6 +136,7 @@ hip::RowSrc make_paged(const hip_paged_kv_t& pg, const void* pages, int esz) {
   r.sp = pg.stride_page; r.sh = pg.stride_h; r.st = pg.stride_t; r.esize = esz; r.paged = 1;
   r.block_table = pg.block_table; r.page_size = pg.page_size; r.max_pages = pg.max_pages_per_seq;
   r.page_shift = -1;
+  r.sp_rows = (pg.stride_t > 0 && pg.stride_page % pg.stride_t == 0) ? pg.stride_page / pg.stride_t : 0;
   for (int sh = 0; sh < 31; ++sh)
     if ((1 << sh) == pg.page_size) r.page_shift = sh;
   return r;
@@ -250,7 +251,13 @@ hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* op = static_cast<char*>(const_cast<void*>(o.ptr));
   cudaError_t e;
-  if (hip::attn_decode_supported(sh))
+  // tcgen05 path: physical row index page * (page stride in rows) + offset must fit in int32
+  const bool tc_rows = ks.sp_rows > 0 && paged->num_pages > 0 &&
+                       (int64_t)paged->num_pages * ks.sp_rows < ((int64_t)1 << 31);
+  if (dtype == HIP_DTYPE_BF16 && tc_rows && hip::attn_tc_supported(sh))
+    e = hip::launch_attn_tc(sh, qs, ks, vs, block_idx, block_cnt, scale, op, o.stride_b, o.stride_h, o.stride_t, lse,
+                            st, sms);
+  else if (hip::attn_decode_supported(sh))
     e = hip::launch_attn_decode(sh, qs, ks, vs, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, scale, op, o.stride_b,
                                 o.stride_h, o.stride_t, lse, st, sms);
   else

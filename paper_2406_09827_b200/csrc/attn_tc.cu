@@ -59,6 +59,7 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   return v[0];
 }
 
+template <bool kPaged>
 __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
                                                                 const int32_t* __restrict__ idx,
                                                                 const int32_t* __restrict__ cnt, float scale_log2,
@@ -128,13 +129,24 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
       const char* src = q_ptr(qsrc, b, h, (int64_t)q * sh.bq + (ok ? r : 0)) + c16 * 16;
       cp_async16(sb + L::q + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
     }
-    // token of every selected key slot (or -1 past T_k / past cnt), staged once per unit
+    // row of every selected key slot (or -1 past T_k / past cnt), staged once per unit: the token
+    // index for contiguous K/V, the physical row page * (page stride in rows) + offset for a paged
+    // cache (K and V share the block table and strides), so the gathers carry no dependent load
     for (int k = threadIdx.x; k < nch * 128; k += kATThreads) {
       int s = -1;
       if (k < nkeys) {
         const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
         s = (j << lbk) + (k & ((1 << lbk) - 1));
         if (s >= Tk) s = -1;
+        if constexpr (kPaged) {
+          if (s >= 0) {
+            const uint32_t us = (uint32_t)s;
+            const uint32_t pi = ks.page_shift >= 0 ? (us >> ks.page_shift) : (us / (uint32_t)ks.page_size);
+            const uint32_t off = us - pi * (uint32_t)ks.page_size;
+            const int64_t page = __ldg(ks.block_table + (int64_t)b * ks.max_pages + pi);
+            s = (int)(page * ks.sp_rows + off);
+          }
+        }
       }
       tok[k] = s;
     }
@@ -144,8 +156,8 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
       lurun[threadIdx.x] = 0.f;
     }
     __syncthreads();
-    const char* kbase = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
-    const char* vbase = vs.base + (b * vs.sb + hk * vs.sh) * (int64_t)vs.esize;
+    const char* kbase = ks.base + ((kPaged ? 0 : b * ks.sb) + hk * ks.sh) * (int64_t)ks.esize;
+    const char* vbase = vs.base + ((kPaged ? 0 : b * vs.sb) + hk * vs.sh) * (int64_t)vs.esize;
     const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
 
     // item i: chunk ch = i >> 2; (i & 3) = 0, 1: K_ch d-half 0 / 1; 2, 3: V_ch keys [0,64) / [64,128)
@@ -198,7 +210,18 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         tc_fence_after();
         float v[32];
         tmem_ld_32x32b_x32(tmem_lane, v);
-        const int s = tok[ch * 128 + 32 * warp + lane];
+        int s;  // token position of this lane's key (-1: none)
+        if constexpr (kPaged) {
+          const int k = ch * 128 + 32 * warp + lane;
+          s = -1;
+          if (k < nkeys) {
+            const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
+            s = (j << lbk) + (k & ((1 << lbk) - 1));
+            if (s >= Tk) s = -1;
+          }
+        } else {
+          s = tok[ch * 128 + 32 * warp + lane];
+        }
         const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -349,8 +372,10 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   if (warp == 0) tmem_dealloc<64>(tmem);
 }
 
+// Any query block of <= 32 rows (decode included: the N = 32 operand is zero-padded, the tensor
+// cores are idle anyway); <= 512 selected keys (the staged row list).
 bool attn_tc_supported(const Shape& sh) {
-  return sh.d == 128 && sh.bq >= 8 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 &&
+  return sh.d == 128 && sh.bq >= 1 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 &&
          (int64_t)sh.n * sh.bk <= 512;
 }
 
@@ -358,13 +383,14 @@ cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, co
                            const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                            float* lse, cudaStream_t stream, int num_sms) {
   const size_t smem = AttnTCSmem::total + 1024;
+  auto kern = ks.paged ? attn_tc_kernel<true> : attn_tc_kernel<false>;
   int per_sm = 1;
-  cudaError_t e = persistent_ctas(attn_tc_kernel, kATThreads, smem, 64, &per_sm);
+  cudaError_t e = persistent_ctas(kern, kATThreads, smem, 64, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
-  attn_tc_kernel<<<(unsigned)grid, kATThreads, smem, stream>>>(sh, qs, ks, vs, idx, cnt, sm_scale * kATLog2e, o, osb,
-                                                               osh, ost, lse);
+  kern<<<(unsigned)grid, kATThreads, smem, stream>>>(sh, qs, ks, vs, idx, cnt, sm_scale * kATLog2e, o, osb, osh, ost,
+                                                     lse);
   return cudaGetLastError();
 }
 

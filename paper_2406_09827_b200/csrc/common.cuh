@@ -27,6 +27,7 @@ struct RowSrc {
   const int32_t* block_table;
   int32_t page_size, max_pages;
   int32_t page_shift;        // paged: log2(page_size) if a power of two, else -1
+  int64_t sp_rows;           // paged: sp / st when integral (page stride in rows), else 0
   int32_t paged;
   int32_t esize;             // bytes per element
 };
