@@ -17,7 +17,9 @@
  *                             (P:178-180), keep the top-n branches with
  *                             ties toward the smaller block (G10), until every node is one block
  *                             (G5, G6).  Causal reading G7/G8.
- *   - oracle_sparse_attention Eq. 2-3: softmax over the selected tokens only, fp64.
+ *   - oracle_sparse_attention Eq. 2-3: softmax over the selected tokens only, fp64;
+ *                             *_sw adds the StreamingLLM sink and sliding-window tokens (P:641-645,
+ *                             the EffectiveMask union of S:285-301; reading G14).
  *   - oracle_dense_attention  S = QK^T, P = softmax(S), O = PV, fp64, causal optional.
  *   - oracle_exact_block_topn top-n of the exact block-max scores (the textbook top-k of P:116 at
  *                             block granularity) — used for pins and recall.
@@ -429,11 +431,18 @@ static void attend_row(const float *q, const float *Kh, const float *Vh, int Tk,
     free(x);
 }
 
-/* Shared driver: dense = 1 attends to every visible key; else the idx/cnt selection. */
+/* Shared driver: dense = 1 attends to every visible key; else the idx/cnt selection,  */
+/* optionally united with StreamingLLM sink and sliding-window tokens ("local sliding window and    */
+/* global sink attention are also added during block sparse flash attention"; the       */
+/* EffectiveMask of S:285-301): row t at position p = t + Tk - Tq attends to                         */
+/*     (selected block tokens) U [0, sink) U (p - window, p],  intersected with [0, Tk) and, if       */
+/* causal, with s <= p; each token once (sorted, duplicates removed), visited in ascending order.    */
 static int attention_impl(const float *Q, const float *K, const float *V, int B, int Hq, int Hkv, int Tq,
                           int Tk, int d, int n, int bq, int bk, int causal, double sm_scale,
-                          const int32_t *idx, const int32_t *cnt, int dense, double *O, double *lse)
+                          const int32_t *idx, const int32_t *cnt, int dense, int sink, int window, double *O,
+                          double *lse)
 {
+    if (sink < 0 || window < 0) return ORC_EINVAL;
     if (sm_scale <= 0.0) sm_scale = 1.0 / sqrt((double)d);
     int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
     int64_t nkb = ((int64_t)Tk + bk - 1) / bk;
@@ -447,7 +456,7 @@ static int attention_impl(const float *Q, const float *K, const float *V, int B,
         int64_t q = t / bq, u = bh * nqb + q;
         const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
         const float *Vh = V + ((b * Hkv + hk) * (int64_t)Tk) * d;
-        int64_t cap = dense ? (int64_t)Tk : (int64_t)n * bk;
+        int64_t cap = dense ? (int64_t)Tk : (int64_t)n * bk + sink + window;
         int64_t *tok = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cap > 0 ? cap : 1));
         int64_t ntok = 0;
         int bad = 0;
@@ -464,6 +473,18 @@ static int attention_impl(const float *Q, const float *K, const float *V, int B,
                 prev = j;
                 for (int64_t s = j * bk; s < imin64((j + 1) * (int64_t)bk, Tk); ++s)
                     if (!causal || s <= t + delta) tok[ntok++] = s;
+            }
+            if (!bad && (sink > 0 || window > 0)) {
+                int64_t p = t + delta;
+                for (int64_t s = 0; s < imin64(sink, Tk); ++s)
+                    if (!causal || s <= p) tok[ntok++] = s;
+                for (int64_t s = p - window + 1; s <= p; ++s)
+                    if (s >= 0 && s < Tk) tok[ntok++] = s;
+                qsort(tok, (size_t)ntok, sizeof(int64_t), i64_cmp);
+                int64_t w = 0;
+                for (int64_t i = 0; i < ntok; ++i)
+                    if (w == 0 || tok[i] != tok[w - 1]) tok[w++] = tok[i];
+                ntok = w;
             }
         }
         if (bad) {
@@ -483,8 +504,20 @@ int oracle_sparse_attention(const float *Q, const float *K, const float *V, int 
 {
     int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
     if (rc) return rc;
-    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, k / bk, bq, bk, causal, sm_scale, idx, cnt, 0, O,
-                          lse);
+    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, k / bk, bq, bk, causal, sm_scale, idx, cnt, 0, 0, 0,
+                          O, lse);
+}
+
+/* The same with sink and sliding-window tokens. */
+int oracle_sparse_attention_sw(const float *Q, const float *K, const float *V, int B, int Hq, int Hkv, int Tq,
+                               int Tk, int d, int k, int bq, int bk, int causal, double sm_scale,
+                               const int32_t *idx, const int32_t *cnt, int sink, int window, double *O,
+                               double *lse)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, k / bk, bq, bk, causal, sm_scale, idx, cnt, 0, sink,
+                          window, O, lse);
 }
 
 int oracle_dense_attention(const float *Q, const float *K, const float *V, int B, int Hq, int Hkv, int Tq,
@@ -492,7 +525,8 @@ int oracle_dense_attention(const float *Q, const float *K, const float *V, int B
 {
     int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, 1, 1, 1, causal);
     if (rc) return rc;
-    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, 1, 1, 1, causal, sm_scale, NULL, NULL, 1, O, lse);
+    return attention_impl(Q, K, V, B, Hq, Hkv, Tq, Tk, d, 1, 1, 1, causal, sm_scale, NULL, NULL, 1, 0, 0, O,
+                          lse);
 }
 
 /* -------------------------------------------------------------------------------------------- */
@@ -559,11 +593,11 @@ int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int pa
     return err;
 }
 
-int oracle_sparse_attention_paged(const float *Q, const float *Kpages, const float *Vpages, int num_pages,
-                                  int page_size, const int32_t *block_table, int max_pages,
-                                  const int32_t *seq_lens, int B, int Hq, int Hkv, int Tq, int d, int k, int bq,
-                                  int bk, int causal, double sm_scale, const int32_t *idx, const int32_t *cnt,
-                                  double *O, double *lse)
+int oracle_sparse_attention_paged_sw(const float *Q, const float *Kpages, const float *Vpages, int num_pages,
+                                     int page_size, const int32_t *block_table, int max_pages,
+                                     const int32_t *seq_lens, int B, int Hq, int Hkv, int Tq, int d, int k,
+                                     int bq, int bk, int causal, double sm_scale, const int32_t *idx,
+                                     const int32_t *cnt, int sink, int window, double *O, double *lse)
 {
     if (page_size < 1 || page_size % bk != 0 || num_pages < 1) return ORC_EINVAL;
     int n = k / bk;
@@ -586,7 +620,7 @@ int oracle_sparse_attention_paged(const float *Q, const float *Kpages, const flo
                 int64_t off = ((int64_t)b * Hq + h);
                 /* one (b, h) slice as a B=Hq=Hkv=1 problem */
                 rc = attention_impl(Q + off * Tq * d, Kh, Vh, 1, 1, 1, Tq, Tk, d, n, bq, bk, causal, sm_scale,
-                                    idx + off * nqb * n, cnt + off * nqb, 0, O + off * Tq * d,
+                                    idx + off * nqb * n, cnt + off * nqb, 0, sink, window, O + off * Tq * d,
                                     lse ? lse + off * Tq : NULL);
                 if (rc) err = rc;
             }
@@ -595,6 +629,17 @@ int oracle_sparse_attention_paged(const float *Q, const float *Kpages, const flo
         }
     }
     return err;
+}
+
+int oracle_sparse_attention_paged(const float *Q, const float *Kpages, const float *Vpages, int num_pages,
+                                  int page_size, const int32_t *block_table, int max_pages,
+                                  const int32_t *seq_lens, int B, int Hq, int Hkv, int Tq, int d, int k, int bq,
+                                  int bk, int causal, double sm_scale, const int32_t *idx, const int32_t *cnt,
+                                  double *O, double *lse)
+{
+    return oracle_sparse_attention_paged_sw(Q, Kpages, Vpages, num_pages, page_size, block_table, max_pages,
+                                            seq_lens, B, Hq, Hkv, Tq, d, k, bq, bk, causal, sm_scale, idx, cnt, 0,
+                                            0, O, lse);
 }
 
 int oracle_num_threads(void)

@@ -59,11 +59,15 @@ def lib():
         _lib.oracle_mask_paged.argtypes = [P, P, i32, i32, P, i32, P] + [i32] * 9 + [P] * 6
         _lib.oracle_sparse_attention_paged.argtypes = ([P, P, P, i32, i32, P, i32, P] + [i32] * 9
                                                        + [f64, P, P, P, P])
+        _lib.oracle_sparse_attention_sw.argtypes = [P, P, P] + [i32] * 10 + [f64, P, P, i32, i32, P, P]
+        _lib.oracle_sparse_attention_paged_sw.argtypes = ([P, P, P, i32, i32, P, i32, P] + [i32] * 9
+                                                          + [f64, P, P, i32, i32, P, P])
         _lib.oracle_num_threads.restype = i32
         _lib.oracle_set_num_threads.argtypes = [i32]
         for name in ("oracle_mask", "oracle_mask_trace", "oracle_exact_block_topn", "oracle_block_scores",
                      "oracle_sparse_attention", "oracle_dense_attention", "oracle_mask_paged",
-                     "oracle_sparse_attention_paged"):
+                     "oracle_sparse_attention_paged", "oracle_sparse_attention_sw",
+                     "oracle_sparse_attention_paged_sw"):
             getattr(_lib, name).restype = i32
     return _lib
 
@@ -173,16 +177,23 @@ def block_scores(Q, K, bq: int, bk: int, causal: bool, tuples, mode: int = F64):
     return sc, em
 
 
-def sparse_attention(Q, K, V, k: int, bq: int, bk: int, causal: bool, idx, cnt, sm_scale: float = 0.0):
-    """Eq. 2-3 in fp64 over the selection idx/cnt -> (O [B,Hq,Tq,d] f64, lse [B,Hq,Tq] f64)."""
+def sparse_attention(Q, K, V, k: int, bq: int, bk: int, causal: bool, idx, cnt, sm_scale: float = 0.0,
+                     sink: int = 0, window: int = 0):
+    """Eq. 2-3 in fp64 over the selection idx/cnt -> (O [B,Hq,Tq,d] f64, lse [B,Hq,Tq] f64).  With
+    sink/window > 0 the selection is united with the sink and sliding-window tokens."""
     Q, K, V = _f32(Q), _f32(K), _f32(V)
     idx, cnt = _i32(idx), _i32(cnt)
     B, Hq, Tq, d = Q.shape
     _, Hkv, Tk, _ = K.shape
     O = np.empty((B, Hq, Tq, d), np.float64)
     lse = np.empty((B, Hq, Tq), np.float64)
-    rc = lib().oracle_sparse_attention(_p(Q), _p(K), _p(V), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal),
-                                       float(sm_scale), _p(idx), _p(cnt), _p(O), _p(lse))
+    if sink or window:
+        rc = lib().oracle_sparse_attention_sw(_p(Q), _p(K), _p(V), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal),
+                                              float(sm_scale), _p(idx), _p(cnt), int(sink), int(window), _p(O),
+                                              _p(lse))
+    else:
+        rc = lib().oracle_sparse_attention(_p(Q), _p(K), _p(V), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal),
+                                           float(sm_scale), _p(idx), _p(cnt), _p(O), _p(lse))
     _check(rc, "oracle_sparse_attention")
     return O, lse
 
@@ -223,7 +234,7 @@ def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causa
 
 
 def sparse_attention_paged(Q, Kpages, Vpages, block_table, seq_lens, k: int, bq: int, bk: int, causal: bool,
-                           idx, cnt, sm_scale: float = 0.0):
+                           idx, cnt, sm_scale: float = 0.0, sink: int = 0, window: int = 0):
     Q, Kp, Vp = _f32(Q), _f32(Kpages), _f32(Vpages)
     bt, sl = _i32(block_table), _i32(seq_lens)
     idx, cnt = _i32(idx), _i32(cnt)
@@ -231,8 +242,9 @@ def sparse_attention_paged(Q, Kpages, Vpages, block_table, seq_lens, k: int, bq:
     num_pages, Hkv, ps, _ = Kp.shape
     O = np.empty((B, Hq, Tq, d), np.float64)
     lse = np.empty((B, Hq, Tq), np.float64)
-    rc = lib().oracle_sparse_attention_paged(_p(Q), _p(Kp), _p(Vp), num_pages, ps, _p(bt), bt.shape[1], _p(sl),
-                                             B, Hq, Hkv, Tq, d, k, bq, bk, int(causal), float(sm_scale),
-                                             _p(idx), _p(cnt), _p(O), _p(lse))
+    rc = lib().oracle_sparse_attention_paged_sw(_p(Q), _p(Kp), _p(Vp), num_pages, ps, _p(bt), bt.shape[1],
+                                                _p(sl), B, Hq, Hkv, Tq, d, k, bq, bk, int(causal),
+                                                float(sm_scale), _p(idx), _p(cnt), int(sink), int(window), _p(O),
+                                                _p(lse))
     _check(rc, "oracle_sparse_attention_paged")
     return O, lse

@@ -29,6 +29,10 @@ MUTANTS = {
     "exact case up to 2n": ("if (Bq <= n) { /* exact case */", "if (Bq <= 2 * n) { /* exact case */"),
     "split rounds half down": ("int64_t m = (f + l + 1) / 2;", "int64_t m = (f + l) / 2;"),
     "paged slot uses page index": ("+ s % ps) * d;", "+ s / ps % ps) * d;"),
+    "window one token too long": ("for (int64_t s = p - window + 1; s <= p; ++s)", "for (int64_t s = p - window; s <= p; ++s)"),
+    "sink ignores causality": ("for (int64_t s = 0; s < imin64(sink, Tk); ++s)\n                    if (!causal || s <= p) tok[ntok++] = s;",
+                               "for (int64_t s = 0; s < imin64(sink, Tk); ++s)\n                    tok[ntok++] = s;"),
+    "union keeps duplicates": ("if (w == 0 || tok[i] != tok[w - 1]) tok[w++] = tok[i];", "tok[w++] = tok[i];"),
 }
 
 

@@ -459,3 +459,100 @@ def test_f32l_mode_pins(orc):
     assert (np.abs(s_l - s_64) <= gamma * em).all()
     with pytest.raises(ValueError):
         orc.mask(Q[..., :24], K[..., :24], k, bq, bk, True, mode=orc.F32L)
+
+
+# --------------------------------------------------------------------------------------------
+# Sink + sliding window (f1; "local sliding window and global sink attention are also
+# added", sizes (128, 32); the EffectiveMask of S:285-301: per row the union of the selected block
+# tokens, [0, sink) and (p - window, p], intersected with the causal bound, each token once).
+# --------------------------------------------------------------------------------------------
+def _brute_effective_attention(Q, K, V, bq, bk, causal, idx, cnt, sink, window, scale):
+    """Plain-Python sets -> explicit boolean mask -> fp64 softmax (independent of the oracle)."""
+    Q, K, V = (np.asarray(x, np.float64) for x in (Q, K, V))
+    B, Hq, Tq, d = Q.shape
+    Hkv, Tk = K.shape[1], K.shape[2]
+    O = np.zeros_like(Q)
+    for b in range(B):
+        for h in range(Hq):
+            hk = h // (Hq // Hkv)
+            for t in range(Tq):
+                p = t + Tk - Tq
+                q = t // bq
+                keys = set()
+                for i in range(int(cnt[b, h, q])):
+                    j = int(idx[b, h, q, i])
+                    keys |= set(range(j * bk, min((j + 1) * bk, Tk)))
+                keys |= set(range(min(sink, Tk)))
+                keys |= {s for s in range(p - window + 1, p + 1) if 0 <= s < Tk}
+                if causal:
+                    keys = {s for s in keys if s <= p}
+                ks = sorted(keys)
+                if not ks:
+                    continue
+                x = scale * (K[b, hk, ks] @ Q[b, h, t])
+                w = np.exp(x - x.max())
+                O[b, h, t] = (w[:, None] * V[b, hk, ks]).sum(0) / w.sum()
+    return O
+
+
+def test_sinkwin_spec_example(orc):
+    """empty BlockMask, sink = 1, window = 1, causal, row at position 5 -> tokens {0, 5}."""
+    T, d = 8, 16
+    Q, K, V = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=40, dtype=torch.float32)
+    idx = np.full((1, 1, T, 1), -1, np.int32)
+    cnt = np.zeros((1, 1, T), np.int32)
+    O, lse = orc.sparse_attention(Q, K, V, 1, 1, 1, True, idx, cnt, sink=1, window=1)
+    q, Kn, Vn = (x.double().numpy() for x in (Q[0, 0, 5], K[0, 0], V[0, 0]))
+    x = np.array([q @ Kn[0], q @ Kn[5]]) / math.sqrt(d)
+    w = np.exp(x - x.max())
+    ref = (w[0] * Vn[0] + w[1] * Vn[5]) / w.sum()
+    assert np.abs(O[0, 0, 5] - ref).max() < 1e-12
+    assert abs(lse[0, 0, 5] - (x.max() + math.log(w.sum()))) < 1e-12
+
+
+def test_sinkwin_zero_is_plain_and_full_window_is_dense(orc):
+    T, d, k, bq, bk = 300, 32, 64, 16, 2
+    Q, K, V = synth.gen_qkv(1, 2, 1, T, T, d, "llm", seed=41, dtype=torch.float32)
+    idx, cnt = orc.mask(Q, K, k, bq, bk, True)
+    a = orc.sparse_attention(Q, K, V, k, bq, bk, True, idx, cnt)
+    b = orc.sparse_attention(Q, K, V, k, bq, bk, True, idx, cnt, sink=0, window=0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # window >= T: every causal key of every row -> dense causal attention (library routine)
+    O, _ = orc.sparse_attention(Q, K, V, k, bq, bk, True, idx, cnt, sink=3, window=T)
+    assert np.abs(O - _sdpa64(Q, K, V, True, 1.0 / math.sqrt(d))).max() < 1e-12
+    # S:300: defaults (window 128, sink 32) at position 40 cover {0..40}: the row is dense causal
+    O, _ = orc.sparse_attention(Q, K, V, k, bq, bk, True, idx, cnt, sink=32, window=128)
+    assert np.abs(O[:, :, 40] - _sdpa64(Q, K, V, True, 1.0 / math.sqrt(d))[:, :, 40]).max() < 1e-12
+
+
+@pytest.mark.parametrize("Tq,Tk,bq,bk,k,causal,sink,window", [
+    (200, 200, 16, 2, 32, True, 4, 16),     # overlaps between blocks, sink and window (dedup)
+    (70, 250, 8, 4, 40, True, 32, 128),     # T_q < T_k (bottom-right), paper sizes
+    (120, 120, 32, 1, 16, False, 5, 9),     # non-causal
+    (33, 33, 32, 2, 2, True, 0, 3),         # ragged last block, window only
+])
+def test_sinkwin_union_brute_force(orc, Tq, Tk, bq, bk, k, causal, sink, window):
+    d = 16
+    Q, K, V = synth.gen_qkv(2, 2, 1, Tq, Tk, d, "iid", seed=42, dtype=torch.float32)
+    nqb = -(-Tq // bq)
+    hi = torch.tensor([[[_visible(q, bq, bk, Tq, Tk, causal) for q in range(nqb)]] * 2] * 2)
+    idx, cnt = synth.gen_block_indices(2, 2, nqb, k // bk, hi, seed=42)
+    O, _ = orc.sparse_attention(Q, K, V, k, bq, bk, causal, idx, cnt, sink=sink, window=window)
+    ref = _brute_effective_attention(Q, K, V, bq, bk, causal, idx.numpy(), cnt.numpy(), sink, window,
+                                     1.0 / math.sqrt(d))
+    assert np.abs(O - ref).max() < 1e-12
+
+
+def test_sinkwin_paged_equals_contiguous(orc):
+    B, Hq, Hkv, d, k, bk = 2, 4, 2, 32, 64, 2
+    seq = [300, 129]
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=43, dtype=torch.float32)
+    _, Kc, Vc = synth.gen_qkv(B, Hkv, Hkv, 1, T, d, "iid", seed=43, dtype=torch.float32)
+    kp, vp, bt, sl = synth.to_paged(Kc, Vc, seq, 16, seed=1)
+    idx, cnt = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True)
+    O, lse = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, idx, cnt, sink=32, window=128)
+    for b in range(B):
+        Ob, lb = orc.sparse_attention(Q[b:b + 1], Kc[b:b + 1, :, : seq[b]], Vc[b:b + 1, :, : seq[b]], k, 1, bk, True,
+                                      idx[b:b + 1], cnt[b:b + 1], sink=32, window=128)
+        assert np.array_equal(O[b:b + 1], Ob) and np.array_equal(lse[b:b + 1], lb)
