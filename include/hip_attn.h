@@ -68,6 +68,12 @@ typedef struct {
     float sm_scale;   /* attention softmax scale; <= 0 means 1/sqrt(d) (G11).  The mask uses raw
                          q.k and ignores it.                                         */
     uint32_t flags;   /* HIP_FLAG_*                                                                  */
+    int32_t sink_tokens;   /* attention only (0 = off): every row also attends to keys [0, sink)    */
+    int32_t window_tokens; /* attention only (0 = off): row at position p also attends to keys
+                              (p - window, p].  StreamingLLM sink + sliding window, fused into the
+                              sparse kernels (the paper uses (window, sink) = (128, 32);
+                              the union of S:285-301, each token once; reading G14).  Both >= 0,
+                              sink + window + b_q - 1 <= 256.  hip_mask_estimate ignores them.     */
 } hip_params_t;
 
 typedef struct {
@@ -149,9 +155,11 @@ hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_
  *                (normally the output of hip_mask_estimate with the same params; any ascending
  *                set of distinct blocks in [0, ceil(T_k / b_k)) is accepted)
  *   o            OUT [B, H_q, T_q, d] (dtype): row t = sum_s softmax_s(sm_scale q_t . k_s) v_s over
- *                the tokens s of the selected blocks with s < T_k and (causal) s <= t + T_k - T_q
+ *                the tokens s of the selected blocks with s < T_k and (causal) s <= t + T_k - T_q,
+ *                united with [0, params->sink_tokens) and (p - params->window_tokens, p] for the
+ *                row's position p = t + T_k - T_q when those are > 0 (each token once; G14)
  *   lse          OUT optional fp32 [B, H_q, T_q] contiguous (natural log-sum-exp of the scaled
- *                scores), NULL to skip.  A row with no visible selected token gets o = 0 and
+ *                scores), NULL to skip.  A row with no visible token gets o = 0 and
  *                lse = -inf (G13).
  *   Arithmetic: fp32 scores and softmax; bf16 probabilities into the PV contraction (bf16 path).
  *   Errors: as hip_mask_estimate; block indices are NOT range-checked on the device (garbage in,

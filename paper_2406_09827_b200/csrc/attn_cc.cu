@@ -9,6 +9,7 @@
 // WR row groups (prefill: one row per warp at a time) x WK key groups (decode: the keys of the
 // single row are split over warps), and the WK partial softmax states are merged at the end.
 #include "kernels.h"
+#include "sinkwin.cuh"
 
 namespace hip {
 
@@ -32,7 +33,9 @@ __global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(
   float* qs = reinterpret_cast<float*>(smem);                 // [R][QP]
   float* S = qs + R * QP;                                      // [R][kKC + 1]
   int* tok = reinterpret_cast<int*>(S + R * (kKC + 1));        // [S][kKC] token of each staged key (-1 none)
-  char* kst = smem + align_up((size_t)((char*)(tok + kACStages * kKC) - smem), 128);  // [S][kKC][KP]
+  int* xlist = tok + kACStages * kKC;                          // [kMaxExtra] sink / window tokens
+  int* wtot = xlist + kMaxExtra;                               // [32] scan scratch
+  char* kst = smem + align_up((size_t)((char*)(wtot + 32) - smem), 128);  // [S][kKC][KP]
   char* vst = kst + kACStages * kKC * KP;                      // [S][kKC][KP]
   float* part = reinterpret_cast<float*>(kst);                 // reused for the WK merge
 
@@ -54,6 +57,12 @@ __global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(
     const int c = min(max(__ldg(cnt + lin), 0), sh.n);
     const int nkeys = c * sh.bk;
     const int32_t* blk = idx + lin * sh.n;
+    const int lbk = 31 - __clz(sh.bk);
+    const int ne = (sh.sink > 0 || sh.window > 0)
+                       ? build_extra<kACThreads>(blk, c, lbk, Tk, tpos0, tpos0 + rows_q - 1, sh.causal, sh.sink,
+                                                 sh.window, xlist, wtot)
+                       : 0;
+    const int nall = nkeys + ne;
 
     for (int i = threadIdx.x; i < rows_q * D; i += kACThreads) {
       int t = i / D, cc = i - t * D;
@@ -73,10 +82,10 @@ __global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(
       for (int e = 0; e < E; ++e) acc[i][e] = 0.f;
     }
 
-    const int nch = (nkeys + kKC - 1) / kKC;
+    const int nch = (nall + kKC - 1) / kKC;
     auto issue = [&](int ch) {
       if (ch >= nch) return;
-      const int k0 = ch * kKC, kc = min(kKC, nkeys - k0);
+      const int k0 = ch * kKC, kc = min(kKC, nall - k0);
       constexpr int pieces = D * sizeof(T) / 16;
       const int slot = ch % kACStages;
       int* tk = tok + slot * kKC;
@@ -85,12 +94,18 @@ __global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(
         int rem = p - which * kKC * pieces;
         int r = rem / pieces, c16 = rem - r * pieces;
         int64_t s = -1;
+        bool extra = false;
         if (r < kc) {
-          int j = min(max(__ldg(blk + (k0 + r) / sh.bk), 0), nkb - 1);
-          s = (int64_t)j * sh.bk + (k0 + r) % sh.bk;
-          if (s >= Tk) s = -1;
+          if (k0 + r < nkeys) {
+            int j = min(max(__ldg(blk + (k0 + r) / sh.bk), 0), nkb - 1);
+            s = (int64_t)j * sh.bk + (k0 + r) % sh.bk;
+            if (s >= Tk) s = -1;
+          } else {
+            s = xlist[k0 + r - nkeys];
+            extra = true;
+          }
         }
-        if (which == 0 && c16 == 0) tk[r] = (int)s;
+        if (which == 0 && c16 == 0) tk[r] = s >= 0 && extra ? (int)s | kExtraBit : (int)s;
         const RowSrc& src = which ? vs : ks;
         char* dst = (which ? vst : kst) + (slot * kKC + r) * KP + c16 * 16;
         const char* g = row_ptr(src, b, hk, s >= 0 ? s : 0) + c16 * 16;
@@ -114,8 +129,11 @@ __global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(
       for (int p = threadIdx.x; p < rows_q * kKC; p += kACThreads) {
         int t = p % rows_q, r = p / rows_q;
         int s = tk[r];
+        const bool extra = s >= 0 && (s & kExtraBit);
+        if (extra) s &= ~kExtraBit;
         float x = -INFINITY;
-        if (s >= 0 && (!sh.causal || s <= tpos0 + t)) {
+        if (s >= 0 && (!sh.causal || s <= tpos0 + t) &&
+            (!extra || extra_visible(s, tpos0 + t, sh.causal, sh.sink, sh.window))) {
           const float4* qr = reinterpret_cast<const float4*>(qs + t * QP);
           float a = 0.f;
           if constexpr (sizeof(T) == 4) {
@@ -252,7 +270,8 @@ static cudaError_t launch_acc(const Shape& sh, const QSrc& qs, const RowSrc& ks,
   int WR = R >= 8 ? 8 : (R >= 4 ? 4 : (R >= 2 ? 2 : 1));
   constexpr int KP = D * sizeof(T) + 16;
   const size_t stages = 2 * (size_t)kACStages * kKC * KP;
-  size_t smem = align_up((size_t)R * (D + 4) * 4 + (size_t)R * (kKC + 1) * 4 + kACStages * kKC * 4, 128) + stages;
+  size_t smem = align_up((size_t)R * (D + 4) * 4 + (size_t)R * (kKC + 1) * 4 + kACStages * kKC * 4 +
+                              (kMaxExtra + 32) * 4, 128) + stages;
   size_t merge = (size_t)(8 / WR) * R * (D + 2) * 4;
   if (merge > stages) smem += merge - stages;
   smem = align_up(smem, 16);

@@ -9,6 +9,7 @@
 // The 8 half-warps of the CTA split the unit's keys and merge their states through shared memory
 // at the end; rows are normalised and stored coalesced.
 #include "kernels.h"
+#include "sinkwin.cuh"
 
 namespace hip {
 
@@ -28,6 +29,8 @@ __global__ void __launch_bounds__(kADThreads, 4) attn_decode_kernel(Shape sh, QS
   constexpr int NV = (E * (int)sizeof(T) + 15) / 16;
   constexpr int HW = kADThreads / 16;
   __shared__ float part[HW][RM][D + 2];
+  __shared__ int xlist[kMaxExtra];  // sink / window tokens of the unit (sinkwin.cuh)
+  __shared__ int wtot[32];
   const int lane16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
   const int lbk = 31 - __clz(sh.bk), bmask = sh.bk - 1;
 
@@ -44,6 +47,11 @@ __global__ void __launch_bounds__(kADThreads, 4) attn_decode_kernel(Shape sh, QS
     const int c = min(max(__ldg(cnt + lin), 0), sh.n);
     const int nkeys = c << lbk;
     const int32_t* blk = idx + lin * sh.n;
+    const int ne = (sh.sink > 0 || sh.window > 0)
+                       ? build_extra<kADThreads>(blk, c, lbk, Tk, tpos0, tpos0 + rows_q - 1, sh.causal, sh.sink,
+                                                 sh.window, xlist, wtot)
+                       : 0;
+    const int nall = nkeys + ne;
     const char* kbase = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
     const char* vbase = vs.base + (b * vs.sb + hk * vs.sh) * (int64_t)vs.esize;
     const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(kADThreads, 4) attn_decode_kernel(Shape sh, QS
     }
 
     // uniform trip count for every half-warp (the xor shuffles below span the full warp)
-    const int nbatch = (nkeys + HW * kADU - 1) / (HW * kADU);
+    const int nbatch = (nall + HW * kADU - 1) / (HW * kADU);
     for (int bt = 0; bt < nbatch; ++bt) {
       const int k0 = bt * HW * kADU + hw * kADU;
       uint4 kb[kADU][NV], vb[kADU][NV];
@@ -79,12 +87,16 @@ __global__ void __launch_bounds__(kADThreads, 4) attn_decode_kernel(Shape sh, QS
       for (int i = 0; i < kADU; ++i) {
         const int k = k0 + i;
         int s = -1;
+        bool extra = false;
         if (k < nkeys) {
           const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
           s = (j << lbk) + (k & bmask);
           if (s >= Tk) s = -1;
+        } else if (k < nall) {
+          s = xlist[k - nkeys];
+          extra = true;
         }
-        sv[i] = s;
+        sv[i] = extra ? (s | kExtraBit) : s;
         const int ss = s >= 0 ? s : 0;
         const char* kp;
         const char* vp;
@@ -127,7 +139,9 @@ __global__ void __launch_bounds__(kADThreads, 4) attn_decode_kernel(Shape sh, QS
           }
 #pragma unroll
           for (int off = 8; off >= 1; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-          const bool ok = sv[i] >= 0 && (!sh.causal || sv[i] <= tpos0 + t);
+          const int si = sv[i] & ~kExtraBit;
+          const bool ok = sv[i] >= 0 && (!sh.causal || si <= tpos0 + t) &&
+                          (!(sv[i] & kExtraBit) || extra_visible(si, tpos0 + t, sh.causal, sh.sink, sh.window));
           x[i] = ok ? a * scale_log2 : -INFINITY;
           bm = fmaxf(bm, x[i]);
         }

@@ -18,6 +18,7 @@
 // columns, ~53 KB shared) keep 4 query blocks per SM in flight: the gathers are L2-bound
 // (profiles/r01/gather_ceiling.json), and independent streams are what saturates L2.
 #include "kernels.h"
+#include "sinkwin.cuh"
 
 namespace hip {
 
@@ -37,8 +38,10 @@ struct AttnTCSmem {
   static constexpr uint32_t p = ring + 2 * kATSlot;               // one P chunk
   static constexpr uint32_t red = p + kATPChunk;                  // floats, see below
   static constexpr int kRedFloats = 3 * 4 * 32 + 6 * 32 + 32;     // [3][4][32] + m, l, lu, corr, invl, pad + flag
-  static constexpr uint32_t tok = red + kRedFloats * 4;           // [512] int token per key slot
-  static constexpr uint32_t misc = (uint32_t)align_up(tok + 512 * 4, 64);
+  static constexpr int kTok = 768;                                // selected (<= 512) + extra (<= 256) keys
+  static constexpr uint32_t tok = red + kRedFloats * 4;           // [kTok] row of each key slot
+  static constexpr uint32_t xlist = tok + kTok * 4;               // [kMaxExtra] sink / window tokens
+  static constexpr uint32_t misc = (uint32_t)align_up(xlist + kMaxExtra * 4, 64);
   static constexpr uint32_t total = misc + 64;
 };
 
@@ -59,7 +62,8 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   return v[0];
 }
 
-template <bool kPaged>
+// kSW: sink / sliding-window tokens enabled (a separate instantiation, so the plain path pays nothing).
+template <bool kPaged, bool kSW>
 __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
                                                                 const int32_t* __restrict__ idx,
                                                                 const int32_t* __restrict__ cnt, float scale_log2,
@@ -79,6 +83,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   float* invl = red + 512;
   int* flag = reinterpret_cast<int*>(red + 576);
   int* tok = reinterpret_cast<int*>(base + L::tok);
+  int* xlist = reinterpret_cast<int*>(base + L::xlist);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -109,7 +114,12 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     const int nkb = (Tk + sh.bk - 1) / sh.bk;
     const int c = min(max(__ldg(cnt + lin), 0), sh.n);
     const int nkeys = c * sh.bk;
-    const int nch = (nkeys + 127) / 128;
+    // sink / sliding-window tokens not covered by the selected blocks (sinkwin.cuh)
+    const int ne = kSW ? build_extra<kATThreads>(idx + lin * sh.n, c, lbk, Tk, tpos0, tpos0 + rows_q - 1, sh.causal,
+                                                 sh.sink, sh.window, xlist, reinterpret_cast<int*>(red))
+                       : 0;
+    const int nall = nkeys + ne;
+    const int nch = (nall + 127) / 128;
     const int32_t* blk = idx + lin * sh.n;
 
     if (nch == 0) {  // no selected block: O = 0, lse = -inf (G13)
@@ -134,10 +144,14 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     // cache (K and V share the block table and strides), so the gathers carry no dependent load
     for (int k = threadIdx.x; k < nch * 128; k += kATThreads) {
       int s = -1;
-      if (k < nkeys) {
-        const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
-        s = (j << lbk) + (k & ((1 << lbk) - 1));
-        if (s >= Tk) s = -1;
+      if (k < nall) {
+        if (k < nkeys) {
+          const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
+          s = (j << lbk) + (k & ((1 << lbk) - 1));
+          if (s >= Tk) s = -1;
+        } else if constexpr (kSW) {
+          s = xlist[k - nkeys];
+        }
         if constexpr (kPaged) {
           if (s >= 0) {
             const uint32_t us = (uint32_t)s;
@@ -146,6 +160,8 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
             const int64_t page = __ldg(ks.block_table + (int64_t)b * ks.max_pages + pi);
             s = (int)(page * ks.sp_rows + off);
           }
+        } else if constexpr (kSW) {
+          if (k >= nkeys && s >= 0) s |= kExtraBit;  // contiguous: the token itself, extras flagged
         }
       }
       tok[k] = s;
@@ -178,7 +194,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
           r = x & 63; dh = x >> 6; key = ch * 128 + (kind - 2) * 64 + r; g0 = vbase; rb = vrow;
           dst = slot + dh * 8192 + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4);
         }
-        const int s = tok[key];
+        const int s = kSW ? (tok[key] & ~kExtraBit) : tok[key];  // -1 stays negative
         cp_async16(dst, g0 + (uint64_t)(uint32_t)(s >= 0 ? s : 0) * rb + dh * 128 + c8 * 16, s >= 0 ? 16u : 0u);
       }
     };
@@ -211,21 +227,31 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         float v[32];
         tmem_ld_32x32b_x32(tmem_lane, v);
         int s;  // token position of this lane's key (-1: none)
-        if constexpr (kPaged) {
+        bool extra;  // a sink / window token: row-dependent visibility
+        {
           const int k = ch * 128 + 32 * warp + lane;
-          s = -1;
-          if (k < nkeys) {
-            const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
-            s = (j << lbk) + (k & ((1 << lbk) - 1));
-            if (s >= Tk) s = -1;
+          if constexpr (kPaged) {
+            s = -1;
+            extra = kSW && k >= nkeys;
+            if (k < nkeys) {
+              const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
+              s = (j << lbk) + (k & ((1 << lbk) - 1));
+              if (s >= Tk) s = -1;
+            } else if (kSW && k < nall) {
+              s = xlist[k - nkeys];
+            }
+          } else {
+            s = tok[k];
+            extra = kSW && s >= 0 && (s & kExtraBit);
+            if (extra) s &= ~kExtraBit;
           }
-        } else {
-          s = tok[ch * 128 + 32 * warp + lane];
         }
-        const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0);
+        const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0) &&
+                             (!extra || extra_visible(s, tpos0 + 31, sh.causal, sh.sink, sh.window));
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const bool ok = all_vis || (s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j));
+          const bool ok = all_vis || (s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j) &&
+                                      (!extra || extra_visible(s, tpos0 + j, sh.causal, sh.sink, sh.window)));
           v[j] = ok ? v[j] * scale_log2 : -INFINITY;
         }
         float x[32];
@@ -373,17 +399,19 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
 }
 
 // Any query block of <= 32 rows (decode included: the N = 32 operand is zero-padded, the tensor
-// cores are idle anyway); <= 512 selected keys (the staged row list).
+// cores are idle anyway); <= 512 selected keys plus <= 256 sink / window tokens (the staged list).
 bool attn_tc_supported(const Shape& sh) {
   return sh.d == 128 && sh.bq >= 1 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 &&
-         (int64_t)sh.n * sh.bk <= 512;
+         (int64_t)sh.n * sh.bk <= 512 && sh.sink + sh.window + sh.bq - 1 <= kMaxExtra;
 }
 
 cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
                            const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                            float* lse, cudaStream_t stream, int num_sms) {
   const size_t smem = AttnTCSmem::total + 1024;
-  auto kern = ks.paged ? attn_tc_kernel<true> : attn_tc_kernel<false>;
+  const bool sw = sh.sink > 0 || sh.window > 0;
+  auto kern = ks.paged ? (sw ? attn_tc_kernel<true, true> : attn_tc_kernel<true, false>)
+                       : (sw ? attn_tc_kernel<false, true> : attn_tc_kernel<false, false>);
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kATThreads, smem, 64, &per_sm);
   if (e != cudaSuccess) return e;

@@ -62,6 +62,7 @@ struct Shape {
   int B, Hq, Hkv, Tq, Tk, d;
   int n, bq, bk, causal;
   int nqb;
+  int sink, window;  // attention: sink / sliding-window tokens (sinkwin.cuh), 0 = off
   const int32_t* seq_lens;
 };
 

@@ -34,7 +34,8 @@ class HipError(RuntimeError):
 
 class Params(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("b_q", ctypes.c_int32), ("b_k", ctypes.c_int32), ("causal", ctypes.c_int32),
-                ("sm_scale", ctypes.c_float), ("flags", ctypes.c_uint32)]
+                ("sm_scale", ctypes.c_float), ("flags", ctypes.c_uint32), ("sink_tokens", ctypes.c_int32),
+                ("window_tokens", ctypes.c_int32)]
 
 
 class TensorDesc(ctypes.Structure):
@@ -107,9 +108,10 @@ def _stream(t: torch.Tensor, stream=None) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
-def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False) -> Params:
+def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False, sink: int = 0,
+            window: int = 0) -> Params:
     return Params(int(k), int(b_q), int(b_k), int(bool(causal)), float(sm_scale or 0.0),
-                  HIP_FLAG_EXACT_SCORES if exact else 0)
+                  HIP_FLAG_EXACT_SCORES if exact else 0, int(sink), int(window))
 
 
 def _require_cuda(*ts):
@@ -184,13 +186,15 @@ def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, 
 
 
 def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
-                             causal: bool = True, sm_scale=None, out=None, return_lse: bool = False, stream=None):
-    """hip_sparse_attention_prefill.  Returns o (and lse fp32 [B,Hq,Tq] if return_lse)."""
+                             causal: bool = True, sm_scale=None, sink: int = 0, window: int = 0, out=None,
+                             return_lse: bool = False, stream=None):
+    """hip_sparse_attention_prefill.  Returns o (and lse fp32 [B,Hq,Tq] if return_lse).  sink/window
+    add StreamingLLM sink and sliding-window tokens to every row (the paper: 32 / 128)."""
     _require_cuda(q, k, v, idx, cnt)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
-    p = _params(k_budget, b_q, b_k, causal, sm_scale)
+    p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window)
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
     with torch.cuda.device(q.device):
@@ -202,13 +206,13 @@ def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int
 
 def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, idx, cnt, *,
                             k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True, sm_scale=None,
-                            out=None, return_lse: bool = False, stream=None):
+                            sink: int = 0, window: int = 0, out=None, return_lse: bool = False, stream=None):
     """hip_sparse_attention_decode on a paged cache.  q [B,Hq,Tq,d] -> o (and lse)."""
     _require_cuda(q, k_pages, v_pages, block_table, seq_lens, idx, cnt)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
-    p = _params(k_budget, b_q, b_k, causal, sm_scale)
+    p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window)
     pg, bt = _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len)
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
@@ -222,8 +226,9 @@ def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_
 
 
 def hip_attention(q, k, v, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True,
-                  sm_scale=None, out=None, stream=None):
-    """One HiP attention layer (prefill): mask estimation then block-sparse attention."""
+                  sm_scale=None, sink: int = 0, window: int = 0, out=None, stream=None):
+    """One HiP attention layer (prefill): mask estimation then block-sparse attention (with the
+    optional sink / sliding-window tokens)."""
     idx, cnt = mask_estimate(q, k, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal, stream=stream)
     return sparse_attention_prefill(q, k, v, idx, cnt, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal,
-                                    sm_scale=sm_scale, out=out, stream=stream)
+                                    sm_scale=sm_scale, sink=sink, window=window, out=out, stream=stream)

@@ -326,3 +326,54 @@ def test_full_size_c2_sampled(orc):
         assert np.abs(o[0, h, q * bq:t1].float().cpu().numpy() - Oo[0, 0]).max() <= 2e-2
     print(f"\n[parity] C2 sampled: {n_bad}/{len(units)} query blocks differ, unexplained {n_unexpl}")
     assert n_unexpl == 0
+
+
+# ------------------------------------------------------------------------------------------------
+# Sink + sliding window fused into the sparse kernels (f1; oracle: the S:285-301 union)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("Tq,Tk,bq,bk,k,causal,sink,window", [
+    (1000, 1000, 32, 2, 512, True, 32, 128),   # the paper's sizes
+    (333, 900, 32, 4, 256, True, 4, 16),       # T_q < T_k, small sizes, overlaps with the blocks
+    (257, 257, 16, 2, 128, False, 8, 33),      # non-causal
+    (300, 300, 32, 2, 2, True, 0, 64),         # one block per query block: mostly window
+])
+def test_attention_sinkwin_prefill_parity(orc, dt, Tq, Tk, bq, bk, k, causal, sink, window):
+    B, Hq, Hkv, d = 1, 2, 1, 128
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, Tq, Tk, d, "llm", seed=20, dtype=dt)
+    idx, cnt = _synthetic_selection(B, Hq, Tq, Tk, k, bq, bk, causal, seed=20)
+    o, lse = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx.cuda(), cnt.cuda(), k_budget=k, b_q=bq,
+                                        b_k=bk, causal=causal, sink=sink, window=window, return_lse=True)
+    torch.cuda.synchronize()
+    Oo, lo = orc.sparse_attention(Q, K, V, k, bq, bk, causal, idx, cnt, sink=sink, window=window)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+    fin = np.isfinite(lo)
+    lg = lse.cpu().numpy()
+    assert np.array_equal(np.isfinite(lg), fin)
+    assert np.abs(lg[fin] - lo[fin]).max() <= 1e-3
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_attention_sinkwin_decode_parity(orc, dt):
+    B, Hq, Hkv, d, k, bk, ps = 4, 8, 2, 128, 512, 2, 64
+    seq = [5000, 1, 200, 4096]
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=21, dtype=dt)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=21, dtype=dt)
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True)
+    o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T,
+                                       torch.from_numpy(oi).cuda(), torch.from_numpy(oc).cuda(), k_budget=k, b_q=1,
+                                       b_k=bk, causal=True, sink=32, window=128, return_lse=True)
+    torch.cuda.synchronize()
+    Oo, lo = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, oi, oc, sink=32, window=128)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+    assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
+
+
+def test_attention_sinkwin_validation():
+    Q, K, V = (x.cuda() for x in synth.gen_qkv(1, 1, 1, 64, 64, 128, "iid", seed=22))
+    idx, cnt = H.mask_estimate(Q, K, k_budget=64, b_q=32, b_k=2)
+    with pytest.raises(H.HipError):
+        H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=64, b_q=32, b_k=2, sink=-1)
+    with pytest.raises(H.HipError):
+        H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=64, b_q=32, b_k=2, sink=200, window=100)
