@@ -1,0 +1,58 @@
+"""decode.py — the HiP decoding loop policy (Alg. 2).
+
+Per HiP layer and decode step: if the current sequence length is divisible by the mask estimation
+period r_m, estimate the attention mask (Alg. 1, O(T log T)) and cache it (O(T) space);
+then run the fused sparse attention with the cached mask.  The paper's default is r_m = 8
+(P:815); r_m = 1 re-estimates every step (its latency benchmarks).  Multi-query
+(speculative) steps pass T_q > 1 query rows per sequence, at positions seq_len - T_q + t
+(P:1154-1159); b_q <= 32 rows form one query block.
+
+A batch holds sequences of different lengths, so the refresh decision is taken per sequence: the
+new mask is estimated for the batch and kept only for the sequences whose length is divisible by
+r_m (the others keep their cached rows).  Policy only: every step runs in the C-ABI kernels
+(hipattn); nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import hipattn as H
+
+
+class HipDecoder:
+    """Cached-mask HiP attention for one layer of a decoder (Alg. 2 lines 8-12)."""
+
+    def __init__(self, r_m: int = 8, k_budget: int = 512, b_k: int = 2, b_q: int = 32, causal: bool = True,
+                 sink: int = 0, window: int = 0, sm_scale=None):
+        if r_m < 1:
+            raise ValueError("r_m must be >= 1")
+        self.r_m, self.k_budget, self.b_k, self.b_q = int(r_m), int(k_budget), int(b_k), int(b_q)
+        self.causal, self.sink, self.window, self.sm_scale = bool(causal), int(sink), int(window), sm_scale
+        self.idx = None
+        self.cnt = None
+        self.refreshes = 0  # number of steps that ran the mask estimation (for tests / stats)
+
+    def refresh_rows(self, seq_lens_host) -> list:
+        """Per-sequence refresh decision for this step (Alg. 2 line 8)."""
+        return [self.idx is None or int(t) % self.r_m == 0 for t in seq_lens_host]
+
+    def step(self, q, k_pages, v_pages, block_table, seq_lens, seq_lens_host, *, return_lse: bool = False,
+             stream=None):
+        """One decode step: q [B, H_q, T_q, d] against the paged cache whose sequence b holds
+        seq_lens[b] tokens (seq_lens_host: the same lengths on the host, which decide refreshes)."""
+        max_len = int(max(int(t) for t in seq_lens_host))
+        rows = self.refresh_rows(seq_lens_host)
+        if any(rows):
+            idx, cnt = H.mask_estimate_paged(q, k_pages, block_table, seq_lens, max_len, k_budget=self.k_budget,
+                                             b_q=self.b_q, b_k=self.b_k, causal=self.causal, stream=stream)
+            if self.idx is None or self.idx.shape != idx.shape or all(rows):
+                self.idx, self.cnt = idx, cnt
+            else:
+                sel = torch.tensor(rows, device=idx.device)
+                self.idx = torch.where(sel.view(-1, 1, 1, 1), idx, self.idx)
+                self.cnt = torch.where(sel.view(-1, 1, 1), cnt, self.cnt)
+            self.refreshes += 1
+        return H.sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_len, self.idx, self.cnt,
+                                         k_budget=self.k_budget, b_q=self.b_q, b_k=self.b_k, causal=self.causal,
+                                         sm_scale=self.sm_scale, sink=self.sink, window=self.window,
+                                         return_lse=return_lse, stream=stream)

@@ -146,3 +146,17 @@ def test_product_package_never_imports_oracle():
                 src = open(os.path.join(dp, f)).read()
                 for pat in (r"import\s+oracle", r"from\s+oracle", "liboracle", "hip_oracle", r'#include\s+".*oracle'):
                     assert not re.search(pat, src), (f, pat)
+
+
+def test_decoder_refresh_rule_host():
+    """Alg. 2 line 8: refresh when the sequence length is divisible by r_m; always on the
+    first step (nothing cached).  Host logic only."""
+    from paper_2406_09827_b200.decode import HipDecoder
+    d = HipDecoder(r_m=8)
+    assert d.refresh_rows([5, 13]) == [True, True]
+    d.idx = object()  # pretend a mask is cached
+    assert d.refresh_rows([8, 13, 16, 1]) == [True, False, True, False]
+    assert HipDecoder(r_m=1).refresh_rows([3]) == [True]
+    import pytest
+    with pytest.raises(ValueError):
+        HipDecoder(r_m=0)

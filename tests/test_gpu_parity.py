@@ -377,3 +377,59 @@ def test_attention_sinkwin_validation():
         H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=64, b_q=32, b_k=2, sink=-1)
     with pytest.raises(H.HipError):
         H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=64, b_q=32, b_k=2, sink=200, window=100)
+
+
+# ------------------------------------------------------------------------------------------------
+# f2: multi-query (speculative) decode and the r_m mask-caching loop (Alg. 2)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dt,dist", [(torch.bfloat16, "int"), (torch.float32, "iid")])
+@pytest.mark.parametrize("Tq", [4, 16])
+def test_multi_query_decode_parity(orc, dt, dist, Tq):
+    """T_q > 1 query rows per sequence at positions seq_len - T_q + t, b_q = T_q."""
+    B, Hq, Hkv, d, k, bk, ps = 3, 4, 2, 128, 256, 2, 16
+    seq = [3000, 40, 777]
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=30, dtype=dt, dist=dist, Tq=Tq)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=30, dtype=dt, dist=dist)
+    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=Tq, b_k=bk)
+    torch.cuda.synchronize()
+    mode = orc.F32L if dt == torch.float32 and Tq <= 4 else orc.F32C
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, Tq, bk, True, mode=mode)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T, idx, cnt, k_budget=k,
+                                       b_q=Tq, b_k=bk, sink=4, window=32, return_lse=True)
+    torch.cuda.synchronize()
+    Oo, lo = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, Tq, bk, True, oi, oc, sink=4, window=32)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+    assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
+
+
+def test_decoder_rm_cache_schedule(orc):
+    """HipDecoder: the mask is re-estimated exactly when a sequence's length is divisible by r_m
+    (Alg. 2 line 8) and reused in between; every step's output is the oracle's attention over the
+    cached selection at the current length (the steps 'append' tokens already present in pages)."""
+    from paper_2406_09827_b200.decode import HipDecoder
+    B, Hq, Hkv, d, k, bk, ps, r_m = 2, 4, 2, 128, 128, 2, 16, 4
+    full = [700, 901]
+    kp, vp, bt, _ = synth.gen_paged_direct(B, Hkv, full, d, ps, seed=31, dist="int")
+    dec = HipDecoder(r_m=r_m, k_budget=k, b_k=bk, b_q=1, sink=4, window=16)
+    lens = [690, 893]
+    cached = None
+    for step in range(8):
+        cur = [lens[0] + step, lens[1] + step]
+        q = synth.gen_decode_q(B, Hq, d, seed=100 + step, dist="int")
+        sl = torch.tensor(cur, dtype=torch.int32)
+        expect_refresh = [cached is None or t % r_m == 0 for t in cur]
+        o = dec.step(q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), cur)
+        torch.cuda.synchronize()
+        oi, oc = orc.mask_paged(q, kp, bt, sl, k, 1, bk, True)  # integer inputs: exact in any order
+        gi, gc = dec.idx.cpu().numpy(), dec.cnt.cpu().numpy()
+        for b in range(B):
+            if expect_refresh[b]:
+                assert np.array_equal(gi[b], oi[b]) and np.array_equal(gc[b], oc[b])
+            else:
+                assert np.array_equal(gi[b], cached[0][b]) and np.array_equal(gc[b], cached[1][b])
+        cached = (gi.copy(), gc.copy())
+        Oo, _ = orc.sparse_attention_paged(q, kp, vp, bt, sl, k, 1, bk, True, gi, gc, sink=4, window=16)
+        assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
+    assert 1 < dec.refreshes < 8
