@@ -175,35 +175,24 @@ typedef struct {
  * trace_nodes (optional) receives the node ranges after every iteration: [max_trace+1][n][2]
  * (row 0 = initial partition); trace_scores [max_trace][n] the kept scores.
  */
-static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t q, int n, int bq,
-                     int bk, int causal, int mode, int32_t *out_idx, int32_t *out_cnt, orc_diag *diag,
-                     int32_t *trace_nodes, double *trace_scores, int max_trace)
+/* Alg. 1 lines 4-17 over the key blocks [lo, lo + L) with n nodes (L > n): initial nodes
+ * f_j = lo + floor((2 j L + n) / (2 n)), split / score / keep the n best until all are single
+ * blocks; writes the n selected blocks ascending to out_idx.  memo is indexed by absolute block. */
+static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t t0, int64_t t1,
+                        int64_t lo, int64_t L, int n, int bk, int causal, int mode, double *memo,
+                        int32_t *out_idx, orc_diag *dg, int32_t *trace_nodes, double *trace_scores,
+                        int max_trace)
 {
-    int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
-    int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
-    orc_diag dg = {INFINITY, 0.0, 0, 0};
-    if (mode == ORC_F32L && d % 16) return ORC_EINVAL;
-
-    if (Bq <= n) { /* exact case */
-        for (int64_t j = 0; j < n; ++j) out_idx[j] = j < Bq ? (int32_t)j : -1;
-        *out_cnt = (int32_t)Bq;
-        if (diag) *diag = dg;
-        return ORC_OK;
-    }
-
-    double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
     orc_node *nodes = (orc_node *)malloc(sizeof(orc_node) * (size_t)n);
     orc_node *cand = (orc_node *)malloc(sizeof(orc_node) * 2 * (size_t)n);
     int64_t *firsts = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
-    if (!memo || !nodes || !cand || !firsts) {
-        free(memo); free(nodes); free(cand); free(firsts);
+    if (!nodes || !cand || !firsts) {
+        free(nodes); free(cand); free(firsts);
         return ORC_ENOMEM;
     }
-    for (int64_t j = 0; j < Bq; ++j) memo[j] = NAN;
-
     for (int j = 0; j < n; ++j) {
-        int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
-        int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
+        int64_t fj = lo + (2 * (int64_t)j * L + n) / (2 * (int64_t)n);
+        int64_t fj1 = lo + (2 * (int64_t)(j + 1) * L + n) / (2 * (int64_t)n);
         nodes[j].f = fj;
         nodes[j].l = fj1 - 1;
         nodes[j].s = NAN;
@@ -235,35 +224,78 @@ static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, in
             if (isnan(memo[r])) {
                 double e = 0.0;
                 memo[r] = block_score(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, &e);
-                if (e > dg.emax) dg.emax = e;
-                dg.n_scored++;
+                if (e > dg->emax) dg->emax = e;
+                dg->n_scored++;
             }
             cand[c].s = memo[r];
         }
         qsort(cand, (size_t)nc, sizeof(orc_node), node_cmp);
         if (nc > n) {
             double gap = cand[n - 1].s - cand[n].s;
-            if (gap < dg.margin_min) dg.margin_min = gap;
+            if (gap < dg->margin_min) dg->margin_min = gap;
         }
         memcpy(nodes, cand, sizeof(orc_node) * (size_t)n);
-        if (trace_nodes && dg.n_iter < max_trace) {
-            int32_t *tn = trace_nodes + (size_t)(dg.n_iter + 1) * 2 * n;
+        if (trace_nodes && dg->n_iter < max_trace) {
+            int32_t *tn = trace_nodes + (size_t)(dg->n_iter + 1) * 2 * n;
             for (int j = 0; j < n; ++j) {
                 tn[2 * j] = (int32_t)nodes[j].f;
                 tn[2 * j + 1] = (int32_t)nodes[j].l;
-                if (trace_scores) trace_scores[(size_t)dg.n_iter * n + j] = nodes[j].s;
+                if (trace_scores) trace_scores[(size_t)dg->n_iter * n + j] = nodes[j].s;
             }
         }
-        dg.n_iter++;
+        dg->n_iter++;
     }
 
     for (int j = 0; j < n; ++j) firsts[j] = nodes[j].f;
     qsort(firsts, (size_t)n, sizeof(int64_t), i64_cmp);
     for (int j = 0; j < n; ++j) out_idx[j] = (int32_t)firsts[j];
+    free(nodes); free(cand); free(firsts);
+    return ORC_OK;
+}
+
+/* One query block.  chunks = S >= 1 (stridden partial top-k; reading G21): when
+ * B_q > n the visible blocks are split into S contiguous chunks [a_s, a_{s+1}),
+ * a_s = floor((2 s B_q + S) / (2 S)), and Alg. 1 runs on each with n / S nodes; the chunks' selections
+ * are concatenated (ascending).  S = 1 is Alg. 1 itself. */
+static int mask_unit_chunked(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t q, int n, int bq,
+                             int bk, int causal, int mode, int chunks, int32_t *out_idx, int32_t *out_cnt,
+                             orc_diag *diag, int32_t *trace_nodes, double *trace_scores, int max_trace)
+{
+    int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
+    int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
+    orc_diag dg = {INFINITY, 0.0, 0, 0};
+    if (mode == ORC_F32L && d % 16) return ORC_EINVAL;
+    if (chunks < 1 || n % chunks) return ORC_EINVAL;
+
+    if (Bq <= n) { /* exact case */
+        for (int64_t j = 0; j < n; ++j) out_idx[j] = j < Bq ? (int32_t)j : -1;
+        *out_cnt = (int32_t)Bq;
+        if (diag) *diag = dg;
+        return ORC_OK;
+    }
+
+    double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
+    if (!memo) return ORC_ENOMEM;
+    for (int64_t j = 0; j < Bq; ++j) memo[j] = NAN;
+    int ns = n / chunks, rc = ORC_OK;
+    for (int c = 0; c < chunks && rc == ORC_OK; ++c) {
+        int64_t a0 = (2 * (int64_t)c * Bq + chunks) / (2 * (int64_t)chunks);
+        int64_t a1 = (2 * (int64_t)(c + 1) * Bq + chunks) / (2 * (int64_t)chunks);
+        rc = search_range(Qh, Kh, Tq, Tk, d, t0, t1, a0, a1 - a0, ns, bk, causal, mode, memo, out_idx + c * ns,
+                          &dg, chunks == 1 ? trace_nodes : NULL, trace_scores, max_trace);
+    }
     *out_cnt = n;
     if (diag) *diag = dg;
-    free(memo); free(nodes); free(cand); free(firsts);
-    return ORC_OK;
+    free(memo);
+    return rc;
+}
+
+static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t q, int n, int bq,
+                     int bk, int causal, int mode, int32_t *out_idx, int32_t *out_cnt, orc_diag *diag,
+                     int32_t *trace_nodes, double *trace_scores, int max_trace)
+{
+    return mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, 1, out_idx, out_cnt, diag,
+                             trace_nodes, trace_scores, max_trace);
 }
 
 /* -------------------------------------------------------------------------------------------- */
@@ -298,6 +330,37 @@ int oracle_mask(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, 
         if (emax) emax[u] = dg.emax;
         if (n_scored) n_scored[u] = dg.n_scored;
         if (n_iter) n_iter[u] = dg.n_iter;
+    }
+    return err;
+}
+
+/* oracle_mask with stridden partial top-k over S = chunks contiguous chunks (G21). */
+int oracle_mask_chunked(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
+                        int bq, int bk, int causal, int mode, int chunks, int32_t *idx, int32_t *cnt,
+                        double *margin_min, double *emax)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    int n = k / bk;
+    if (chunks < 1 || n % chunks) return ORC_EINVAL;
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int64_t units = (int64_t)B * Hq * nqb;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t u = 0; u < units; ++u) {
+        int64_t q = u % nqb, bh = u / nqb;
+        int64_t b = bh / Hq, h = bh % Hq, hk = h / (Hq / Hkv);
+        const float *Qh = Q + ((b * Hq + h) * (int64_t)Tq) * d;
+        const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
+        orc_diag dg;
+        int r = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, chunks, idx + u * n, cnt + u,
+                                  &dg, NULL, NULL, 0);
+        if (r) {
+#pragma omp critical
+            err = r;
+        }
+        if (margin_min) margin_min[u] = dg.margin_min;
+        if (emax) emax[u] = dg.emax;
     }
     return err;
 }

@@ -51,6 +51,7 @@ def lib():
         i32, i64, f64 = ctypes.c_int, ctypes.c_int64, ctypes.c_double
         P = ctypes.c_void_p
         _lib.oracle_mask.argtypes = [P, P] + [i32] * 11 + [P] * 6
+        _lib.oracle_mask_chunked.argtypes = [P, P] + [i32] * 12 + [P] * 4
         _lib.oracle_mask_trace.argtypes = [P, P] + [i32] * 11 + [i32] * 3 + [P, P, P, P, i32, P, P]
         _lib.oracle_exact_block_topn.argtypes = [P, P] + [i32] * 11 + [P, P]
         _lib.oracle_block_scores.argtypes = [P, P] + [i32] * 10 + [P, i64, P, P]
@@ -66,7 +67,7 @@ def lib():
         _lib.oracle_set_num_threads.argtypes = [i32]
         for name in ("oracle_mask", "oracle_mask_trace", "oracle_exact_block_topn", "oracle_block_scores",
                      "oracle_sparse_attention", "oracle_dense_attention", "oracle_mask_paged",
-                     "oracle_sparse_attention_paged", "oracle_sparse_attention_sw",
+                     "oracle_sparse_attention_paged", "oracle_sparse_attention_sw", "oracle_mask_chunked",
                      "oracle_sparse_attention_paged_sw"):
             getattr(_lib, name).restype = i32
     return _lib
@@ -105,10 +106,11 @@ def n_blocks(k: int, bk: int) -> int:
     return k // bk
 
 
-def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: bool = False):
+def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: bool = False, chunks: int = 1):
     """Alg. 1 mask. Q [B,Hq,Tq,d], K [B,Hkv,Tk,d] -> idx [B,Hq,Nqb,n] (asc, -1 pad), cnt [B,Hq,Nqb].
 
-    diag=True also returns dict(margin_min, emax, n_scored, n_iter) per unit."""
+    diag=True also returns dict(margin_min, emax, n_scored, n_iter) per unit.  chunks = S > 1: the
+    stridden partial top-k (reading G21; diag then carries margin_min and emax only)."""
     Q, K = _f32(Q), _f32(K)
     B, Hq, Tq, d = Q.shape
     _, Hkv, Tk, _ = K.shape
@@ -120,6 +122,13 @@ def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: b
     em = np.empty((B, Hq, nqb), np.float64)
     ns = np.empty((B, Hq, nqb), np.int64)
     ni = np.empty((B, Hq, nqb), np.int32)
+    if chunks != 1:
+        rc = lib().oracle_mask_chunked(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, int(chunks),
+                                       _p(idx), _p(cnt), _p(mg), _p(em))
+        _check(rc, "oracle_mask_chunked")
+        if diag:
+            return idx, cnt, dict(margin_min=mg, emax=em)
+        return idx, cnt
     rc = lib().oracle_mask(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, _p(idx), _p(cnt),
                            _p(mg), _p(em), _p(ns), _p(ni))
     _check(rc, "oracle_mask")

@@ -18,8 +18,11 @@ MUTANTS = {
     "tile max over the first query row only": ("for (int64_t t = t0; t < t1; ++t) {\n        const float *q = Qh",
                                                "for (int64_t t = t0; t < t0 + 1; ++t) {\n        const float *q = Qh"),
     "causal bound off by one block": ("int64_t v = (tlast + (Tk - Tq)) / bk + 1;", "int64_t v = (tlast + (Tk - Tq)) / bk;"),
-    "initial partition rounds down": ("int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);",
-                                      "int64_t fj = (2 * (int64_t)j * Bq) / (2 * (int64_t)n);"),
+    "initial partition rounds down": ("int64_t fj = lo + (2 * (int64_t)j * L + n) / (2 * (int64_t)n);",
+                                      "int64_t fj = lo + (2 * (int64_t)j * L) / (2 * (int64_t)n);"),
+    "chunk boundaries round down": ("int64_t a0 = (2 * (int64_t)c * Bq + chunks) / (2 * (int64_t)chunks);",
+                                    "int64_t a0 = (2 * (int64_t)c * Bq) / (2 * (int64_t)chunks);"),
+    "chunk nodes start at block 0": ("int64_t fj = lo + (2", "int64_t fj = 0 + (2"),
     "keep bottom-n": ("if (a->s > b->s) return -1;\n    if (a->s < b->s) return 1;",
                       "if (a->s < b->s) return -1;\n    if (a->s > b->s) return 1;"),
     "attention drops the max subtraction": ("double p = exp(x[i] - M);", "double p = exp(x[i]);"),

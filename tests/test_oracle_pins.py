@@ -556,3 +556,43 @@ def test_sinkwin_paged_equals_contiguous(orc):
         Ob, lb = orc.sparse_attention(Q[b:b + 1], Kc[b:b + 1, :, : seq[b]], Vc[b:b + 1, :, : seq[b]], k, 1, bk, True,
                                       idx[b:b + 1], cnt[b:b + 1], sink=32, window=128)
         assert np.array_equal(O[b:b + 1], Ob) and np.array_equal(lse[b:b + 1], lb)
+
+
+# --------------------------------------------------------------------------------------------
+# Stridden partial top-k (f3; "splits the key-value sequence into S chunks"; reading
+# G21: S contiguous chunks a_s = floor((2 s B_q + S) / (2 S)), Alg. 1 with n / S nodes on each).
+# --------------------------------------------------------------------------------------------
+def test_chunks_one_is_plain(orc):
+    Q, K, _ = synth.gen_qkv(1, 2, 1, 2048, 2048, 64, "llm", seed=50, dtype=torch.float32, make_v=False)
+    a = orc.mask(Q, K, 128, 32, 2, True)
+    b = orc.mask(Q, K, 128, 32, 2, True, chunks=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("S", [2, 4])
+def test_chunks_one_level_is_exact_topn_per_chunk(orc, S):
+    """n_s < chunk <= 2 n_s: one iteration per chunk scores every block of the chunk once, so each
+    chunk keeps the exact top-n_s of its block maxima (brute force, integer inputs with ties)."""
+    Tq, Tk, d, bq, bk, k = 500, 523, 32, 24, 2, 64  # n = 32; B_q of every parity (boundary rounding)
+    Q, K, _ = synth.gen_qkv(1, 1, 1, Tq, Tk, d, "int", seed=51, dtype=torch.float32, make_v=False)
+    idx, cnt = orc.mask(Q, K, k, bq, bk, True, chunks=S)
+    n, ns = k // bk, k // bk // S
+    scores = _brute_block_scores(Q.double().numpy(), K.double().numpy(), bq, bk, True)[0, 0]
+    checked = 0
+    for q in range(-(-Tq // bq)):
+        Bq = _visible(q, bq, bk, Tq, Tk, True)
+        if Bq <= n:
+            assert cnt[0, 0, q] == Bq
+            continue
+        for s in range(S):
+            a0 = (2 * s * Bq + S) // (2 * S)
+            a1 = (2 * (s + 1) * Bq + S) // (2 * S)
+            got = idx[0, 0, q, s * ns:(s + 1) * ns]
+            assert (got >= a0).all() and (got < a1).all() and (np.diff(got) > 0).all()
+            if a1 - a0 <= 2 * ns:
+                row = np.full(scores.shape[1], -np.inf)
+                row[a0:a1] = scores[q, a0:a1]
+                assert np.array_equal(got, _topn_sorted(row, ns))
+                checked += 1
+        assert cnt[0, 0, q] == n
+    assert checked > 0
