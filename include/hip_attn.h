@@ -74,6 +74,11 @@ typedef struct {
                               sparse kernels (the paper uses (window, sink) = (128, 32);
                               the union of S:285-301, each token once; reading G14).  Both >= 0,
                               sink + window + b_q - 1 <= 256.  hip_mask_estimate ignores them.     */
+    int32_t chunks;        /* mask only: stridden partial top-k (reading G21).  0 or 1 =
+                              Alg. 1.  S > 1 (S | n): when B_q > n the visible key blocks are split
+                              into S contiguous chunks [a_s, a_{s+1}), a_s = floor((2 s B_q + S)/(2 S)),
+                              each searched with n / S nodes by its own job (S x more parallel jobs);
+                              the output concatenates the chunks (still ascending, cnt = n).        */
 } hip_params_t;
 
 typedef struct {

@@ -84,6 +84,9 @@ hip_status_t check_common(hip_dtype_t dt, int32_t B, int32_t Hq, int32_t Hkv, in
   if (((int64_t)Tk + p->b_k - 1) / p->b_k >= (1 << 22))
     return fail(HIP_ERROR_NOT_SUPPORTED, "ceil(T_k / b_k) >= 2^22 key blocks (T_k=%d, b_k=%d)", Tk, p->b_k);
   if (std::min(p->b_q, Tq) > 64) return fail(HIP_ERROR_NOT_SUPPORTED, "query block of %d rows > 64", std::min(p->b_q, Tq));
+  if (p->chunks < 0 || (p->chunks > 1 && (p->k / p->b_k) % p->chunks))
+    return fail(HIP_ERROR_INVALID_VALUE, "chunks=%d must be >= 0 and divide n = k/b_k = %d", p->chunks,
+                p->k / p->b_k);
   if (p->sink_tokens < 0 || p->window_tokens < 0)
     return fail(HIP_ERROR_INVALID_VALUE, "sink_tokens=%d window_tokens=%d must be >= 0", p->sink_tokens,
                 p->window_tokens);
@@ -120,6 +123,7 @@ hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk
   s.n = p->k / p->b_k; s.bq = std::min(p->b_q, Tq); s.bk = p->b_k; s.causal = p->causal;
   s.nqb = (Tq + s.bq - 1) / s.bq;
   s.sink = p->sink_tokens; s.window = p->window_tokens;
+  s.chunks = p->chunks > 1 ? p->chunks : 1;
   s.seq_lens = seq_lens;
   return s;
 }

@@ -63,6 +63,7 @@ struct Shape {
   int n, bq, bk, causal;
   int nqb;
   int sink, window;  // attention: sink / sliding-window tokens (sinkwin.cuh), 0 = off
+  int chunks;        // mask: stridden partial top-k chunks S (select.cuh chunk_job), 1 = Alg. 1
   const int32_t* seq_lens;
 };
 

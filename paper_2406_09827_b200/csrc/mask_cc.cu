@@ -124,7 +124,10 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
   float* pairs = reinterpret_cast<float*>(stage0 + kCCStages * stage_bytes);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  const int S = max(sh.chunks, 1);
+  for (int64_t jb = blockIdx.x; jb < units * S; jb += gridDim.x) {
+    const int64_t u = jb / S;
+    const int cs = (int)(jb - u * S);
     int b, h, q;
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
@@ -132,6 +135,8 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
     const int Bq = visible_blocks(sh, q, Tk);
     const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    int lo, len, nn, slot0;
+    if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     if (Bq > sh.n) {
       for (int i = threadIdx.x; i < rows_q * sh.d; i += kCCThreads) {
         int t = i / sh.d, c = i - t * sh.d;
@@ -148,7 +153,8 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
     sc.pairs = pairs; sc.ks = ks; sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.d = sh.d; sc.bk = sh.bk;
     sc.causal = sh.causal; sc.rows_q = rows_q; sc.ch = ch;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
-    tree_search<NMAX, kCCThreads>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
+    tree_search<NMAX, kCCThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr);
+    if (cs == 0 && threadIdx.x == 0) cnt[lin] = min(Bq, sh.n);
     __syncthreads();
   }
 }
@@ -173,7 +179,7 @@ static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   cudaError_t e = persistent_ctas(kern, kCCThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
+  int64_t grid = std::min<int64_t>(units * std::max(sh.chunks, 1), (int64_t)num_sms * per_sm);
   kern<<<(unsigned)grid, kCCThreads, smem, stream>>>(sh, qs, ks, idx, cnt, ch, kpitch, stage_bytes);
   return cudaGetLastError();
 }

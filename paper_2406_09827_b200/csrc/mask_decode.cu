@@ -118,7 +118,10 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
   float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
   const int lbk = 31 - __clz(sh.bk);
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  const int S = max(sh.chunks, 1);
+  for (int64_t jb = blockIdx.x; jb < units * S; jb += gridDim.x) {
+    const int64_t u = jb / S;
+    const int cs = (int)(jb - u * S);
     int b, h, q;
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
@@ -126,6 +129,8 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
     const int Bq = visible_blocks(sh, q, Tk);
     const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    int lo, len, nn, slot0;
+    if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     if (Bq > sh.n) {
       for (int i = threadIdx.x; i < rows_q * D; i += kMDThreads) {
         const int t = i / D, c = i - t * D;
@@ -144,7 +149,8 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
     sc.row_bytes = (uint32_t)(ks.st * ks.esize);
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
-    tree_search<NMAX, kMDThreads>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
+    tree_search<NMAX, kMDThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr);
+    if (cs == 0 && threadIdx.x == 0) cnt[lin] = min(Bq, sh.n);
     __syncthreads();
   }
 }
@@ -164,7 +170,7 @@ static cudaError_t launch_md(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   cudaError_t e = persistent_ctas(kern, kMDThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
+  const int64_t grid = std::min<int64_t>(units * std::max(sh.chunks, 1), (int64_t)num_sms * per_sm);
   kern<<<(unsigned)grid, kMDThreads, smem, stream>>>(sh, qs, ks, idx, cnt);
   return cudaGetLastError();
 }

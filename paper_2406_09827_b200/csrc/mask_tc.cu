@@ -287,7 +287,10 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
 #endif
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  for (int64_t u = (int64_t)blockIdx.x * TEAMS + team; u < units; u += (int64_t)gridDim.x * TEAMS) {
+  const int S = max(sh.chunks, 1);
+  for (int64_t jb = (int64_t)blockIdx.x * TEAMS + team; jb < units * S; jb += (int64_t)gridDim.x * TEAMS) {
+    const int64_t u = jb / S;
+    const int cs = (int)(jb - u * S);
     int b, h, q;
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
@@ -295,6 +298,8 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     const int Bq = visible_blocks(sh, q, Tk);
     const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    int lo, len, nn, slot0;
+    if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     const uint32_t q_s = sbase + L::q + team * kQTileBytes;
     if (Bq > sh.n) {
       // query block -> K-major SW128 tile (B operand, N = 32 rows, rows >= rows_q zero); waited for
@@ -324,7 +329,8 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     sc.pt = &ptimer;
     ptimer.mark(7);  // unit setup / Q load / exact units
 #endif
-    tree_search<kMTNmax, NT, decltype(sc), Sync>(st, sh.n, Bq, sc, idx + lin * sh.n, cnt + lin);
+    tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr);
+    if (cs == 0 && Sync::tid() == 0) cnt[lin] = min(Bq, sh.n);
     Sync::sync();
   }
   tc_fence_before();
@@ -353,7 +359,8 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
   cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  int64_t grid = std::min<int64_t>((units + TEAMS - 1) / TEAMS, (int64_t)num_sms * per_sm);
+  const int64_t jobs = units * std::max(sh.chunks, 1);
+  int64_t grid = std::min<int64_t>((jobs + TEAMS - 1) / TEAMS, (int64_t)num_sms * per_sm);
   kern<<<(unsigned)grid, 128 * TEAMS, smem, stream>>>(sh, qs, ks, idx, cnt);
   return cudaGetLastError();
 }

@@ -188,26 +188,43 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
   }
 }
 
-// Runs the tree search of one query block with B_q visible key blocks and writes the n selected
-// blocks (ascending, -1 padded) to out_idx and the count to *out_cnt.  All NT threads call it.
-// Scorer::score(rep, n_rep, rep_s) must fill rep_s[i] = tile score of key block rep[i] and end
-// with a Sync::sync(); Scorer::mark(p) is a profiling hook (no-op in product builds).
+// Stridden partial top-k (reading G21): a launch runs units x S jobs; job (unit, s)
+// searches chunk s = [a_s, a_{s+1}), a_s = floor((2 s B_q + S) / (2 S)), with n / S nodes and writes
+// slots [s n / S, (s + 1) n / S) of the unit's output.  S = 1, or B_q <= n (exact case, chunk 0
+// alone): the whole range with n nodes.  Returns false for a job with nothing to do.
+__device__ __forceinline__ bool chunk_job(int Bq, int n, int S, int s, int& lo, int& len, int& nn, int& slot0) {
+  if (S <= 1 || Bq <= n) {
+    lo = 0; len = Bq; nn = n; slot0 = 0;
+    return s == 0;
+  }
+  const int64_t a0 = (2 * (int64_t)s * Bq + S) / (2 * (int64_t)S);
+  const int64_t a1 = (2 * (int64_t)(s + 1) * Bq + S) / (2 * (int64_t)S);
+  lo = (int)a0; len = (int)(a1 - a0); nn = n / S; slot0 = s * nn;
+  return true;
+}
+
+// Runs the tree search of one query block over the L key blocks [lo, lo + L) (lo = 0, L = B_q:
+// Alg. 1; one chunk of the stridden partial top-k otherwise, reading G21) and writes the n
+// selected blocks (ascending, -1 padded) to out_idx and, if out_cnt, the count.  All NT threads
+// call it.  Scorer::score(rep, n_rep, rep_s) must fill rep_s[i] = tile score of key block rep[i] and
+// end with a Sync::sync(); Scorer::mark(p) is a profiling hook (no-op in product builds).
 template <int NMAX, int NT, class Scorer, class Sync = CtaSync>
-__device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, int32_t* out_idx, int32_t* out_cnt) {
+__device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& scorer, int32_t* out_idx,
+                            int32_t* out_cnt) {
   static_assert(NMAX % NT == 0 || NT % NMAX == 0, "NMAX and NT must nest");
   constexpr int E = NMAX >= NT ? NMAX / NT : 1;  // nodes per thread (contiguous)
   constexpr int EC = 2 * E;                      // candidates per thread (their children)
   static_assert(EC <= 32, "valid mask");
   const int tid = Sync::tid();
   if (Bq <= n) {  // exact case (G1): every visible block
-    for (int j = tid; j < n; j += NT) out_idx[j] = j < Bq ? j : -1;
-    if (tid == 0) *out_cnt = Bq;
+    for (int j = tid; j < n; j += NT) out_idx[j] = j < Bq ? lo + j : -1;
+    if (tid == 0 && out_cnt) *out_cnt = Bq;
     return;
   }
-  // Initial nodes (Alg. 1 line 4, readings G1-G3): f_j = floor((2 j B_q + n) / (2 n)).
+  // Initial nodes (Alg. 1 line 4, readings G1-G3): f_j = lo + floor((2 j B_q + n) / (2 n)).
   for (int j = tid; j < n; j += NT) {
-    const int64_t fj = (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
-    const int64_t fj1 = (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
+    const int64_t fj = lo + (2 * (int64_t)j * Bq + n) / (2 * (int64_t)n);
+    const int64_t fj1 = lo + (2 * (int64_t)(j + 1) * Bq + n) / (2 * (int64_t)n);
     st.nf[j] = (int)fj;
     st.nl[j] = (int)fj1 - 1;
     st.ns[j] = 0u;
@@ -313,7 +330,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int Bq, Scorer& scorer, i
   }
   // --- output (Alg. 1 line 17): first blocks of the final single-block nodes, already ascending (G18)
   for (int j = tid; j < n; j += NT) out_idx[j] = st.nf[j];
-  if (tid == 0) *out_cnt = n;
+  if (tid == 0 && out_cnt) *out_cnt = n;
   scorer.mark(6);  // output
 }
 

@@ -35,7 +35,7 @@ class HipError(RuntimeError):
 class Params(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("b_q", ctypes.c_int32), ("b_k", ctypes.c_int32), ("causal", ctypes.c_int32),
                 ("sm_scale", ctypes.c_float), ("flags", ctypes.c_uint32), ("sink_tokens", ctypes.c_int32),
-                ("window_tokens", ctypes.c_int32)]
+                ("window_tokens", ctypes.c_int32), ("chunks", ctypes.c_int32)]
 
 
 class TensorDesc(ctypes.Structure):
@@ -109,9 +109,9 @@ def _stream(t: torch.Tensor, stream=None) -> int:
 
 
 def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False, sink: int = 0,
-            window: int = 0) -> Params:
+            window: int = 0, chunks: int = 1) -> Params:
     return Params(int(k), int(b_q), int(b_k), int(bool(causal)), float(sm_scale or 0.0),
-                  HIP_FLAG_EXACT_SCORES if exact else 0, int(sink), int(window))
+                  HIP_FLAG_EXACT_SCORES if exact else 0, int(sink), int(window), int(chunks))
 
 
 def _require_cuda(*ts):
@@ -126,13 +126,14 @@ def num_blocks(k: int, b_k: int) -> int:
 
 
 def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
-                  causal: bool = True, exact: bool = False, out=None, stream=None):
-    """hip_mask_estimate on contiguous keys.  q [B,Hq,Tq,d], k [B,Hkv,Tk,d] -> (idx, cnt)."""
+                  causal: bool = True, exact: bool = False, chunks: int = 1, out=None, stream=None):
+    """hip_mask_estimate on contiguous keys.  q [B,Hq,Tq,d], k [B,Hkv,Tk,d] -> (idx, cnt).  chunks = S:
+    stridden partial top-k."""
     _require_cuda(q, k)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
-    p = _params(k_budget, b_q, b_k, causal, exact=exact)
+    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq
@@ -161,13 +162,14 @@ def _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len: int) -> PagedKV
 
 
 def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, k_budget: int = 512, b_q: int = 32,
-                        b_k: int = 2, causal: bool = True, exact: bool = False, out=None, stream=None):
+                        b_k: int = 2, causal: bool = True, exact: bool = False, chunks: int = 1, out=None,
+                        stream=None):
     """hip_mask_estimate on a paged cache (decode: q [B,Hq,Tq,d], Tq rows at positions seq_len-Tq+t)."""
     _require_cuda(q, k_pages, block_table, seq_lens)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
-    p = _params(k_budget, b_q, b_k, causal, exact=exact)
+    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq

@@ -433,3 +433,35 @@ def test_decoder_rm_cache_schedule(orc):
         Oo, _ = orc.sparse_attention_paged(q, kp, vp, bt, sl, k, 1, bk, True, gi, gc, sink=4, window=16)
         assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
     assert 1 < dec.refreshes < 8
+
+
+# ------------------------------------------------------------------------------------------------
+# f3: stridden partial top-k (S chunks per query block; reading G21)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("S", [2, 4])
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "llm"), (torch.bfloat16, "int")])
+def test_mask_chunked_parity(orc, S, dt, dist):
+    Tq, Tk, k, bq, bk = 1500, 1700, 256, 32, 2
+    Q, K, _ = synth.gen_qkv(1, 2, 1, Tq, Tk, 128, dist, seed=60, dtype=dt, make_v=False)
+    idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, chunks=S)
+    torch.cuda.synchronize()
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, chunks=S)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+
+
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "iid"), (torch.bfloat16, "int")])
+def test_mask_chunked_decode_parity(orc, dt, dist):
+    B, Hq, Hkv, d, k, bk, ps, S = 3, 4, 2, 128, 512, 2, 64, 4
+    seq = [5000, 100, 3333]
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=61, dtype=dt, dist=dist)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=61, dtype=dt, dist=dist)
+    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk,
+                                     chunks=S)
+    torch.cuda.synchronize()
+    gi, gc = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(B):  # the oracle's chunked mask on the contiguous view of each sequence
+        Kb = _paged_to_contiguous(kp, bt, sl, b)
+        mode = orc.F32L if dt == torch.float32 else orc.F32C
+        oi, oc = orc.mask(Q[b:b + 1], Kb, k, 1, bk, True, mode=mode, chunks=S)
+        _assert_mask_equal(gi[b:b + 1], gc[b:b + 1], oi, oc)
