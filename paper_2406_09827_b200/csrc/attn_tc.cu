@@ -177,25 +177,36 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
 
     // item i: chunk ch = i >> 2; (i & 3) = 0, 1: K_ch d-half 0 / 1; 2, 3: V_ch keys [0,64) / [64,128)
+    // Thread (c8, r0) moves 16-byte chunk c8 of the 8 keys r0 + 16 j (j = 0..7) of every chunk: for
+    // K items those 8 rows (one d-half), for V items keys r0 + 16 j' + 64 (kind - 2) of both d-halves.
+    // All eight keys share r0's swizzle phase, so the destinations are one base + immediates, and
+    // the rows' tokens are read once per chunk (at its first item).
+    const int c8 = threadIdx.x & 7, r0 = threadIdx.x >> 3;  // r0 < 16
+    const uint32_t dbase = (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + ((c8 ^ (r0 & 7)) << 4));
+    int srow[8];  // this thread's 8 key rows of the current chunk (-1: none)
     auto issue = [&](int i) {
       const int ch = i >> 2, kind = i & 3;
-      const uint32_t slot = sb + L::ring + (i & 1) * kATSlot;
-      const int c8 = threadIdx.x & 7, r0 = threadIdx.x >> 3;  // r0 < 16
+      const uint32_t dst = sb + L::ring + (i & 1) * kATSlot + dbase;
+      if (kind == 0) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int x = r0 + 16 * j;  // 0..127
-        int r, dh, key;
-        const char* g0;
-        uint32_t rb, dst;
-        if (kind < 2) {  // K: 128 keys x this d-half
-          r = x; dh = kind; key = ch * 128 + r; g0 = kbase; rb = krow;
-          dst = slot + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4);
-        } else {         // V: 64 keys x both d-halves, d-half regions 8 KB apart
-          r = x & 63; dh = x >> 6; key = ch * 128 + (kind - 2) * 64 + r; g0 = vbase; rb = vrow;
-          dst = slot + dh * 8192 + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4);
+        for (int j = 0; j < 8; ++j) {
+          const int t = tok[ch * 128 + r0 + 16 * j];
+          srow[j] = kSW ? (t & ~kExtraBit) : t;  // -1 stays negative
         }
-        const int s = kSW ? (tok[key] & ~kExtraBit) : tok[key];  // -1 stays negative
-        cp_async16(dst, g0 + (uint64_t)(uint32_t)(s >= 0 ? s : 0) * rb + dh * 128 + c8 * 16, s >= 0 ? 16u : 0u);
+      }
+      if (kind < 2) {  // K: 128 keys x d-half `kind`
+        const char* g = kbase + kind * 128 + c8 * 16;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          cp_async16(dst + 2048 * j, g + (uint64_t)(uint32_t)max(srow[j], 0) * krow, srow[j] >= 0 ? 16u : 0u);
+      } else {         // V: 64 keys x both d-halves, d-half regions 8 KB apart
+        const char* g = vbase + c8 * 16;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int sr = kind == 2 ? srow[j & 3] : srow[4 + (j & 3)];  // static indices (registers)
+          cp_async16(dst + 2048 * (j & 3) + 8192 * (j >> 2), g + (uint64_t)(uint32_t)max(sr, 0) * vrow + (j >> 2) * 128,
+                     sr >= 0 ? 16u : 0u);
+        }
       }
     };
     bool pend[2] = {false, false};
@@ -248,11 +259,16 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         }
         const bool all_vis = s >= 0 && rows_q == 32 && (!sh.causal || s <= tpos0) &&
                              (!extra || extra_visible(s, tpos0 + 31, sh.causal, sh.sink, sh.window));
+        if (all_vis) {  // the common case: this key is visible to all 32 rows
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = all_vis || (s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j) &&
-                                      (!extra || extra_visible(s, tpos0 + j, sh.causal, sh.sink, sh.window)));
-          v[j] = ok ? v[j] * scale_log2 : -INFINITY;
+          for (int j = 0; j < 32; ++j) v[j] *= scale_log2;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const bool ok = s >= 0 && j < rows_q && (!sh.causal || s <= tpos0 + j) &&
+                            (!extra || extra_visible(s, tpos0 + j, sh.causal, sh.sink, sh.window));
+            v[j] = ok ? v[j] * scale_log2 : -INFINITY;
+          }
         }
         float x[32];
 #pragma unroll
