@@ -231,6 +231,10 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& s
   }
   Sync::sync();
   bool first = true;
+  // Lower bound of the next selection: the n inherited candidates (left children / unsplit nodes)
+  // keep the keys selected last iteration, all >= that selection's radix prefix, so a key below it
+  // can never be among the n best — excluding those keys narrows the radix range (fewer passes).
+  uint64_t lb = 0ull;
   // Every iteration at least halves the largest node, so <= 31 iterations end the search; the cap
   // only guards against non-finite inputs.
   for (int iter = 0; iter < 40; ++iter) {
@@ -301,7 +305,13 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& s
       key[k] = make_key(kr[k] >= 0 ? ord_score(st.rep_s[kr[k]]) : ks[k], kf[k]);
     uint64_t prefix, mask;
     scorer.mark(8);  // keys
-    const int passes = radix_top<NT, EC, NMAX, Sync>(key, valid, n, st, prefix, mask);
+    uint32_t live = valid;
+#pragma unroll
+    for (int k = 0; k < EC; ++k)
+      if (key[k] < lb) live &= ~(1u << k);
+    const int passes = radix_top<NT, EC, NMAX, Sync>(key, live, n, st, prefix, mask);
+    valid = live;
+    lb = prefix;
     scorer.mark(4);  // radix select
 #ifdef HIPATTN_PHASES
     if (tid == 0) {
