@@ -93,6 +93,12 @@ struct TCScorer {
   __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
     const int c = c0 + (i >> 1), h = i & 1;
     const int tid = Sync::tid(), c8 = tid & 7, r0 = tid >> 3;
+    if constexpr (!kPaged && NT == 128) {
+      if (lbk == 1) {  // b_k = 2 (the paper's setting): thread (c8, g) owns the 8 consecutive rows 8g..8g+7
+        issue_bk2(rep, n_rep, c, h, c8, r0, i);
+        return;
+      }
+    }
     if (h == 0) {
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int bmask = (1 << lbk) - 1;
@@ -111,6 +117,32 @@ struct TCScorer {
 #pragma unroll
     for (int j = 0; j < RJ; ++j)  // rows r0 + RPP j share r0's swizzle phase (RPP % 8 == 0)
       cp_async16(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & 1u) ? 16u : 0u);
+  }
+
+  // b_k = 2: rows 8g..8g+7 of the tile are the 4 blocks 4g..4g+3, so one 16-byte load brings their
+  // representatives and the second row of a block is the first plus one row stride.  A warp
+  // instruction j still moves 4 whole 128-byte half rows (rows 8g + j, g = 4w..4w+3).
+  __device__ __forceinline__ void issue_bk2(const int* rep, int n_rep, int c, int h, int c8, int g, int i) {
+    if (h == 0) {
+      const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
+      const int4 rv = *reinterpret_cast<const int4*>(rep + blk0 + 4 * g);
+      const int r4[4] = {rv.x, rv.y, rv.z, rv.w};
+      rok = 0;
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2) {
+        const bool inb = 4 * g + b2 < nblk;
+        const int s = inb ? r4[b2] << 1 : 0;
+        const bool ok0 = inb && s < Tk, ok1 = inb && s + 1 < Tk;
+        rp[2 * b2] = row(ok0 ? s : 0) + c8 * 16;
+        rp[2 * b2 + 1] = rp[2 * b2] + (ok1 ? row_bytes : 0u);
+        rok |= ((uint32_t)ok0 << (2 * b2)) | ((uint32_t)ok1 << (2 * b2 + 1));
+      }
+    }
+    const uint32_t dst = k_s0 + (uint32_t)(i % SLOTS) * kMTSlot + g * 1024;
+    const uint32_t x = (uint32_t)c8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      cp_async16(dst + j * 128 + ((x ^ j) << 4), rp[j] + h * 128, ((rok >> j) & 1u) ? 16u : 0u);
   }
 
   __device__ __forceinline__ void wait_slot(int slot) {
