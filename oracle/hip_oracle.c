@@ -23,6 +23,10 @@
  *   - oracle_dense_attention  S = QK^T, P = softmax(S), O = PV, fp64, causal optional.
  *   - oracle_exact_block_topn top-n of the exact block-max scores (the textbook top-k of P:116 at
  *                             block granularity) — used for pins and recall.
+ *   - oracle_mask_ext         + the appendix extensions: top-r approximation (readings
+ *                             G22) and the ensemble's jittered splits (G23), with the
+ *                             stridden partial top-k (G21).
+ *   - oracle_vote             the ensemble vote (G24).
  *   - *_paged                 the same on a paged KV cache (decode): token s of
  *                             sequence b lives at page block_table[b][s / page_size], slot
  *                             s % page_size; gathered with plain loops.
@@ -61,6 +65,70 @@ typedef struct {
 
 static int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+/* Extensions of Alg. 1 from the paper's appendix (all off = Alg. 1 itself):
+ *   top-r approximation: a branch score sums q_c k_c over the r components c with the
+ *     largest |q_c| only; for a query block |q_c| is reduced by the max over its rows and ties go to
+ *     the smaller component (reading G22, SPEC D5); the terms are summed in ascending c (G22).
+ *   ensemble sampling: every split point is moved by a random integer offset,
+ *     m = clamp(round_half_up((f+l)/2) + u, f+1, l) with u uniform in [-R, R], R = r_e (reading G23),
+ *     drawn from the counter-based generator below keyed by (seed, unit, iteration, node first). */
+typedef struct {
+    const int *comp; /* top-r components, ascending; NULL = all d components */
+    int ncomp;
+    int R;           /* split jitter magnitude (0 = the deterministic half-up split) */
+    uint64_t key;    /* per-unit generator key (orc_unit_key) */
+} orc_ext;
+
+/* splitmix64 output function (Steele, Lea & Flood 2014): the counter-based generator of the
+ * ensemble.  The CUDA path implements the same published function independently. */
+static uint64_t orc_mix64(uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+#define ORC_GOLDEN 0x9E3779B97F4A7C15ULL
+
+/* first output of a splitmix64 stream seeded with `state` (pinned against the published vector) */
+uint64_t oracle_splitmix64(uint64_t state) { return orc_mix64(state + ORC_GOLDEN); }
+
+/* key of unit lin = (b*Hq + h)*N_qb + q for sample seed `seed` */
+static uint64_t orc_unit_key(uint64_t seed, int64_t lin) { return orc_mix64(orc_mix64(seed + ORC_GOLDEN) ^ (uint64_t)lin); }
+
+/* split offset u in [-R, R] of the node whose first block is f, at iteration it (0 = first split) */
+static int64_t orc_jitter(uint64_t key, int it, int64_t f, int R)
+{
+    uint64_t x = orc_mix64(key ^ (((uint64_t)(uint32_t)it << 32) | (uint64_t)(uint32_t)f));
+    return (int64_t)(x % (uint64_t)(2 * R + 1)) - R;
+}
+
+/* argtop_r(|q|) of a query block (reading G22): a_c = max over the rows of |q_c|, the r
+ * largest a_c with ties toward the smaller c, returned in ascending order.  r >= d: all. */
+static void top_r_components(const float *Qh, int64_t t0, int64_t t1, int d, int r, int *out)
+{
+    double *a = (double *)malloc(sizeof(double) * (size_t)d);
+    char *taken = (char *)calloc((size_t)d, 1);
+    for (int c = 0; c < d; ++c) {
+        a[c] = 0.0;
+        for (int64_t t = t0; t < t1; ++t) {
+            double v = fabs((double)Qh[t * d + c]);
+            if (v > a[c]) a[c] = v;
+        }
+    }
+    /* r rounds of "take the largest remaining, smallest index on ties" */
+    for (int i = 0; i < r; ++i) {
+        int best = -1;
+        for (int c = 0; c < d; ++c)
+            if (!taken[c] && (best < 0 || a[c] > a[best])) best = c;
+        taken[best] = 1;
+    }
+    int w = 0;
+    for (int c = 0; c < d; ++c)
+        if (taken[c]) out[w++] = c;
+    free(a);
+    free(taken);
+}
+
 /* Validation shared by every entry point. */
 static int check_dims(int B, int Hq, int Hkv, int Tq, int Tk, int d, int k, int bq, int bk, int causal)
 {
@@ -87,8 +155,18 @@ static int64_t visible_blocks(int64_t q, int bq, int bk, int Tq, int Tk, int cau
  * block j, restricted to valid pairs (s < Tk; causal: s <= t + Tk - Tq, reading G8).  No softmax
  * scale (G11).  `emax` (optional) receives max over the pairs of sum_c |q_c k_c|, used
  * to bound the rounding error of any fp32 evaluation order. */
+static double block_score_c(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
+                            int Tq, int Tk, int d, int causal, int mode, const int *comp, int ncomp, double *emax);
 static double block_score(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
                           int Tq, int Tk, int d, int causal, int mode, double *emax)
+{
+    return block_score_c(Qh, Kh, t0, t1, j, bk, Tq, Tk, d, causal, mode, NULL, d, emax);
+}
+
+/* The same over the component list comp[0..ncomp) (top-r: sum_{l=1..r} q_{p_l} k_{p_l}, in
+ * ascending component order; comp = NULL: c = 0..d-1). */
+static double block_score_c(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
+                            int Tq, int Tk, int d, int causal, int mode, const int *comp, int ncomp, double *emax)
 {
     int64_t delta = (int64_t)Tk - Tq;
     int64_t s0 = j * bk, s1 = imin64((j + 1) * (int64_t)bk, Tk);
@@ -101,28 +179,39 @@ static double block_score(const float *Qh, const float *Kh, int64_t t0, int64_t 
             double v, e = 0.0;
             if (mode == ORC_F32C) {
                 float acc = 0.0f;
-                for (int c = 0; c < d; ++c) acc = fmaf(q[c], kk[c], acc);
+                for (int i = 0; i < ncomp; ++i) {
+                    int c = comp ? comp[i] : i;
+                    acc = fmaf(q[c], kk[c], acc);
+                }
                 v = (double)acc;
-                for (int c = 0; c < d; ++c) e += fabs((double)q[c] * (double)kk[c]);
+                for (int i = 0; i < ncomp; ++i) {
+                    int c = comp ? comp[i] : i;
+                    e += fabs((double)q[c] * (double)kk[c]);
+                }
             } else if (mode == ORC_F32L) {
-                /* reading G9b: 16 segments of d/16 consecutive terms, each a sequential fmaf
-                 * chain, combined by the pairwise tree v[l] <- v[l] + v[l ^ o], o = 8, 4, 2, 1 */
+                /* reading G9b: 16 segments of d/16 consecutive components, each a sequential fmaf
+                 * chain (over the segment's selected components), combined by the pairwise tree
+                 * v[l] <- v[l] + v[l ^ o], o = 8, 4, 2, 1 */
                 float seg[16], nxt[16];
                 int w = d / 16;
-                for (int l = 0; l < 16; ++l) {
-                    float acc = 0.0f;
-                    for (int c = l * w; c < (l + 1) * w; ++c) acc = fmaf(q[c], kk[c], acc);
-                    seg[l] = acc;
+                for (int l = 0; l < 16; ++l) seg[l] = 0.0f;
+                for (int i = 0; i < ncomp; ++i) {
+                    int c = comp ? comp[i] : i;
+                    seg[c / w] = fmaf(q[c], kk[c], seg[c / w]);
                 }
                 for (int o = 8; o >= 1; o >>= 1) {
                     for (int l = 0; l < 16; ++l) nxt[l] = seg[l] + seg[l ^ o];
                     for (int l = 0; l < 16; ++l) seg[l] = nxt[l];
                 }
                 v = (double)seg[0];
-                for (int c = 0; c < d; ++c) e += fabs((double)q[c] * (double)kk[c]);
+                for (int i = 0; i < ncomp; ++i) {
+                    int c = comp ? comp[i] : i;
+                    e += fabs((double)q[c] * (double)kk[c]);
+                }
             } else {
                 double acc = 0.0;
-                for (int c = 0; c < d; ++c) {
+                for (int i = 0; i < ncomp; ++i) {
+                    int c = comp ? comp[i] : i;
                     double p = (double)q[c] * (double)kk[c]; /* exact: 24+24 bit mantissas */
                     acc += p;
                     e += fabs(p);
@@ -181,8 +270,9 @@ typedef struct {
 static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t t0, int64_t t1,
                         int64_t lo, int64_t L, int n, int bk, int causal, int mode, double *memo,
                         int32_t *out_idx, orc_diag *dg, int32_t *trace_nodes, double *trace_scores,
-                        int max_trace)
+                        int max_trace, const orc_ext *ex)
 {
+    int it = 0; /* iteration of this search (0 = first split), keys the ensemble jitter */
     orc_node *nodes = (orc_node *)malloc(sizeof(orc_node) * (size_t)n);
     orc_node *cand = (orc_node *)malloc(sizeof(orc_node) * 2 * (size_t)n);
     int64_t *firsts = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
@@ -215,6 +305,11 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
                 cand[nc].f = f; cand[nc].l = f; ++nc;
             } else {
                 int64_t m = (f + l + 1) / 2;
+                if (ex->R > 0) { /* ensemble: split "around the center" (G23) */
+                    m += orc_jitter(ex->key, it, f, ex->R);
+                    if (m < f + 1) m = f + 1;
+                    if (m > l) m = l;
+                }
                 cand[nc].f = f; cand[nc].l = m - 1; ++nc;
                 cand[nc].f = m; cand[nc].l = l; ++nc;
             }
@@ -223,7 +318,7 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
             int64_t r = cand[c].f; /* representative = first block of the branch */
             if (isnan(memo[r])) {
                 double e = 0.0;
-                memo[r] = block_score(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, &e);
+                memo[r] = block_score_c(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, ex->comp, ex->ncomp, &e);
                 if (e > dg->emax) dg->emax = e;
                 dg->n_scored++;
             }
@@ -244,6 +339,7 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
             }
         }
         dg->n_iter++;
+        it++;
     }
 
     for (int j = 0; j < n; ++j) firsts[j] = nodes[j].f;
@@ -259,7 +355,8 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
  * are concatenated (ascending).  S = 1 is Alg. 1 itself. */
 static int mask_unit_chunked(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t q, int n, int bq,
                              int bk, int causal, int mode, int chunks, int32_t *out_idx, int32_t *out_cnt,
-                             orc_diag *diag, int32_t *trace_nodes, double *trace_scores, int max_trace)
+                             orc_diag *diag, int32_t *trace_nodes, double *trace_scores, int max_trace,
+                             int top_r, int R, uint64_t seed, int64_t lin)
 {
     int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
     int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
@@ -276,13 +373,22 @@ static int mask_unit_chunked(const float *Qh, const float *Kh, int Tq, int Tk, i
 
     double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
     if (!memo) return ORC_ENOMEM;
+    int comp[1024];
+    orc_ext ex = {NULL, d, R > 0 ? R : 0, 0};
+    if (top_r > 0 && top_r < d) { /* top-r approximation */
+        if (d > 1024) { free(memo); return ORC_EINVAL; }
+        top_r_components(Qh, t0, t1, d, top_r, comp);
+        ex.comp = comp;
+        ex.ncomp = top_r;
+    }
+    if (ex.R > 0) ex.key = orc_unit_key(seed, lin);
     for (int64_t j = 0; j < Bq; ++j) memo[j] = NAN;
     int ns = n / chunks, rc = ORC_OK;
     for (int c = 0; c < chunks && rc == ORC_OK; ++c) {
         int64_t a0 = (2 * (int64_t)c * Bq + chunks) / (2 * (int64_t)chunks);
         int64_t a1 = (2 * (int64_t)(c + 1) * Bq + chunks) / (2 * (int64_t)chunks);
         rc = search_range(Qh, Kh, Tq, Tk, d, t0, t1, a0, a1 - a0, ns, bk, causal, mode, memo, out_idx + c * ns,
-                          &dg, chunks == 1 ? trace_nodes : NULL, trace_scores, max_trace);
+                          &dg, chunks == 1 ? trace_nodes : NULL, trace_scores, max_trace, &ex);
     }
     *out_cnt = n;
     if (diag) *diag = dg;
@@ -295,7 +401,7 @@ static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, in
                      int32_t *trace_nodes, double *trace_scores, int max_trace)
 {
     return mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, 1, out_idx, out_cnt, diag,
-                             trace_nodes, trace_scores, max_trace);
+                             trace_nodes, trace_scores, max_trace, 0, 0, 0, 0);
 }
 
 /* -------------------------------------------------------------------------------------------- */
@@ -335,10 +441,11 @@ int oracle_mask(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, 
 }
 
 /* oracle_mask with stridden partial top-k over S = chunks contiguous chunks (G21). */
-int oracle_mask_chunked(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
-                        int bq, int bk, int causal, int mode, int chunks, int32_t *idx, int32_t *cnt,
-                        double *margin_min, double *emax)
+int oracle_mask_ext(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
+                    int bq, int bk, int causal, int mode, int chunks, int top_r, int jitter, uint64_t seed,
+                    int32_t *idx, int32_t *cnt, double *margin_min, double *emax)
 {
+    if (top_r < 0 || jitter < 0) return ORC_EINVAL;
     int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
     if (rc) return rc;
     int n = k / bk;
@@ -354,7 +461,7 @@ int oracle_mask_chunked(const float *Q, const float *K, int B, int Hq, int Hkv, 
         const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
         orc_diag dg;
         int r = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, chunks, idx + u * n, cnt + u,
-                                  &dg, NULL, NULL, 0);
+                                  &dg, NULL, NULL, 0, top_r, jitter, seed, u);
         if (r) {
 #pragma omp critical
             err = r;
@@ -365,24 +472,130 @@ int oracle_mask_chunked(const float *Q, const float *K, int B, int Hq, int Hkv, 
     return err;
 }
 
+int oracle_mask_chunked(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
+                        int bq, int bk, int causal, int mode, int chunks, int32_t *idx, int32_t *cnt,
+                        double *margin_min, double *emax)
+{
+    return oracle_mask_ext(Q, K, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal, mode, chunks, 0, 0, 0, idx, cnt,
+                           margin_min, emax);
+}
+
 /* Node trace of one unit (for the invariant pins, PIN-5).  trace_nodes: [(max_trace+1) * n * 2],
  * trace_scores: [max_trace * n]; *n_iter receives the iteration count. */
+int oracle_mask_trace_ext(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
+                          int bq, int bk, int causal, int mode, int b, int h, int q, int32_t *idx_out,
+                          int32_t *cnt_out, int32_t *trace_nodes, double *trace_scores, int max_trace,
+                          int32_t *n_iter, int64_t *n_scored, int top_r, int jitter, uint64_t seed)
+{
+    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
+    if (rc) return rc;
+    if (top_r < 0 || jitter < 0) return ORC_EINVAL;
+    int hk = h / (Hq / Hkv);
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    const float *Qh = Q + (((int64_t)b * Hq + h) * (int64_t)Tq) * d;
+    const float *Kh = K + (((int64_t)b * Hkv + hk) * (int64_t)Tk) * d;
+    orc_diag dg;
+    rc = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, k / bk, bq, bk, causal, mode, 1, idx_out, cnt_out, &dg,
+                           trace_nodes, trace_scores, max_trace, top_r, jitter, seed,
+                           ((int64_t)b * Hq + h) * nqb + q);
+    if (n_iter) *n_iter = dg.n_iter;
+    if (n_scored) *n_scored = dg.n_scored;
+    return rc;
+}
+
 int oracle_mask_trace(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
                       int bq, int bk, int causal, int mode, int b, int h, int q, int32_t *idx_out,
                       int32_t *cnt_out, int32_t *trace_nodes, double *trace_scores, int max_trace,
                       int32_t *n_iter, int64_t *n_scored)
 {
-    int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
-    if (rc) return rc;
-    int hk = h / (Hq / Hkv);
-    const float *Qh = Q + (((int64_t)b * Hq + h) * (int64_t)Tq) * d;
-    const float *Kh = K + (((int64_t)b * Hkv + hk) * (int64_t)Tk) * d;
-    orc_diag dg;
-    rc = mask_unit(Qh, Kh, Tq, Tk, d, q, k / bk, bq, bk, causal, mode, idx_out, cnt_out, &dg, trace_nodes,
-                   trace_scores, max_trace);
-    if (n_iter) *n_iter = dg.n_iter;
-    if (n_scored) *n_scored = dg.n_scored;
-    return rc;
+    return oracle_mask_trace_ext(Q, K, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal, mode, b, h, q, idx_out, cnt_out,
+                                 trace_nodes, trace_scores, max_trace, n_iter, n_scored, 0, 0, 0);
+}
+
+/* argtop_r(|q|) of one query block (rows [0, nrows) of Qb [nrows, d]) -> out[r], ascending (G22). */
+int oracle_top_r_components(const float *Qb, int nrows, int d, int r, int32_t *out)
+{
+    if (nrows < 1 || d < 1 || r < 1 || r > d) return ORC_EINVAL;
+    int *tmp = (int *)malloc(sizeof(int) * (size_t)d);
+    if (!tmp) return ORC_ENOMEM;
+    top_r_components(Qb, 0, nrows, d, r, tmp);
+    for (int i = 0; i < r; ++i) out[i] = tmp[i];
+    free(tmp);
+    return ORC_OK;
+}
+
+/* Split offset of the ensemble generator (for the generator pins). */
+int64_t oracle_jitter(uint64_t seed, int64_t lin, int it, int64_t f, int R)
+{
+    return R > 0 ? orc_jitter(orc_unit_key(seed, lin), it, f, R) : 0;
+}
+
+/* -------------------------------------------------------------------------------------------- */
+/* Ensemble vote: per unit, an index survives iff at least theta of the n_e sample   */
+/* masks contain it; tau = 1 truncates the survivors to n, preferring more votes, then the smaller */
+/* block (reading G24, SPEC vote ordering); the output is ascending, -1 padded to n_out.           */
+/* idx [n_e][units][n_in] with cnt [n_e][units]; out_idx [units][n_out], out_cnt [units].          */
+/* -------------------------------------------------------------------------------------------- */
+typedef struct { int32_t j, v; } orc_vote;
+
+static int vote_cmp(const void *pa, const void *pb) /* votes desc, block asc */
+{
+    const orc_vote *a = (const orc_vote *)pa, *b = (const orc_vote *)pb;
+    if (a->v != b->v) return a->v > b->v ? -1 : 1;
+    return (a->j > b->j) - (a->j < b->j);
+}
+
+static int i32_cmp(const void *pa, const void *pb)
+{
+    int32_t a = *(const int32_t *)pa, b = *(const int32_t *)pb;
+    return (a > b) - (a < b);
+}
+
+int oracle_vote(int n_e, int64_t units, int n_in, const int32_t *idx, const int32_t *cnt, int theta, int tau,
+                int n_out, int32_t *out_idx, int32_t *out_cnt)
+{
+    if (n_e < 1 || units < 0 || n_in < 1 || theta < 1 || theta > n_e || (tau != 0 && tau != 1) || n_out < 1)
+        return ORC_EINVAL;
+    if (!tau && n_out < n_e * n_in) return ORC_EINVAL;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t u = 0; u < units; ++u) {
+        int32_t *all = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_e * n_in);
+        orc_vote *sv = (orc_vote *)malloc(sizeof(orc_vote) * (size_t)n_e * n_in);
+        int m = 0, ns = 0, bad = 0;
+        for (int e = 0; e < n_e; ++e) {
+            int c = cnt[(int64_t)e * units + u];
+            if (c < 0 || c > n_in) { bad = 1; break; }
+            for (int i = 0; i < c; ++i) all[m++] = idx[((int64_t)e * units + u) * n_in + i];
+        }
+        if (!bad) {
+            /* count the agreements per index: sort, then runs of equal values */
+            qsort(all, (size_t)m, sizeof(int32_t), i32_cmp);
+            for (int i = 0; i < m;) {
+                int j = i;
+                while (j < m && all[j] == all[i]) ++j;
+                if (j - i >= theta) { sv[ns].j = all[i]; sv[ns].v = j - i; ++ns; }
+                i = j;
+            }
+            if (tau && ns > n_in) { /* truncate by votes, then block (G24) */
+                qsort(sv, (size_t)ns, sizeof(orc_vote), vote_cmp);
+                ns = n_in;
+            }
+            if (ns > n_out) bad = 1;
+        }
+        if (bad) {
+#pragma omp critical
+            err = ORC_ERANGE;
+        } else {
+            for (int i = 0; i < ns; ++i) all[i] = sv[i].j;
+            qsort(all, (size_t)ns, sizeof(int32_t), i32_cmp);
+            for (int i = 0; i < n_out; ++i) out_idx[u * n_out + i] = i < ns ? all[i] : -1;
+            out_cnt[u] = ns;
+        }
+        free(all);
+        free(sv);
+    }
+    return err;
 }
 
 /* Exact block-level top-n (textbook top-k, at key-block granularity with the same tile
@@ -615,11 +828,13 @@ static float *gather_paged(const float *pages, int num_pages, int Hkv, int ps, i
     return out;
 }
 
-int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int page_size,
+int oracle_mask_paged_ext(const float *Q, const float *Kpages, int num_pages, int page_size,
                       const int32_t *block_table, int max_pages, const int32_t *seq_lens, int B, int Hq,
                       int Hkv, int Tq, int d, int k, int bq, int bk, int causal, int mode, int32_t *idx,
-                      int32_t *cnt, double *margin_min, double *emax, int64_t *n_scored, int32_t *n_iter)
+                      int32_t *cnt, double *margin_min, double *emax, int64_t *n_scored, int32_t *n_iter,
+                          int chunks, int top_r, int jitter, uint64_t seed)
 {
+    if (top_r < 0 || jitter < 0 || chunks < 1 || bk < 1 || (k / bk) % chunks) return ORC_EINVAL;
     if (page_size < 1 || page_size % bk != 0 || num_pages < 1) return ORC_EINVAL;
     int n = k / bk;
     int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
@@ -639,8 +854,8 @@ int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int pa
                 int64_t u = ((int64_t)b * Hq + h) * nqb + q;
                 const float *Qh = Q + (((int64_t)b * Hq + h) * (int64_t)Tq) * d;
                 orc_diag dg;
-                int r = mask_unit(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, idx + u * n, cnt + u, &dg,
-                                  NULL, NULL, 0);
+                int r = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, chunks, idx + u * n,
+                                          cnt + u, &dg, NULL, NULL, 0, top_r, jitter, seed, u);
                 if (r) {
 #pragma omp critical
                     err = r;
@@ -654,6 +869,16 @@ int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int pa
         }
     }
     return err;
+}
+
+int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int page_size,
+                      const int32_t *block_table, int max_pages, const int32_t *seq_lens, int B, int Hq,
+                      int Hkv, int Tq, int d, int k, int bq, int bk, int causal, int mode, int32_t *idx,
+                      int32_t *cnt, double *margin_min, double *emax, int64_t *n_scored, int32_t *n_iter)
+{
+    return oracle_mask_paged_ext(Q, Kpages, num_pages, page_size, block_table, max_pages, seq_lens, B, Hq, Hkv, Tq,
+                                 d, k, bq, bk, causal, mode, idx, cnt, margin_min, emax, n_scored, n_iter, 1, 0, 0,
+                                 0);
 }
 
 int oracle_sparse_attention_paged_sw(const float *Q, const float *Kpages, const float *Vpages, int num_pages,

@@ -57,12 +57,27 @@ def lib():
         _lib.oracle_block_scores.argtypes = [P, P] + [i32] * 10 + [P, i64, P, P]
         _lib.oracle_sparse_attention.argtypes = [P, P, P] + [i32] * 10 + [f64, P, P, P, P]
         _lib.oracle_dense_attention.argtypes = [P, P, P] + [i32] * 7 + [f64, P, P]
-        _lib.oracle_mask_paged.argtypes = [P, P, i32, i32, P, i32, P] + [i32] * 9 + [P] * 6
+        _lib.oracle_mask_paged.argtypes = [P, P, i32, i32, P, i32, P] + [i32] * 10 + [P] * 6
         _lib.oracle_sparse_attention_paged.argtypes = ([P, P, P, i32, i32, P, i32, P] + [i32] * 9
                                                        + [f64, P, P, P, P])
         _lib.oracle_sparse_attention_sw.argtypes = [P, P, P] + [i32] * 10 + [f64, P, P, i32, i32, P, P]
         _lib.oracle_sparse_attention_paged_sw.argtypes = ([P, P, P, i32, i32, P, i32, P] + [i32] * 9
                                                           + [f64, P, P, i32, i32, P, P])
+        u64 = ctypes.c_uint64
+        _lib.oracle_mask_ext.argtypes = [P, P] + [i32] * 14 + [u64] + [P] * 4
+        _lib.oracle_mask_trace_ext.argtypes = ([P, P] + [i32] * 11 + [i32] * 3 + [P, P, P, P, i32, P, P]
+                                               + [i32, i32, u64])
+        _lib.oracle_mask_paged_ext.argtypes = ([P, P, i32, i32, P, i32, P] + [i32] * 10 + [P] * 6
+                                               + [i32, i32, i32, u64])
+        _lib.oracle_top_r_components.argtypes = [P, i32, i32, i32, P]
+        _lib.oracle_splitmix64.argtypes = [u64]
+        _lib.oracle_splitmix64.restype = u64
+        _lib.oracle_jitter.argtypes = [u64, i64, i32, i64, i32]
+        _lib.oracle_jitter.restype = i64
+        _lib.oracle_vote.argtypes = [i32, i64, i32, P, P, i32, i32, i32, P, P]
+        for name in ("oracle_mask_ext", "oracle_mask_trace_ext", "oracle_mask_paged_ext", "oracle_top_r_components",
+                     "oracle_vote"):
+            getattr(_lib, name).restype = i32
         _lib.oracle_num_threads.restype = i32
         _lib.oracle_set_num_threads.argtypes = [i32]
         for name in ("oracle_mask", "oracle_mask_trace", "oracle_exact_block_topn", "oracle_block_scores",
@@ -106,11 +121,14 @@ def n_blocks(k: int, bk: int) -> int:
     return k // bk
 
 
-def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: bool = False, chunks: int = 1):
+def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: bool = False, chunks: int = 1,
+         top_r: int = 0, jitter: int = 0, seed: int = 0):
     """Alg. 1 mask. Q [B,Hq,Tq,d], K [B,Hkv,Tk,d] -> idx [B,Hq,Nqb,n] (asc, -1 pad), cnt [B,Hq,Nqb].
 
     diag=True also returns dict(margin_min, emax, n_scored, n_iter) per unit.  chunks = S > 1: the
-    stridden partial top-k (reading G21; diag then carries margin_min and emax only)."""
+    stridden partial top-k (reading G21; diag then carries margin_min and emax only).
+    top_r = r in (0, d): top-r approximation (G22).  jitter = R > 0: an ensemble sample
+    with split offsets in [-R, R] from generator seed `seed` (G23)."""
     Q, K = _f32(Q), _f32(K)
     B, Hq, Tq, d = Q.shape
     _, Hkv, Tk, _ = K.shape
@@ -122,10 +140,10 @@ def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: b
     em = np.empty((B, Hq, nqb), np.float64)
     ns = np.empty((B, Hq, nqb), np.int64)
     ni = np.empty((B, Hq, nqb), np.int32)
-    if chunks != 1:
-        rc = lib().oracle_mask_chunked(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, int(chunks),
-                                       _p(idx), _p(cnt), _p(mg), _p(em))
-        _check(rc, "oracle_mask_chunked")
+    if chunks != 1 or top_r or jitter:
+        rc = lib().oracle_mask_ext(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, int(chunks),
+                                   int(top_r), int(jitter), int(seed) & (2**64 - 1), _p(idx), _p(cnt), _p(mg), _p(em))
+        _check(rc, "oracle_mask_ext")
         if diag:
             return idx, cnt, dict(margin_min=mg, emax=em)
         return idx, cnt
@@ -138,7 +156,7 @@ def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: b
 
 
 def mask_trace(Q, K, k: int, bq: int, bk: int, causal: bool, b: int, h: int, q: int, mode: int = F32C,
-               max_trace: int = 64):
+               max_trace: int = 64, top_r: int = 0, jitter: int = 0, seed: int = 0):
     """Node ranges after every iteration of one unit: list of [n,2] arrays (entry 0 = initial)."""
     Q, K = _f32(Q), _f32(K)
     B, Hq, Tq, d = Q.shape
@@ -150,8 +168,9 @@ def mask_trace(Q, K, k: int, bq: int, bk: int, causal: bool, b: int, h: int, q: 
     ts = np.full((max_trace, n), np.nan, np.float64)
     nit = np.zeros(1, np.int32)
     nsc = np.zeros(1, np.int64)
-    rc = lib().oracle_mask_trace(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, b, h, q,
-                                 _p(idx), _p(cnt), _p(tn), _p(ts), max_trace, _p(nit), _p(nsc))
+    rc = lib().oracle_mask_trace_ext(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, b, h, q,
+                                     _p(idx), _p(cnt), _p(tn), _p(ts), max_trace, _p(nit), _p(nsc), int(top_r),
+                                     int(jitter), int(seed) & (2**64 - 1))
     _check(rc, "oracle_mask_trace")
     it = int(nit[0])
     return dict(idx=idx, cnt=int(cnt[0]), nodes=[tn[i] for i in range(it + 1)] if it else [],
@@ -220,7 +239,7 @@ def dense_attention(Q, K, V, causal: bool, sm_scale: float = 0.0):
 
 
 def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causal: bool, mode: int = F32C,
-               diag: bool = False):
+               diag: bool = False, chunks: int = 1, top_r: int = 0, jitter: int = 0, seed: int = 0):
     """Mask on a paged cache. Kpages [num_pages, Hkv, page_size, d]; block_table [B, max_pages]."""
     Q, Kp = _f32(Q), _f32(Kpages)
     bt, sl = _i32(block_table), _i32(seq_lens)
@@ -234,8 +253,9 @@ def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causa
     em = np.empty((B, Hq, nqb), np.float64)
     ns = np.empty((B, Hq, nqb), np.int64)
     ni = np.empty((B, Hq, nqb), np.int32)
-    rc = lib().oracle_mask_paged(_p(Q), _p(Kp), num_pages, ps, _p(bt), bt.shape[1], _p(sl), B, Hq, Hkv, Tq, d,
-                                 k, bq, bk, int(causal), mode, _p(idx), _p(cnt), _p(mg), _p(em), _p(ns), _p(ni))
+    rc = lib().oracle_mask_paged_ext(_p(Q), _p(Kp), num_pages, ps, _p(bt), bt.shape[1], _p(sl), B, Hq, Hkv, Tq,
+                                     d, k, bq, bk, int(causal), mode, _p(idx), _p(cnt), _p(mg), _p(em), _p(ns),
+                                     _p(ni), int(chunks), int(top_r), int(jitter), int(seed) & (2**64 - 1))
     _check(rc, "oracle_mask_paged")
     if diag:
         return idx, cnt, dict(margin_min=mg, emax=em, n_scored=ns, n_iter=ni)
@@ -257,3 +277,38 @@ def sparse_attention_paged(Q, Kpages, Vpages, block_table, seq_lens, k: int, bq:
                                                 _p(lse))
     _check(rc, "oracle_sparse_attention_paged")
     return O, lse
+
+
+def top_r_components(Qb, r: int) -> np.ndarray:
+    """argtop_r(|q|) of one query block Qb [rows, d] (reading G22) -> r components, ascending."""
+    Qb = _f32(Qb)
+    rows, d = Qb.shape
+    out = np.empty(r, np.int32)
+    _check(lib().oracle_top_r_components(_p(Qb), rows, d, int(r), _p(out)), "oracle_top_r_components")
+    return out
+
+
+def splitmix64(state: int) -> int:
+    """First output of splitmix64 seeded with `state` (the ensemble's counter-based generator)."""
+    return int(lib().oracle_splitmix64(int(state) & (2**64 - 1)))
+
+
+def jitter_offset(seed: int, lin: int, it: int, f: int, R: int) -> int:
+    """Split offset u in [-R, R] of node (first block f) at iteration it of unit lin (reading G23)."""
+    return int(lib().oracle_jitter(int(seed) & (2**64 - 1), int(lin), int(it), int(f), int(R)))
+
+
+def vote(idx_samples, cnt_samples, theta: int, tau: int, n_out: int | None = None):
+    """Ensemble vote (reading G24).  idx_samples [n_e, ..., n], cnt_samples [n_e, ...]
+    -> (idx [..., n_out] ascending, -1 pad, cnt [...]).  n_out defaults to n (tau = 1) or n_e * n."""
+    I, C = _i32(idx_samples), _i32(cnt_samples)
+    n_e, n = I.shape[0], I.shape[-1]
+    lead = I.shape[1:-1]
+    units = int(np.prod(lead)) if lead else 1
+    if n_out is None:
+        n_out = n if tau else n_e * n
+    out = np.empty(lead + (n_out,), np.int32)
+    oc = np.empty(lead, np.int32)
+    _check(lib().oracle_vote(n_e, units, n, _p(I), _p(C), int(theta), int(tau), int(n_out), _p(out), _p(oc)),
+           "oracle_vote")
+    return out, oc

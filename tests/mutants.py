@@ -35,6 +35,17 @@ MUTANTS = {
     "window one token too long": ("for (int64_t s = p - window + 1; s <= p; ++s)", "for (int64_t s = p - window; s <= p; ++s)"),
     "sink ignores causality": ("for (int64_t s = 0; s < imin64(sink, Tk); ++s)\n                    if (!causal || s <= p) tok[ntok++] = s;",
                                "for (int64_t s = 0; s < imin64(sink, Tk); ++s)\n                    tok[ntok++] = s;"),
+    "top-r reduces |q| over the first row only": ("for (int64_t t = t0; t < t1; ++t) {\n            double v = fabs(",
+                                                 "for (int64_t t = t0; t < t0 + 1; ++t) {\n            double v = fabs("),
+    "top-r ties toward the larger component": ("if (!taken[c] && (best < 0 || a[c] > a[best])) best = c;",
+                                               "if (!taken[c] && (best < 0 || a[c] >= a[best])) best = c;"),
+    "top-r score ignores the component list": ("int c = comp ? comp[i] : i;\n                    acc = fmaf(q[c], kk[c], acc);",
+                                               "int c = i;\n                    acc = fmaf(q[c], kk[c], acc);"),
+    "jitter range one short": ("% (uint64_t)(2 * R + 1)) - R;", "% (uint64_t)(2 * R)) - R;"),
+    "jitter clamp allows an empty left branch": ("if (m < f + 1) m = f + 1;", "if (m < f) m = f;"),
+    "vote truncation prefers larger blocks": ("return (a->j > b->j) - (a->j < b->j);\n}\n\nstatic int i32_cmp",
+                                              "return (a->j < b->j) - (a->j > b->j);\n}\n\nstatic int i32_cmp"),
+    "vote threshold strict": ("if (j - i >= theta)", "if (j - i > theta)"),
     "union keeps duplicates": ("if (w == 0 || tok[i] != tok[w - 1]) tok[w++] = tok[i];", "tok[w++] = tok[i];"),
 }
 

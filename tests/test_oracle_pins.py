@@ -596,3 +596,228 @@ def test_chunks_one_level_is_exact_topn_per_chunk(orc, S):
                 checked += 1
         assert cnt[0, 0, q] == n
     assert checked > 0
+
+
+# --------------------------------------------------------------------------------------------
+# f4a: top-r approximation: q.k ~ sum over the r components with the largest |q_c|;
+# reading G22: a query block reduces |q_c| by the max over its rows, ties -> smaller component,
+# terms summed in ascending component order.
+# --------------------------------------------------------------------------------------------
+def _brute_top_r(Qb, r):
+    a = np.abs(np.asarray(Qb, np.float64)).max(axis=0)
+    order = np.lexsort((np.arange(len(a)), -a))
+    return np.sort(order[:r])
+
+
+def test_topr_spec_examples(orc):
+    """SPEC top_r_select examples and the tie rule."""
+    assert orc.top_r_components([[3, -5, 1]], 2).tolist() == [0, 1]
+    assert orc.top_r_components([[3, -5, 1]], 3).tolist() == [0, 1, 2]
+    assert orc.top_r_components([[1, 0], [0, 2]], 1).tolist() == [1]  # componentwise max |q| = [1, 2]
+    assert orc.top_r_components([[2, -2, 1]], 1).tolist() == [0]      # tie -> smaller component
+    assert orc.top_r_components([[0, 1, -1, 1]], 2).tolist() == [1, 2]
+
+
+def test_topr_components_brute_force(orc):
+    rng = np.random.default_rng(70)
+    for _ in range(200):
+        rows, d = int(rng.integers(1, 9)), int(rng.integers(2, 40))
+        r = int(rng.integers(1, d + 1))
+        Qb = rng.integers(-3, 4, size=(rows, d)).astype(np.float32)  # many ties
+        assert np.array_equal(orc.top_r_components(Qb, r), _brute_top_r(Qb, r))
+
+
+def test_topr_r_equals_d_is_plain(orc):
+    Q, K, _ = synth.gen_qkv(1, 2, 1, 1500, 1500, 32, "llm", seed=71, dtype=torch.float32, make_v=False)
+    a = orc.mask(Q, K, 64, 16, 2, True)
+    for r in (32, 0):
+        b = orc.mask(Q, K, 64, 16, 2, True, top_r=r)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_topr_fixed_components_equal_sliced_problem(orc):
+    """If every query block's top-r set is the same P, the top-r mask is the plain mask of the problem
+    restricted to the components P (Q[..., P], K[..., P]) — bit-identical, since both sum q_c k_c
+    over P in ascending order."""
+    T, d, r = 2000, 32, 8
+    Q, K, _ = synth.gen_qkv(1, 2, 1, T, T, d, "int", seed=72, dtype=torch.float32, make_v=False)
+    Q = Q.clone()
+    P = np.array([1, 4, 5, 11, 17, 20, 26, 31])
+    sign = torch.where(Q[..., P] >= 0, 1.0, -1.0)
+    Q[..., P] = sign * (8.0 + Q[..., P].abs())  # |q_c| >= 8 > 4 >= the others
+    for mode in (orc.F32C, orc.F64):
+        a = orc.mask(Q, K, 64, 16, 2, True, mode=mode, top_r=r)
+        b = orc.mask(Q[..., P].contiguous(), K[..., P].contiguous(), 64, 16, 2, True, mode=mode)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        c = orc.mask(Q, K, 64, 16, 2, True, mode=mode)
+        assert not np.array_equal(a[0], c[0])  # the approximation really changes the mask
+
+
+def test_topr_one_level_is_exact_topn_of_approximate_scores(orc):
+    """n < B_q <= 2n: the mask is the exact top-n of the block maxima of the APPROXIMATE scores
+    sum_{c in P_q} q_c k_c, P_q = argtop_r of the block (numpy brute force, per query block)."""
+    T, d, k, bq, bk, r = 1024, 32, 128, 16, 2, 6
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "int", seed=73, dtype=torch.float32, make_v=False)
+    n = k // bk
+    idx, _ = orc.mask(Q, K, k, bq, bk, True, top_r=r)
+    Qn, Kn = Q.double().numpy()[0, 0], K.double().numpy()[0, 0]
+    checked = 0
+    for q in range(T // bq):
+        vis = _visible(q, bq, bk, T, T, True)
+        if not (n < vis <= 2 * n):
+            continue
+        P = _brute_top_r(Qn[q * bq:(q + 1) * bq], r)
+        Qz = np.zeros_like(Qn)
+        Qz[q * bq:(q + 1) * bq, P] = Qn[q * bq:(q + 1) * bq, P]
+        bs = _brute_block_scores(Qz[None, None], Kn[None, None], bq, bk, True)[0, 0, q, :vis]
+        assert np.array_equal(idx[0, 0, q], _topn_sorted(bs, n)), q
+        checked += 1
+    assert checked == 8
+
+
+# --------------------------------------------------------------------------------------------
+# f4b: HiP ensemble (P:1162-1184).  Samples: every split is moved "around the center" by a random
+# integer in [-R, R] (reading G23), clamped so both branches stay non-empty, drawn from splitmix64
+# keyed by (seed, unit, iteration, node).  Vote: an index survives with >= theta votes; tau = 1
+# truncates to n by (votes desc, block asc) (reading G24).
+# --------------------------------------------------------------------------------------------
+def test_splitmix64_published_vectors(orc):
+    """splitmix64 seeded with 0: the published first outputs (Vigna's reference implementation)."""
+    g = 0x9E3779B97F4A7C15
+    assert orc.splitmix64(0) == 0xE220A8397B1DCDAF
+    assert orc.splitmix64(g) == 0x6E789E6AA1B965F4
+    assert orc.splitmix64((2 * g) % 2**64) == 0x06C45D188009454F
+
+
+def test_jitter_offsets_uniform(orc):
+    """u is uniform on the 2R+1 integers [-R, R] (chi-square, loose) for any key."""
+    for R in (1, 3, 5):
+        u = np.array([orc.jitter_offset(7, lin, it, f, R) for lin in range(20) for it in range(5)
+                      for f in range(0, 600, 7)])
+        assert u.min() == -R and u.max() == R
+        cnt = np.bincount(u + R, minlength=2 * R + 1)
+        exp = len(u) / (2 * R + 1)
+        assert ((cnt - exp) ** 2 / exp).sum() < 4 * (2 * R + 1)
+    assert orc.jitter_offset(7, 3, 1, 40, 0) == 0
+
+
+def test_jitter_zero_is_plain_and_deterministic(orc):
+    Q, K, _ = synth.gen_qkv(1, 2, 1, 3000, 3000, 32, "llm", seed=74, dtype=torch.float32, make_v=False)
+    a = orc.mask(Q, K, 64, 16, 2, True)
+    b = orc.mask(Q, K, 64, 16, 2, True, jitter=0, seed=123)
+    assert np.array_equal(a[0], b[0])
+    c1 = orc.mask(Q, K, 64, 16, 2, True, jitter=5, seed=9)
+    c2 = orc.mask(Q, K, 64, 16, 2, True, jitter=5, seed=9)
+    c3 = orc.mask(Q, K, 64, 16, 2, True, jitter=5, seed=10)
+    assert np.array_equal(c1[0], c2[0])
+    assert not np.array_equal(c1[0], a[0]) and not np.array_equal(c1[0], c3[0])
+
+
+def test_jitter_one_level_unchanged(orc):
+    """B_q <= 2n: every initial node has <= 2 blocks, whose only split is (f, f)(l, l) — the jitter
+    cannot move it, so the sample equals the deterministic mask."""
+    T, d, k, bq, bk = 1024, 32, 128, 16, 2
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=75, dtype=torch.float32, make_v=False)
+    a = orc.mask(Q, K, k, bq, bk, True)
+    b = orc.mask(Q, K, k, bq, bk, True, jitter=4, seed=3)
+    n = k // bk
+    for q in range(T // bq):
+        if _visible(q, bq, bk, T, T, True) <= 2 * n:
+            assert np.array_equal(a[0][0, 0, q], b[0][0, 0, q])
+
+
+def test_jitter_trace_invariants(orc):
+    """Jittered samples keep PIN-5's invariants: n disjoint non-empty nested nodes per iteration,
+    each split point within R of the half-up midpoint; final: n distinct ascending visible blocks."""
+    T, d, k, bq, bk, R = 3000, 32, 96, 16, 2, 3
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "llm", seed=76, dtype=torch.float32, make_v=False)
+    n = k // bk
+    moved = 0
+    for q in [7, 50, 101, 150, -(-T // bq) - 1]:
+        vis = _visible(q, bq, bk, T, T, True)
+        tr = orc.mask_trace(Q, K, k, bq, bk, True, 0, 0, q, jitter=R, seed=5)
+        prev = None
+        for nodes in tr["nodes"]:
+            f, l = nodes[:, 0], nodes[:, 1]
+            assert (l >= f).all() and (f >= 0).all() and (l < vis).all()
+            o = np.argsort(f)
+            assert (f[o][1:] > l[o][:-1]).all()  # disjoint
+            if prev is not None:
+                pf, pl = prev
+                for a, b in zip(f, l):  # nested in a parent; a split child starts at f or at m
+                    j = np.nonzero((pf <= a) & (b <= pl))[0]
+                    assert len(j) == 1
+                    pa, pb = pf[j[0]], pl[j[0]]
+                    mid = (pa + pb + 1) // 2
+                    if (a, b) != (pa, pb):
+                        m = a if a > pa else b + 1
+                        assert pa + 1 <= m <= pb and abs(m - mid) <= R
+                        moved += m != mid
+            prev = (f, l)
+        final = tr["idx"][: tr["cnt"]]
+        assert tr["cnt"] == n and (np.diff(final) > 0).all() and final[-1] < vis
+    assert moved > 0
+
+
+def test_vote_spec_examples(orc):
+    A, B, C = 3, 7, 9
+    def v(samples, theta, tau, n):
+        I = np.full((len(samples), 1, n), -1, np.int32)
+        Cn = np.zeros((len(samples), 1), np.int32)
+        for e, s in enumerate(samples):
+            I[e, 0, :len(s)] = sorted(s)
+            Cn[e, 0] = len(s)
+        idx, cnt = orc.vote(I, Cn, theta, tau)
+        return idx[0, :cnt[0]].tolist()
+    assert v([[A], [A, B]], 2, 0, 2) == [A]
+    assert v([[A], [B]], 1, 0, 2) == [A, B]
+    assert v([[A], [A, B], [B, C]], 1, 1, 2) == [A, B]
+    assert v([[A, B]], 1, 0, 2) == [A, B]
+
+
+def test_vote_brute_force(orc):
+    """Counter-based brute force: survivors, truncation order, ascending output; monotone in theta;
+    theta = n_e is the intersection, theta = 1 (tau = 0) the union."""
+    from collections import Counter
+    rng = np.random.default_rng(77)
+    for _ in range(60):
+        n_e, n, units = int(rng.integers(1, 6)), int(rng.integers(1, 12)), 5
+        hi = int(rng.integers(n, 3 * n + 2))
+        I = np.full((n_e, units, n), -1, np.int32)
+        Cn = np.zeros((n_e, units), np.int32)
+        for e in range(n_e):
+            for u in range(units):
+                c = int(rng.integers(0, n + 1))
+                I[e, u, :c] = np.sort(rng.choice(hi, c, replace=False))
+                Cn[e, u] = c
+        prev = None
+        for theta in range(1, n_e + 1):
+            for tau in (0, 1):
+                idx, cnt = orc.vote(I, Cn, theta, tau)
+                for u in range(units):
+                    votes = Counter(x for e in range(n_e) for x in I[e, u, :Cn[e, u]].tolist())
+                    surv = sorted(x for x, c in votes.items() if c >= theta)
+                    if tau and len(surv) > n:
+                        surv = sorted(sorted(surv, key=lambda x: (-votes[x], x))[:n])
+                    got = idx[u, :cnt[u]].tolist()
+                    assert got == surv
+                    assert (idx[u, cnt[u]:] == -1).all()
+                    if theta == n_e and not tau:
+                        inter = set.intersection(*[set(I[e, u, :Cn[e, u]].tolist()) for e in range(n_e)])
+                        assert set(got) == inter
+                    if theta == 1 and not tau:
+                        assert set(got) == set(votes)
+            cur = orc.vote(I, Cn, theta, 0)
+            if prev is not None:
+                for u in range(units):
+                    assert set(cur[0][u, :cur[1][u]].tolist()) <= set(prev[0][u, :prev[1][u]].tolist())
+            prev = cur
+
+
+def test_ensemble_single_sample_is_plain(orc):
+    """(n_e = 1, R = 0, theta = 1): the pipeline output equals the deterministic mask (SPEC)."""
+    Q, K, _ = synth.gen_qkv(1, 2, 1, 2000, 2000, 32, "llm", seed=78, dtype=torch.float32, make_v=False)
+    a = orc.mask(Q, K, 64, 16, 2, True)
+    s = orc.mask(Q, K, 64, 16, 2, True, jitter=0, seed=4)
+    idx, cnt = orc.vote(s[0][None], s[1][None], 1, 1)
+    assert np.array_equal(idx, a[0]) and np.array_equal(cnt, a[1])
