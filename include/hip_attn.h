@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define HIP_ATTN_VERSION 100 /* 1.0.0 */
+#define HIP_ATTN_VERSION 110 /* 1.1.0: top_r, split_jitter, sample_seed, hip_mask_vote */
 
 typedef enum {
     HIP_SUCCESS = 0,
@@ -79,6 +79,17 @@ typedef struct {
                               into S contiguous chunks [a_s, a_{s+1}), a_s = floor((2 s B_q + S)/(2 S)),
                               each searched with n / S nodes by its own job (S x more parallel jobs);
                               the output concatenates the chunks (still ascending, cnt = n).        */
+    int32_t top_r;         /* mask only: top-r approximation (reading G22).  0 (or >= d) =
+                              exact branch scores.  0 < r < d: a branch score sums q_c k_c over the r
+                              components with the largest max-over-rows |q_c| of the query block
+                              (ties -> smaller c) only; key chunks holding no kept component are not
+                              fetched.                                                              */
+    int32_t split_jitter;  /* mask only: ensemble sampling (reading G23).  0 = Alg. 1's
+                              half-up split.  R > 0 (<= 65535): every split point moves by u uniform in
+                              [-R, R] (splitmix64 keyed by sample_seed, the unit (b*H_q + h)*N_qb + q,
+                              the iteration and the node's first block), clamped so both branches stay
+                              non-empty.  Combine samples with hip_mask_vote.                       */
+    uint64_t sample_seed;  /* mask only: seed of the ensemble sample (ignored when split_jitter = 0) */
 } hip_params_t;
 
 typedef struct {
@@ -189,6 +200,29 @@ hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H
                                          const hip_params_t* params, const int32_t* block_idx,
                                          const int32_t* block_cnt, hip_tensor_t o, float* lse, void* workspace,
                                          size_t workspace_bytes, void* stream);
+
+/*
+ * hip_mask_vote — the HiP ensemble vote (Appendix D; reading G24).
+ *
+ *   n_e          number of sample masks, 1 <= n_e <= 16 (typically hip_mask_estimate outputs with
+ *                split_jitter > 0 and different sample_seed)
+ *   units        number of query blocks per sample (B * H_q * N_qb)
+ *   n_in         index row length of the samples (n = k / b_k); n_e * n_in <= 4096
+ *   block_idx_samples  [n_e, units, n_in] int32 device, each row ascending distinct, -1 padded
+ *   block_cnt_samples  [n_e, units] int32 device
+ *   theta        agreement threshold, 1 <= theta <= n_e (1 = union, n_e = intersection)
+ *   tau          0: keep every index with >= theta votes (a row may exceed n_in — dynamic sparsity);
+ *                1: keep at most n_in of them, by (votes desc, block asc)
+ *   n_out        OUT row length: >= n_in if tau = 1, >= n_e * n_in if tau = 0
+ *   block_idx    OUT [units, n_out] ascending, -1 padded; block_cnt OUT [units]
+ *   The outputs feed hip_sparse_attention_* with a params whose k = n_out * b_k.
+ *   Errors: INVALID_VALUE for NULL pointers or out-of-range n_e / n_in / theta / tau / n_out;
+ *   NOT_SUPPORTED on a device that is not sm_100.  Sample rows must be ascending and distinct (not
+ *   checked on the device; other input gives an unspecified but in-bounds result).
+ */
+hip_status_t hip_mask_vote(int32_t n_e, int64_t units, int32_t n_in, const int32_t* block_idx_samples,
+                           const int32_t* block_cnt_samples, int32_t theta, int32_t tau, int32_t n_out,
+                           int32_t* block_idx, int32_t* block_cnt, void* stream);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,9 @@ hip_status_t check_common(hip_dtype_t dt, int32_t B, int32_t Hq, int32_t Hkv, in
   if (p->chunks < 0 || (p->chunks > 1 && (p->k / p->b_k) % p->chunks))
     return fail(HIP_ERROR_INVALID_VALUE, "chunks=%d must be >= 0 and divide n = k/b_k = %d", p->chunks,
                 p->k / p->b_k);
+  if (p->top_r < 0) return fail(HIP_ERROR_INVALID_VALUE, "top_r=%d must be >= 0", p->top_r);
+  if (p->split_jitter < 0 || p->split_jitter > 65535)
+    return fail(HIP_ERROR_INVALID_VALUE, "split_jitter=%d must be in [0, 65535]", p->split_jitter);
   if (p->sink_tokens < 0 || p->window_tokens < 0)
     return fail(HIP_ERROR_INVALID_VALUE, "sink_tokens=%d window_tokens=%d must be >= 0", p->sink_tokens,
                 p->window_tokens);
@@ -124,6 +127,9 @@ hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk
   s.nqb = (Tq + s.bq - 1) / s.bq;
   s.sink = p->sink_tokens; s.window = p->window_tokens;
   s.chunks = p->chunks > 1 ? p->chunks : 1;
+  s.top_r = p->top_r > 0 && p->top_r < d ? p->top_r : 0;
+  s.jitter = p->split_jitter;
+  s.seed = p->sample_seed;
   s.seq_lens = seq_lens;
   return s;
 }
@@ -205,6 +211,28 @@ hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_
   else
     e = hip::launch_mask_cc(sh, qs, ks, dtype == HIP_DTYPE_BF16, block_idx, block_cnt, st, sms);
   if (e != cudaSuccess) return cuda_fail(e, "hip_mask_estimate launch");
+  return HIP_SUCCESS;
+}
+
+hip_status_t hip_mask_vote(int32_t n_e, int64_t units, int32_t n_in, const int32_t* block_idx_samples,
+                           const int32_t* block_cnt_samples, int32_t theta, int32_t tau, int32_t n_out,
+                           int32_t* block_idx, int32_t* block_cnt, void* stream) {
+  if (!block_idx_samples || !block_cnt_samples || !block_idx || !block_cnt)
+    return fail(HIP_ERROR_INVALID_VALUE, "hip_mask_vote: NULL pointer");
+  if (n_e < 1 || n_e > 16) return fail(HIP_ERROR_INVALID_VALUE, "n_e=%d must be in [1, 16]", n_e);
+  if (units < 0) return fail(HIP_ERROR_INVALID_VALUE, "units=%lld < 0", (long long)units);
+  if (n_in < 1 || (int64_t)n_e * n_in > 4096)
+    return fail(HIP_ERROR_INVALID_VALUE, "n_in=%d: need 1 <= n_in and n_e * n_in <= 4096", n_in);
+  if (theta < 1 || theta > n_e) return fail(HIP_ERROR_INVALID_VALUE, "theta=%d must be in [1, n_e=%d]", theta, n_e);
+  if (tau != 0 && tau != 1) return fail(HIP_ERROR_INVALID_VALUE, "tau=%d must be 0 or 1", tau);
+  if (n_out < (tau ? n_in : n_e * n_in))
+    return fail(HIP_ERROR_INVALID_VALUE, "n_out=%d < %d", n_out, tau ? n_in : n_e * n_in);
+  int sms = 0;
+  hip_status_t s;
+  if ((s = device_info(&sms))) return s;
+  cudaError_t e = hip::launch_vote(n_e, units, n_in, block_idx_samples, block_cnt_samples, theta, tau, n_out,
+                                   block_idx, block_cnt, static_cast<cudaStream_t>(stream), sms);
+  if (e != cudaSuccess) return cuda_fail(e, "hip_mask_vote launch");
   return HIP_SUCCESS;
 }
 

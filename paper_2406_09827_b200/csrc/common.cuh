@@ -64,6 +64,9 @@ struct Shape {
   int nqb;
   int sink, window;  // attention: sink / sliding-window tokens (sinkwin.cuh), 0 = off
   int chunks;        // mask: stridden partial top-k chunks S (select.cuh chunk_job), 1 = Alg. 1
+  int top_r;         // mask: top-r approximation (topr.cuh), 0 = all d components
+  int jitter;        // mask: ensemble split jitter R (select.cuh SplitJitter), 0 = half-up split
+  uint64_t seed;     // mask: ensemble sample seed
   const int32_t* seq_lens;
 };
 

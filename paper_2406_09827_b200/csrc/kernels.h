@@ -78,4 +78,8 @@ cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, co
                            const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                            float* lse, cudaStream_t stream, int num_sms);
 
+// Ensemble vote (vote.cu).
+cudaError_t launch_vote(int n_e, int64_t units, int n_in, const int32_t* idx, const int32_t* cnt, int theta, int tau,
+                        int n_out, int32_t* out_idx, int32_t* out_cnt, cudaStream_t stream, int num_sms);
+
 }  // namespace hip

@@ -11,6 +11,7 @@
 // pairs, and one thread per block takes the tile max over the valid (causal) pairs.
 #include "kernels.h"
 #include "select.cuh"
+#include "topr.cuh"
 
 namespace hip {
 
@@ -147,13 +148,16 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
         qs[t * qpitch + c] = v;
       }
       __syncthreads();
+      if (sh.top_r > 0 && sh.top_r < sh.d)  // top-r approximation (G22)
+        top_r_zero_f32<kCCThreads>(qs, qpitch, rows_q, sh.d, sh.top_r, st.rep_s);
     }
     CCScorer<T> sc;
     sc.qs = qs; sc.qpitch = qpitch; sc.stage0 = stage0; sc.stage_bytes = stage_bytes; sc.kpitch = kpitch;
     sc.pairs = pairs; sc.ks = ks; sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.d = sh.d; sc.bk = sh.bk;
     sc.causal = sh.causal; sc.rows_q = rows_q; sc.ch = ch;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
-    tree_search<NMAX, kCCThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr);
+    tree_search<NMAX, kCCThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
+                            make_jitter(sh.jitter, sh.seed, lin));
     if (cs == 0 && threadIdx.x == 0) cnt[lin] = min(Bq, sh.n);
     __syncthreads();
   }

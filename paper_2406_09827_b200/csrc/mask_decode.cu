@@ -14,6 +14,7 @@
 // select.cuh.
 #include "kernels.h"
 #include "select.cuh"
+#include "topr.cuh"
 
 namespace hip {
 
@@ -141,6 +142,8 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
         qs[t * D + c] = v;
       }
       __syncthreads();
+      if (sh.top_r > 0 && sh.top_r < D)  // top-r approximation (G22)
+        top_r_zero_f32<kMDThreads>(qs, D, rows_q, D, sh.top_r, st.rep_s);
     }
     LaneScorer<T, D, RM, kPaged> sc;
     sc.qs = qs;
@@ -149,7 +152,8 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
     sc.row_bytes = (uint32_t)(ks.st * ks.esize);
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
-    tree_search<NMAX, kMDThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr);
+    tree_search<NMAX, kMDThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
+                            make_jitter(sh.jitter, sh.seed, lin));
     if (cs == 0 && threadIdx.x == 0) cnt[lin] = min(Bq, sh.n);
     __syncthreads();
   }

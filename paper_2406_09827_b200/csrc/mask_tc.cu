@@ -34,6 +34,7 @@
 
 #include "kernels.h"
 #include "select.cuh"
+#include "topr.cuh"
 
 namespace hip {
 
@@ -77,6 +78,8 @@ struct TCScorer {
   const int* pg;         // paged: page of each representative block (aliases the score output)
   const char* rp[RJ];    // this thread's source rows of the tile being issued
   uint32_t rok;          // bit j: rp[j] is a real row (< T_k, block < n_rep)
+  uint32_t ckeep = 3u;   // top-r: bit h = this thread's chunk of d-half h has a kept component
+                         // (else the chunk is zero-filled without a global read, topr.cuh)
   HIP_PT_MEMBER
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
@@ -116,7 +119,7 @@ struct TCScorer {
     const uint32_t dst = k_s0 + (i % SLOTS) * kMTSlot + sw128_off(r0, c8);
 #pragma unroll
     for (int j = 0; j < RJ; ++j)  // rows r0 + RPP j share r0's swizzle phase (RPP % 8 == 0)
-      cp_async16(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & 1u) ? 16u : 0u);
+      cp_async16(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
   }
 
   // b_k = 2: rows 8g..8g+7 of the tile are the 4 blocks 4g..4g+3, so one 16-byte load brings their
@@ -142,7 +145,7 @@ struct TCScorer {
     const uint32_t x = (uint32_t)c8;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      cp_async16(dst + j * 128 + ((x ^ j) << 4), rp[j] + h * 128, ((rok >> j) & 1u) ? 16u : 0u);
+      cp_async16(dst + j * 128 + ((x ^ j) << 4), rp[j] + h * 128, ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
   }
 
   __device__ __forceinline__ void wait_slot(int slot) {
@@ -333,7 +336,43 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     int lo, len, nn, slot0;
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     const uint32_t q_s = sbase + L::q + team * kQTileBytes;
-    if (Bq > sh.n) {
+    uint32_t ckeep = 3u;  // bit h: this thread's 16-byte key chunk of d-half h holds a kept component
+    if (Bq > sh.n && sh.top_r > 0 && sh.top_r < 128) {
+      // top-r approximation (G22; topr.cuh): a_c = max_t |q_tc| (thread c), keep bits by
+      // rank -> st.warp_tot[c / 32]; the query tile is stored with the dropped components zeroed
+      float* a = reinterpret_cast<float*>(st.rep);
+      {
+        const int c = Sync::tid();
+        float m = 0.f;
+        for (int t = 0; t < rows_q; ++t) {
+          const __nv_bfloat16 v = *reinterpret_cast<const __nv_bfloat16*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + t) + 2 * c);
+          m = fmaxf(m, fabsf(__bfloat162float(v)));
+        }
+        a[c] = m;
+      }
+      Sync::sync();
+      const unsigned kb = __ballot_sync(0xffffffffu, top_r_keep(a, 128, Sync::tid(), sh.top_r));
+      if ((threadIdx.x & 31) == 0) st.warp_tot[Sync::tid() >> 5] = (int)kb;
+      Sync::sync();
+      const uint32_t kw[4] = {(uint32_t)st.warp_tot[0], (uint32_t)st.warp_tot[1], (uint32_t)st.warp_tot[2],
+                              (uint32_t)st.warp_tot[3]};
+      for (int p = Sync::tid(); p < 32 * 16; p += NT) {
+        const int r = p >> 4, c16 = p & 15;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < rows_q) v = *reinterpret_cast<const uint4*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + r) + c16 * 16);
+        const uint32_t kbyte = (kw[c16 >> 2] >> ((c16 & 3) * 8)) & 0xffu;
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          w[e] &= (((kbyte >> (2 * e)) & 1u) ? 0x0000ffffu : 0u) | (((kbyte >> (2 * e + 1)) & 1u) ? 0xffff0000u : 0u);
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(q_s + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7)),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
+      }
+      const int c8 = Sync::tid() & 7;  // the gather chunk of this thread: components 64 h + 8 c8 .. + 8
+      ckeep = (((kw[c8 >> 2] >> ((c8 & 3) * 8)) & 0xffu) ? 1u : 0u) |
+              (((kw[2 + (c8 >> 2)] >> ((c8 & 3) * 8)) & 0xffu) ? 2u : 0u);
+      cp_async_commit();  // (empty group: keeps the ring's group accounting unchanged)
+    } else if (Bq > sh.n) {
       // query block -> K-major SW128 tile (B operand, N = 32 rows, rows >= rows_q zero); waited for
       // together with the first item of the first round
       for (int p = Sync::tid(); p < 32 * 16; p += NT) {
@@ -357,11 +396,13 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.bpt = 128 >> lbk;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+    sc.ckeep = ckeep;
 #ifdef HIPATTN_PHASES
     sc.pt = &ptimer;
     ptimer.mark(7);  // unit setup / Q load / exact units
 #endif
-    tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr);
+    tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
+                                                 make_jitter(sh.jitter, sh.seed, lin));
     if (cs == 0 && Sync::tid() == 0) cnt[lin] = min(Bq, sh.n);
     Sync::sync();
   }

@@ -188,6 +188,35 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
   }
 }
 
+// Ensemble sampling (reading G23): every split point moves by u uniform in [-R, R],
+// m = clamp(floor((f + l + 1) / 2) + u, f + 1, l), u drawn from splitmix64 (Steele, Lea & Flood's
+// published output function) keyed by (seed, unit, iteration, first block of the node).  R = 0 is
+// the deterministic half-up split.
+struct SplitJitter {
+  int R = 0;
+  uint64_t key = 0;
+};
+__device__ __forceinline__ uint64_t splitmix_out(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ SplitJitter make_jitter(int R, uint64_t seed, int64_t lin) {
+  SplitJitter j;
+  j.R = R;
+  j.key = R > 0 ? splitmix_out(splitmix_out(seed + 0x9E3779B97F4A7C15ull) ^ (uint64_t)lin) : 0ull;
+  return j;
+}
+__device__ __forceinline__ int jittered_split(const SplitJitter& jt, int iter, int f, int l) {
+  int m = (f + l + 1) >> 1;
+  if (jt.R > 0) {
+    const uint64_t x = splitmix_out(jt.key ^ (((uint64_t)(uint32_t)iter << 32) | (uint64_t)(uint32_t)f));
+    m += (int)(x % (uint64_t)(2 * jt.R + 1)) - jt.R;
+    m = min(max(m, f + 1), l);
+  }
+  return m;
+}
+
 // Stridden partial top-k (reading G21): a launch runs units x S jobs; job (unit, s)
 // searches chunk s = [a_s, a_{s+1}), a_s = floor((2 s B_q + S) / (2 S)), with n / S nodes and writes
 // slots [s n / S, (s + 1) n / S) of the unit's output.  S = 1, or B_q <= n (exact case, chunk 0
@@ -210,7 +239,7 @@ __device__ __forceinline__ bool chunk_job(int Bq, int n, int S, int s, int& lo, 
 // end with a Sync::sync(); Scorer::mark(p) is a profiling hook (no-op in product builds).
 template <int NMAX, int NT, class Scorer, class Sync = CtaSync>
 __device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& scorer, int32_t* out_idx,
-                            int32_t* out_cnt) {
+                            int32_t* out_cnt, const SplitJitter& jit = SplitJitter()) {
   static_assert(NMAX % NT == 0 || NT % NMAX == 0, "NMAX and NT must nest");
   constexpr int E = NMAX >= NT ? NMAX / NT : 1;  // nodes per thread (contiguous)
   constexpr int EC = 2 * E;                      // candidates per thread (their children)
@@ -273,7 +302,7 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& s
       ks[2 * i] = ks[2 * i + 1] = 0u;
       if (j < n) {
         const bool split = l[i] > f[i];
-        const int m = (f[i] + l[i] + 1) >> 1;
+        const int m = split ? jittered_split(jit, iter, f[i], l[i]) : f[i];
         kf[2 * i] = f[i];
         kl[2 * i] = split ? m - 1 : l[i];
         ks[2 * i] = s[i];

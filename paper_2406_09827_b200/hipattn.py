@@ -23,7 +23,7 @@ HIP_FLAG_EXACT_SCORES = 1
 HIP_OP_MASK, HIP_OP_PREFILL, HIP_OP_DECODE = 0, 1, 2
 
 EXPORTS = ("hip_version", "hip_last_error", "hip_num_blocks", "hip_workspace_bytes", "hip_mask_estimate",
-           "hip_sparse_attention_prefill", "hip_sparse_attention_decode")
+           "hip_sparse_attention_prefill", "hip_sparse_attention_decode", "hip_mask_vote")
 
 
 class HipError(RuntimeError):
@@ -35,7 +35,8 @@ class HipError(RuntimeError):
 class Params(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("b_q", ctypes.c_int32), ("b_k", ctypes.c_int32), ("causal", ctypes.c_int32),
                 ("sm_scale", ctypes.c_float), ("flags", ctypes.c_uint32), ("sink_tokens", ctypes.c_int32),
-                ("window_tokens", ctypes.c_int32), ("chunks", ctypes.c_int32)]
+                ("window_tokens", ctypes.c_int32), ("chunks", ctypes.c_int32), ("top_r", ctypes.c_int32),
+                ("split_jitter", ctypes.c_int32), ("sample_seed", ctypes.c_uint64)]
 
 
 class TensorDesc(ctypes.Structure):
@@ -74,6 +75,8 @@ def load(path: str = LIB_PATH):
     lib.hip_sparse_attention_prefill.restype = ctypes.c_int
     lib.hip_sparse_attention_prefill.argtypes = ([ctypes.c_int] + [i32] * 6 + [TensorDesc] * 3 +
                                                  [ctypes.POINTER(Params), P, P, TensorDesc, P, P])
+    lib.hip_mask_vote.restype = ctypes.c_int
+    lib.hip_mask_vote.argtypes = [i32, ctypes.c_int64, i32, P, P, i32, i32, i32, P, P, P]
     lib.hip_sparse_attention_decode.restype = ctypes.c_int
     lib.hip_sparse_attention_decode.argtypes = ([ctypes.c_int] + [i32] * 5 + [TensorDesc, ctypes.POINTER(PagedKV),
                                                 ctypes.POINTER(Params), P, P, TensorDesc, P, P, sz, P])
@@ -109,9 +112,10 @@ def _stream(t: torch.Tensor, stream=None) -> int:
 
 
 def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False, sink: int = 0,
-            window: int = 0, chunks: int = 1) -> Params:
+            window: int = 0, chunks: int = 1, top_r: int = 0, jitter: int = 0, seed: int = 0) -> Params:
     return Params(int(k), int(b_q), int(b_k), int(bool(causal)), float(sm_scale or 0.0),
-                  HIP_FLAG_EXACT_SCORES if exact else 0, int(sink), int(window), int(chunks))
+                  HIP_FLAG_EXACT_SCORES if exact else 0, int(sink), int(window), int(chunks), int(top_r),
+                  int(jitter), int(seed) & (2**64 - 1))
 
 
 def _require_cuda(*ts):
@@ -126,14 +130,16 @@ def num_blocks(k: int, b_k: int) -> int:
 
 
 def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
-                  causal: bool = True, exact: bool = False, chunks: int = 1, out=None, stream=None):
+                  causal: bool = True, exact: bool = False, chunks: int = 1, top_r: int = 0, jitter: int = 0,
+                  seed: int = 0, out=None, stream=None):
     """hip_mask_estimate on contiguous keys.  q [B,Hq,Tq,d], k [B,Hkv,Tk,d] -> (idx, cnt).  chunks = S:
-    stridden partial top-k."""
+    stridden partial top-k; top_r: top-r approximation; jitter / seed: one
+    ensemble sample (combine with mask_vote)."""
     _require_cuda(q, k)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
-    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks)
+    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq
@@ -145,6 +151,31 @@ def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q:
     with torch.cuda.device(q.device):
         _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, Tk, d, _desc(q), _desc(k), None,
                                      ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), None, 0, _stream(q, stream)))
+    return idx, cnt
+
+
+def mask_vote(idx_samples: torch.Tensor, cnt_samples: torch.Tensor, *, theta: int, tau: int, n_out=None,
+              stream=None):
+    """hip_mask_vote: idx_samples [n_e, ..., n] int32, cnt_samples [n_e, ...] -> (idx [..., n_out], cnt [...]).
+    n_out defaults to n (tau = 1) or n_e * n (tau = 0).  Feed the result to the attention with
+    k_budget = n_out * b_k."""
+    _require_cuda(idx_samples, cnt_samples)
+    if idx_samples.dtype != torch.int32 or cnt_samples.dtype != torch.int32:
+        raise TypeError("int32 indices / counts")
+    lib = load()
+    I, C = idx_samples.contiguous(), cnt_samples.contiguous()
+    n_e, n = I.shape[0], I.shape[-1]
+    lead = tuple(I.shape[1:-1])
+    units = 1
+    for x in lead:
+        units *= int(x)
+    if n_out is None:
+        n_out = n if tau else n_e * n
+    idx = torch.empty(lead + (int(n_out),), dtype=torch.int32, device=I.device)
+    cnt = torch.empty(lead, dtype=torch.int32, device=I.device)
+    with torch.cuda.device(I.device):
+        _check(lib.hip_mask_vote(n_e, units, n, I.data_ptr(), C.data_ptr(), int(theta), int(tau), int(n_out),
+                                 idx.data_ptr(), cnt.data_ptr(), _stream(I, stream)))
     return idx, cnt
 
 
@@ -162,14 +193,14 @@ def _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len: int) -> PagedKV
 
 
 def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, k_budget: int = 512, b_q: int = 32,
-                        b_k: int = 2, causal: bool = True, exact: bool = False, chunks: int = 1, out=None,
-                        stream=None):
+                        b_k: int = 2, causal: bool = True, exact: bool = False, chunks: int = 1, top_r: int = 0,
+                        jitter: int = 0, seed: int = 0, out=None, stream=None):
     """hip_mask_estimate on a paged cache (decode: q [B,Hq,Tq,d], Tq rows at positions seq_len-Tq+t)."""
     _require_cuda(q, k_pages, block_table, seq_lens)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
-    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks)
+    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq

@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     lib = H.load()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.hip_version() == 100
+    assert lib.hip_version() == 110
 
 
 def test_nm_dynamic_symbols():
@@ -160,3 +160,37 @@ def test_decoder_refresh_rule_host():
     import pytest
     with pytest.raises(ValueError):
         HipDecoder(r_m=0)
+
+
+def test_params_struct_layout_matches_header(tmp_path):
+    """The ctypes mirrors of hip_params_t / hip_paged_kv_t have the C compiler's size and offsets."""
+    import subprocess
+    src = tmp_path / "off.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "hip_attn.h"\nint main(void){'
+                   'printf("%zu %zu %zu %zu %zu\\n", sizeof(hip_params_t), offsetof(hip_params_t, chunks),'
+                   'offsetof(hip_params_t, top_r), offsetof(hip_params_t, sample_seed), sizeof(hip_paged_kv_t));}')
+    exe = tmp_path / "off"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert got == [ctypes.sizeof(H.Params), H.Params.chunks.offset, H.Params.top_r.offset,
+                   H.Params.sample_seed.offset, ctypes.sizeof(H.PagedKV)]
+
+
+def test_appendix_params_validation():
+    lib = H.load()
+    q = H.TensorDesc(0x1000, 64 * 128, 64 * 128, 128)
+    for bad in (dict(top_r=-1), dict(jitter=-2), dict(jitter=70000)):
+        p = H._params(512, 32, 2, True, **bad)
+        rc = lib.hip_mask_estimate(1, 1, 1, 1, 64, 64, 128, q, q, None, ctypes.byref(p), 0x3000, 0x4000, None, 0, None)
+        assert rc == H.HIP_ERROR_INVALID_VALUE, bad
+
+
+def test_vote_validation():
+    lib = H.load()
+    P = 0x1000
+    cases = [(0, 4, 8, 1, 1, 8), (17, 4, 8, 1, 1, 8), (2, 4, 8, 0, 1, 8), (2, 4, 8, 3, 1, 8), (2, 4, 8, 1, 2, 8),
+             (2, 4, 8, 1, 0, 8), (2, 4, 8, 1, 1, 7), (8, 4, 1024, 1, 1, 1024)]
+    for n_e, units, n_in, theta, tau, n_out in cases:
+        rc = lib.hip_mask_vote(n_e, units, n_in, P, P, theta, tau, n_out, P, P, None)
+        assert rc == H.HIP_ERROR_INVALID_VALUE, (n_e, n_in, theta, tau, n_out)
+    assert lib.hip_mask_vote(2, 4, 8, None, P, 1, 1, 8, P, P, None) == H.HIP_ERROR_INVALID_VALUE

@@ -465,3 +465,100 @@ def test_mask_chunked_decode_parity(orc, dt, dist):
         mode = orc.F32L if dt == torch.float32 else orc.F32C
         oi, oc = orc.mask(Q[b:b + 1], Kb, k, 1, bk, True, mode=mode, chunks=S)
         _assert_mask_equal(gi[b:b + 1], gc[b:b + 1], oi, oc)
+
+
+# ------------------------------------------------------------------------------------------------
+# f4: top-r approximation (G22), ensemble samples (G23) and vote
+# (G24).  Bit-exact tiers as for the plain mask: fp32 kernels issue the oracle's fmaf
+# order with the dropped components zeroed (exact zeros), tcgen05 on integer-valued inputs.
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("r", [16, 40])
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "llm"), (torch.bfloat16, "int")])
+def test_mask_topr_parity(orc, r, dt, dist):
+    Tq, Tk, k, bq, bk = 2500, 2600, 256, 32, 2
+    Q, K, _ = synth.gen_qkv(1, 2, 1, Tq, Tk, 128, dist, seed=80, dtype=dt, make_v=False)
+    idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, top_r=r)
+    torch.cuda.synchronize()
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, top_r=r)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    pi, _ = orc.mask(Q, K, k, bq, bk, True)
+    assert not np.array_equal(pi, oi)  # the approximation is active
+
+
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "iid"), (torch.bfloat16, "int")])
+def test_mask_topr_decode_parity(orc, dt, dist):
+    B, Hq, Hkv, d, k, bk, ps, r = 3, 4, 2, 128, 256, 2, 16, 24
+    seq = [5000, 100, 3333]
+    Q = synth.gen_decode_q(B, Hq, d, seed=81, dtype=dt, dist=dist)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=81, dtype=dt, dist=dist)
+    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), max(seq), k_budget=k, b_q=1, b_k=bk,
+                                     top_r=r)
+    torch.cuda.synchronize()
+    mode = orc.F32L if dt == torch.float32 else orc.F32C
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=mode, top_r=r)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+
+
+@pytest.mark.parametrize("R,seed,S", [(3, 1, 1), (5, 2, 1), (4, 3, 2)])
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "llm"), (torch.bfloat16, "int")])
+def test_mask_jitter_parity(orc, R, seed, S, dt, dist):
+    Tq, Tk, k, bq, bk = 3000, 3000, 128, 32, 2
+    Q, K, _ = synth.gen_qkv(1, 3, 1, Tq, Tk, 128, dist, seed=82, dtype=dt, make_v=False)
+    idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, jitter=R, seed=seed, chunks=S)
+    torch.cuda.synchronize()
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, jitter=R, seed=seed, chunks=S)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+
+
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "iid"), (torch.bfloat16, "int")])
+def test_mask_jitter_decode_parity(orc, dt, dist):
+    B, Hq, Hkv, d, k, bk, ps = 3, 4, 2, 128, 128, 2, 64
+    seq = [6000, 90, 3333]
+    Q = synth.gen_decode_q(B, Hq, d, seed=83, dtype=dt, dist=dist)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=83, dtype=dt, dist=dist)
+    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), max(seq), k_budget=k, b_q=1, b_k=bk,
+                                     jitter=5, seed=11, top_r=32)
+    torch.cuda.synchronize()
+    mode = orc.F32L if dt == torch.float32 else orc.F32C
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=mode, jitter=5, seed=11, top_r=32)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+
+
+@pytest.mark.parametrize("n_e,theta,tau", [(1, 1, 1), (3, 1, 0), (3, 2, 1), (4, 2, 0), (4, 4, 1), (8, 3, 1)])
+def test_vote_parity_synthetic(orc, n_e, theta, tau):
+    """GPU vote vs oracle vote on seeded synthetic sample masks (bit-exact)."""
+    B, Hq, nqb, n = 1, 3, 40, 64
+    hi = torch.randint(1, 300, (B, Hq, nqb), generator=torch.Generator().manual_seed(n_e))
+    samples = [synth.gen_block_indices(B, Hq, nqb, n, hi, seed=100 + e) for e in range(n_e)]
+    I = torch.stack([s[0] for s in samples])
+    C = torch.stack([s[1] for s in samples])
+    gi, gc = H.mask_vote(I.cuda(), C.cuda(), theta=theta, tau=tau)
+    torch.cuda.synchronize()
+    oi, oc = orc.vote(I, C, theta, tau)
+    assert np.array_equal(gc.cpu().numpy(), oc)
+    assert np.array_equal(gi.cpu().numpy(), oi)
+
+
+def test_ensemble_end_to_end(orc):
+    """n_e jittered samples -> vote -> sparse attention, on integer bf16 inputs: the GPU samples and
+    vote equal the oracle's bit-for-bit, and the attention on that selection (tau = 0: up to
+    n_e * k tokens per row) matches the fp64 oracle within the bf16 bar."""
+    Tq = Tk = 2048
+    k, bq, bk, n_e, R = 128, 32, 2, 3, 5
+    Q, K, V = synth.gen_qkv(1, 2, 1, Tq, Tk, 128, "int", seed=84, dtype=torch.bfloat16)
+    Qd, Kd, Vd = Q.cuda(), K.cuda(), V.cuda()
+    gs = [H.mask_estimate(Qd, Kd, k_budget=k, b_q=bq, b_k=bk, jitter=R, seed=s) for s in range(n_e)]
+    os_ = [orc.mask(Q, K, k, bq, bk, True, jitter=R, seed=s) for s in range(n_e)]
+    for (gi, gc), (oi, oc) in zip(gs, os_):
+        torch.cuda.synchronize()
+        _assert_mask_equal(gi.cpu().numpy(), gc.cpu().numpy(), oi, oc)
+    for theta, tau in ((1, 0), (2, 1)):
+        vi, vc = H.mask_vote(torch.stack([g[0] for g in gs]), torch.stack([g[1] for g in gs]), theta=theta, tau=tau)
+        oi, oc = orc.vote(np.stack([o[0] for o in os_]), np.stack([o[1] for o in os_]), theta, tau)
+        torch.cuda.synchronize()
+        assert np.array_equal(vi.cpu().numpy(), oi) and np.array_equal(vc.cpu().numpy(), oc)
+        kk = oi.shape[-1] * bk
+        o = H.sparse_attention_prefill(Qd, Kd, Vd, vi, vc, k_budget=kk, b_q=bq, b_k=bk)
+        Oo, _ = orc.sparse_attention(Q, K, V, kk, bq, bk, True, oi, oc)
+        torch.cuda.synchronize()
+        assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
