@@ -32,18 +32,24 @@ constexpr float kATLog2e = 1.4426950408889634f;
 constexpr float kATLn2 = 0.6931471805599453f;
 constexpr float kATRescale = 8.f;                     // lazy rescale threshold (log2 units)
 
-struct AttnTCSmem {
+template <int kTokN>
+struct AttnTCSmemT {
   static constexpr uint32_t q = 0;
   static constexpr uint32_t ring = kATQTile;                      // 2 slots
   static constexpr uint32_t p = ring + 2 * kATSlot;               // one P chunk
   static constexpr uint32_t red = p + kATPChunk;                  // floats, see below
   static constexpr int kRedFloats = 3 * 4 * 32 + 6 * 32 + 32;     // [3][4][32] + m, l, lu, corr, invl, pad + flag
-  static constexpr int kTok = 768;                                // selected (<= 512) + extra (<= 256) keys
+  static constexpr int kTok = kTokN;                              // selected + extra (<= 256) key slots
   static constexpr uint32_t tok = red + kRedFloats * 4;           // [kTok] row of each key slot
   static constexpr uint32_t xlist = tok + kTok * 4;               // [kMaxExtra] sink / window tokens
   static constexpr uint32_t misc = (uint32_t)align_up(xlist + kMaxExtra * 4, 64);
   static constexpr uint32_t total = misc + 64;
 };
+// Default: <= 512 selected keys (k = 512) + <= 256 extra, 4 CTAs per SM.  Wide: the ensemble's
+// union masks (hip_mask_vote with tau = 0, up to 16 x 256 blocks) — a longer staged key list, at
+// the cost of shared memory (fewer CTAs per SM); the rest of the kernel is unchanged.
+constexpr int kATTokDefault = 768, kATTokWide = 4096 + 256;
+using AttnTCSmem = AttnTCSmemT<kATTokDefault>;
 
 // Lane L ends with op-reduction over the 32 lanes of query L (values v[0..31] per lane = queries).
 template <bool kMax>
@@ -63,7 +69,7 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 }
 
 // kSW: sink / sliding-window tokens enabled (a separate instantiation, so the plain path pays nothing).
-template <bool kPaged, bool kSW>
+template <bool kPaged, bool kSW, int TOK>
 __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
                                                                 const int32_t* __restrict__ idx,
                                                                 const int32_t* __restrict__ cnt, float scale_log2,
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sb = raw + pad;
-  using L = AttnTCSmem;
+  using L = AttnTCSmemT<TOK>;
   float* red = reinterpret_cast<float*>(base + L::red);   // [0,384): per-warp max / sum / unrounded sum
   float* mrun = red + 384;                                 // running max per query (log2 units)
   float* lrun = red + 416;                                 // running sum of bf16-rounded p
@@ -415,19 +421,20 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
 }
 
 // Any query block of <= 32 rows (decode included: the N = 32 operand is zero-padded, the tensor
-// cores are idle anyway); <= 512 selected keys plus <= 256 sink / window tokens (the staged list).
+// cores are idle anyway); up to 4096 selected keys plus <= 256 sink / window tokens (the staged list).
 bool attn_tc_supported(const Shape& sh) {
   return sh.d == 128 && sh.bq >= 1 && sh.bq <= 32 && (128 % sh.bk) == 0 && (sh.bk & (sh.bk - 1)) == 0 &&
-         (int64_t)sh.n * sh.bk <= 512 && sh.sink + sh.window + sh.bq - 1 <= kMaxExtra;
+         (int64_t)sh.n * sh.bk <= 4096 && sh.sink + sh.window + sh.bq - 1 <= kMaxExtra;
 }
 
-cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
-                           const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
-                           float* lse, cudaStream_t stream, int num_sms) {
-  const size_t smem = AttnTCSmem::total + 1024;
+template <int TOK>
+static cudaError_t launch_attn_tc_t(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs,
+                                    const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb,
+                                    int64_t osh, int64_t ost, float* lse, cudaStream_t stream, int num_sms) {
+  const size_t smem = AttnTCSmemT<TOK>::total + 1024;
   const bool sw = sh.sink > 0 || sh.window > 0;
-  auto kern = ks.paged ? (sw ? attn_tc_kernel<true, true> : attn_tc_kernel<true, false>)
-                       : (sw ? attn_tc_kernel<false, true> : attn_tc_kernel<false, false>);
+  auto kern = ks.paged ? (sw ? attn_tc_kernel<true, true, TOK> : attn_tc_kernel<true, false, TOK>)
+                       : (sw ? attn_tc_kernel<false, true, TOK> : attn_tc_kernel<false, false, TOK>);
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kATThreads, smem, 64, &per_sm);
   if (e != cudaSuccess) return e;
@@ -436,6 +443,14 @@ cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, co
   kern<<<(unsigned)grid, kATThreads, smem, stream>>>(sh, qs, ks, vs, idx, cnt, sm_scale * kATLog2e, o, osb, osh, ost,
                                                      lse);
   return cudaGetLastError();
+}
+
+cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
+                           const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
+                           float* lse, cudaStream_t stream, int num_sms) {
+  if ((int64_t)sh.n * sh.bk + kMaxExtra <= kATTokDefault)
+    return launch_attn_tc_t<kATTokDefault>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
+  return launch_attn_tc_t<kATTokWide>(sh, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, num_sms);
 }
 
 }  // namespace hip

@@ -281,7 +281,9 @@ struct TCScorer {
 };
 
 // TEAMS units per CTA (NT = 128 threads each); TEAMS = 2 shares the ring (see the header).
-template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB>
+// kExt: the appendix options (top-r, ensemble split jitter) — a separate instantiation, so the plain
+// Alg. 1 kernel carries none of their code or registers.
+template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, bool kExt>
 __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     const uint32_t q_s = sbase + L::q + team * kQTileBytes;
     uint32_t ckeep = 3u;  // bit h: this thread's 16-byte key chunk of d-half h holds a kept component
-    if (Bq > sh.n && sh.top_r > 0 && sh.top_r < 128) {
+    if (kExt && Bq > sh.n && sh.top_r > 0 && sh.top_r < 128) {
       // top-r approximation (G22; topr.cuh): a_c = max_t |q_tc| (thread c), keep bits by
       // rank -> st.warp_tot[c / 32]; the query tile is stored with the dropped components zeroed
       float* a = reinterpret_cast<float*>(st.rep);
@@ -354,8 +356,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       const unsigned kb = __ballot_sync(0xffffffffu, top_r_keep(a, 128, Sync::tid(), sh.top_r));
       if ((threadIdx.x & 31) == 0) st.warp_tot[Sync::tid() >> 5] = (int)kb;
       Sync::sync();
-      const uint32_t kw[4] = {(uint32_t)st.warp_tot[0], (uint32_t)st.warp_tot[1], (uint32_t)st.warp_tot[2],
-                              (uint32_t)st.warp_tot[3]};
+      const uint32_t* kw = reinterpret_cast<const uint32_t*>(st.warp_tot);  // 4 keep words (shared)
       for (int p = Sync::tid(); p < 32 * 16; p += NT) {
         const int r = p >> 4, c16 = p & 15;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     ptimer.mark(7);  // unit setup / Q load / exact units
 #endif
     tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
-                                                 make_jitter(sh.jitter, sh.seed, lin));
+                                                 kExt ? make_jitter(sh.jitter, sh.seed, lin) : SplitJitter());
     if (cs == 0 && Sync::tid() == 0) cnt[lin] = min(Bq, sh.n);
     Sync::sync();
   }
@@ -423,11 +424,12 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int SLOTS, int TT, int TEAMS, int MINB>
+template <int SLOTS, int TT, int TEAMS, int MINB, bool kExt = false>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
   const size_t smem = MaskTCSmemLayout<SLOTS, TEAMS>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB> : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB>;
+  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, kExt>
+                       : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, kExt>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
   if (e != cudaSuccess) return e;
@@ -441,6 +443,7 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
   // HIPATTN_MASK_TC selects a variant (tuning aid, profiles/r01).
+  if (sh.top_r > 0 || sh.jitter > 0) return launch_v<2, 4, 1, 4, true>(sh, qs, ks, idx, cnt, stream, num_sms);
   const char* v = getenv("HIPATTN_MASK_TC");
   if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);

@@ -3,6 +3,7 @@ bench.py reports as roofline.traffic (dram__bytes_read.sum + dram__bytes_write.s
 
 usage: python profiles/ncu_to_json.py <config> <kernel_key>=<report.ncu-rep> [...]
 e.g.   python profiles/ncu_to_json.py c2 mask_estimate=gpurun_out/mask_full.ncu-rep
+       python profiles/ncu_to_json.py c4 mask_estimate=rep.ncu-rep#0 sparse_attention_prefill=rep.ncu-rep#1
 """
 import csv
 import json
@@ -43,7 +44,11 @@ def main():
     j = json.load(open(path)) if os.path.exists(path) else {}
     for arg in sys.argv[2:]:
         key, rep = arg.split("=", 1)
-        m = launch_metrics(rep)[0]
+        i = 0
+        if "#" in rep:  # report#i: the i-th launch of a multi-kernel report
+            rep, i = rep.rsplit("#", 1)
+            i = int(i)
+        m = launch_metrics(rep)[i]
         m["report"] = os.path.basename(rep)
         j.setdefault(cfg, {})[key] = m
         print(cfg, key, m)

@@ -298,25 +298,30 @@ def test_hip_layer_end_to_end(orc, dt, dist):
 # Full-size configuration (BASELINE C2 shape, sampled): the launch bench.py times
 # ------------------------------------------------------------------------------------------------
 @pytest.mark.slow
-def test_full_size_c2_sampled(orc):
-    B, Hq, Hkv, T, d, k, bq, bk = 1, 32, 32, 32768, 128, 512, 32, 2
-    Q, K, V = synth.gen_qkv(B, Hq, Hkv, T, T, d, "llm", seed=0, dtype=torch.bfloat16, device="cuda")
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
+def test_full_size_sampled(orc, cfg):
+    """The launches bench.py times (C2 32 heads x 32k, C4 40 x 128k, C5 32 x 1M; bf16, llm inputs),
+    checked on sampled query blocks — the regime boundaries q in {0, 15, 16, 31, 32, N_qb - 1} plus
+    random ones — against the oracle run on the sub-problem (the block's Q rows, the K/V prefix:
+    bottom-right alignment makes it exact)."""
+    Hq, T, n_heads, per_head = {"c2": (32, 32768, 48, 7), "c4": (40, 131072, 8, 7), "c5": (32, 1048576, 3, 7)}[cfg]
+    B, d, k, bq, bk = 1, 128, 512, 32, 2
+    Q, K, V = synth.gen_qkv(B, Hq, Hq, T, T, d, "llm", seed=0, dtype=torch.bfloat16, device="cuda")
     idx, cnt = H.mask_estimate(Q, K, k_budget=k, b_q=bq, b_k=bk)
     o = H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=k, b_q=bq, b_k=bk)
     torch.cuda.synchronize()
     nqb = T // bq
     rng = np.random.default_rng(0)
-    units = [(h, q) for h in rng.integers(0, Hq, 48) for q in
-             [0, 15, 16, 31, 32, nqb - 1, int(rng.integers(33, nqb - 1))]]
+    units = [(int(h), q) for h in rng.integers(0, Hq, n_heads) for q in
+             [0, 15, 16, 31, 32, nqb - 1, int(rng.integers(33, nqb - 1))][:per_head]]
     n_bad = n_unexpl = 0
-    gi_all, gc_all = idx.cpu().numpy(), cnt.cpu().numpy()
     for h, q in units:
         t1 = (q + 1) * bq
         Qs = Q[:, h:h + 1, q * bq:t1].cpu()
         Ks, Vs = K[:, h:h + 1, :t1].cpu(), V[:, h:h + 1, :t1].cpu()
         oi, oc, dg = orc.mask(Qs, Ks, k, bq, bk, True, mode=orc.F64, diag=True)
-        gi = gi_all[0, h, q]
-        assert gc_all[0, h, q] == oc[0, 0, 0]
+        gi = idx[0, h, q].cpu().numpy()
+        assert int(cnt[0, h, q]) == oc[0, 0, 0]
         if not np.array_equal(gi, oi[0, 0, 0]):
             n_bad += 1
             eps = TAU_UNIT * d * dg["emax"][0, 0, 0]
@@ -324,8 +329,10 @@ def test_full_size_c2_sampled(orc):
             continue
         Oo, _ = orc.sparse_attention(Qs, Ks, Vs, k, bq, bk, True, oi, oc)
         assert np.abs(o[0, h, q * bq:t1].float().cpu().numpy() - Oo[0, 0]).max() <= 2e-2
-    print(f"\n[parity] C2 sampled: {n_bad}/{len(units)} query blocks differ, unexplained {n_unexpl}")
+    print(f"\n[parity] {cfg} sampled: {n_bad}/{len(units)} query blocks differ, unexplained {n_unexpl}")
     assert n_unexpl == 0
+    del Q, K, V, o, idx, cnt
+    torch.cuda.empty_cache()
 
 
 # ------------------------------------------------------------------------------------------------
@@ -562,3 +569,24 @@ def test_ensemble_end_to_end(orc):
         Oo, _ = orc.sparse_attention(Q, K, V, kk, bq, bk, True, oi, oc)
         torch.cuda.synchronize()
         assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
+
+
+@pytest.mark.parametrize("paged", [False, True])
+def test_attention_wide_selection_parity(orc, paged):
+    """Selections longer than k = 512 keys (the ensemble's tau = 0 union: up to n_e * n blocks) run on
+    the wide tcgen05 instantiation; seeded synthetic selections of up to 1024 blocks = 2048 keys."""
+    Tq, Tk, bq, bk, n = 700, 4000, 32, 2, 1024
+    Q, K, V = synth.gen_qkv(1, 2, 1, Tq, Tk, 128, "iid", seed=85, dtype=torch.bfloat16)
+    idx, cnt = _synthetic_selection(1, 2, Tq, Tk, n * bk, bq, bk, True, seed=85)
+    if not paged:
+        o = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx.cuda(), cnt.cuda(), k_budget=n * bk, b_q=bq,
+                                       b_k=bk, sink=32, window=128)
+        Oo, _ = orc.sparse_attention(Q, K, V, n * bk, bq, bk, True, idx, cnt, sink=32, window=128)
+    else:
+        kp, vp, bt, sl = synth.to_paged(K, V, [Tk], 64, seed=85)
+        o = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), Tk, idx.cuda(), cnt.cuda(),
+                                      k_budget=n * bk, b_q=bq, b_k=bk)
+        Oo, _ = orc.sparse_attention_paged(Q, kp, vp, bt, sl, n * bk, bq, bk, True, idx, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.max()) > 256
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
