@@ -26,6 +26,8 @@
  *   - oracle_mask_ext         + the appendix extensions: top-r approximation (readings
  *                             G22) and the ensemble's jittered splits (G23), with the
  *                             stridden partial top-k (G21).
+ *                             gqa_shared: one mask per GQA group scored over all its query
+ *                             heads' rows (reading G25).
  *   - oracle_vote             the ensemble vote (G24).
  *   - *_paged                 the same on a paged KV cache (decode): token s of
  *                             sequence b lives at page block_table[b][s / page_size], slot
@@ -77,6 +79,8 @@ typedef struct {
     int ncomp;
     int R;           /* split jitter magnitude (0 = the deterministic half-up split) */
     uint64_t key;    /* per-unit generator key (orc_unit_key) */
+    int G;           /* query heads scored together (GQA-shared mask, G25); 1 = one head */
+    int64_t hstride; /* floats between the Q rows of consecutive heads of the group */
 } orc_ext;
 
 /* splitmix64 output function (Steele, Lea & Flood 2014): the counter-based generator of the
@@ -104,16 +108,18 @@ static int64_t orc_jitter(uint64_t key, int it, int64_t f, int R)
 
 /* argtop_r(|q|) of a query block (reading G22): a_c = max over the rows of |q_c|, the r
  * largest a_c with ties toward the smaller c, returned in ascending order.  r >= d: all. */
-static void top_r_components(const float *Qh, int64_t t0, int64_t t1, int d, int r, int *out)
+static void top_r_components(const float *Qh, int64_t t0, int64_t t1, int G, int64_t hstride, int d, int r,
+                             int *out)
 {
     double *a = (double *)malloc(sizeof(double) * (size_t)d);
     char *taken = (char *)calloc((size_t)d, 1);
     for (int c = 0; c < d; ++c) {
         a[c] = 0.0;
-        for (int64_t t = t0; t < t1; ++t) {
-            double v = fabs((double)Qh[t * d + c]);
-            if (v > a[c]) a[c] = v;
-        }
+        for (int g = 0; g < G; ++g)
+            for (int64_t t = t0; t < t1; ++t) {
+                double v = fabs((double)Qh[g * hstride + t * d + c]);
+                if (v > a[c]) a[c] = v;
+            }
     }
     /* r rounds of "take the largest remaining, smallest index on ties" */
     for (int i = 0; i < r; ++i) {
@@ -156,23 +162,27 @@ static int64_t visible_blocks(int64_t q, int bq, int bk, int Tq, int Tk, int cau
  * scale (G11).  `emax` (optional) receives max over the pairs of sum_c |q_c k_c|, used
  * to bound the rounding error of any fp32 evaluation order. */
 static double block_score_c(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
-                            int Tq, int Tk, int d, int causal, int mode, const int *comp, int ncomp, double *emax);
+                            int Tq, int Tk, int d, int causal, int mode, const int *comp, int ncomp, int G,
+                            int64_t hstride, double *emax);
 static double block_score(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
                           int Tq, int Tk, int d, int causal, int mode, double *emax)
 {
-    return block_score_c(Qh, Kh, t0, t1, j, bk, Tq, Tk, d, causal, mode, NULL, d, emax);
+    return block_score_c(Qh, Kh, t0, t1, j, bk, Tq, Tk, d, causal, mode, NULL, d, 1, 0, emax);
 }
 
 /* The same over the component list comp[0..ncomp) (top-r: sum_{l=1..r} q_{p_l} k_{p_l}, in
- * ascending component order; comp = NULL: c = 0..d-1). */
+ * ascending component order; comp = NULL: c = 0..d-1), and over the query rows of G heads
+ * (GQA-shared mask, reading G25: head g's rows start at Qh + g * hstride; G = 1: one head). */
 static double block_score_c(const float *Qh, const float *Kh, int64_t t0, int64_t t1, int64_t j, int bk,
-                            int Tq, int Tk, int d, int causal, int mode, const int *comp, int ncomp, double *emax)
+                            int Tq, int Tk, int d, int causal, int mode, const int *comp, int ncomp, int G,
+                            int64_t hstride, double *emax)
 {
     int64_t delta = (int64_t)Tk - Tq;
     int64_t s0 = j * bk, s1 = imin64((j + 1) * (int64_t)bk, Tk);
     double best = -INFINITY, e_best = 0.0;
-    for (int64_t t = t0; t < t1; ++t) {
-        const float *q = Qh + t * d;
+    for (int64_t gt = 0; gt < (int64_t)G * (t1 - t0); ++gt) {
+        int64_t t = t0 + gt % (t1 - t0); /* row t of head gt / (t1 - t0) of the group */
+        const float *q = Qh + (gt / (t1 - t0)) * hstride + t * d;
         for (int64_t s = s0; s < s1; ++s) {
             if (causal && s > t + delta) continue;
             const float *kk = Kh + s * d;
@@ -318,7 +328,8 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
             int64_t r = cand[c].f; /* representative = first block of the branch */
             if (isnan(memo[r])) {
                 double e = 0.0;
-                memo[r] = block_score_c(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, ex->comp, ex->ncomp, &e);
+                memo[r] = block_score_c(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, ex->comp, ex->ncomp, ex->G,
+                                        ex->hstride, &e);
                 if (e > dg->emax) dg->emax = e;
                 dg->n_scored++;
             }
@@ -356,7 +367,7 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
 static int mask_unit_chunked(const float *Qh, const float *Kh, int Tq, int Tk, int d, int64_t q, int n, int bq,
                              int bk, int causal, int mode, int chunks, int32_t *out_idx, int32_t *out_cnt,
                              orc_diag *diag, int32_t *trace_nodes, double *trace_scores, int max_trace,
-                             int top_r, int R, uint64_t seed, int64_t lin)
+                             int top_r, int R, uint64_t seed, int64_t lin, int G)
 {
     int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
     int64_t t0 = q * (int64_t)bq, t1 = imin64(t0 + bq, Tq);
@@ -374,10 +385,10 @@ static int mask_unit_chunked(const float *Qh, const float *Kh, int Tq, int Tk, i
     double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
     if (!memo) return ORC_ENOMEM;
     int comp[1024];
-    orc_ext ex = {NULL, d, R > 0 ? R : 0, 0};
+    orc_ext ex = {NULL, d, R > 0 ? R : 0, 0, G, (int64_t)Tq * d};
     if (top_r > 0 && top_r < d) { /* top-r approximation */
         if (d > 1024) { free(memo); return ORC_EINVAL; }
-        top_r_components(Qh, t0, t1, d, top_r, comp);
+        top_r_components(Qh, t0, t1, G, (int64_t)Tq * d, d, top_r, comp);
         ex.comp = comp;
         ex.ncomp = top_r;
     }
@@ -401,7 +412,7 @@ static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, in
                      int32_t *trace_nodes, double *trace_scores, int max_trace)
 {
     return mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, 1, out_idx, out_cnt, diag,
-                             trace_nodes, trace_scores, max_trace, 0, 0, 0, 0);
+                             trace_nodes, trace_scores, max_trace, 0, 0, 0, 0, 1);
 }
 
 /* -------------------------------------------------------------------------------------------- */
@@ -441,9 +452,11 @@ int oracle_mask(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, 
 }
 
 /* oracle_mask with stridden partial top-k over S = chunks contiguous chunks (G21). */
+/* gqa_shared = 1 (reading G25): one mask per (b, kv head, query block), scored over the query rows
+ * of all H_q / H_kv heads of the group; idx [B, Hkv, Nqb, n], cnt [B, Hkv, Nqb]. */
 int oracle_mask_ext(const float *Q, const float *K, int B, int Hq, int Hkv, int Tq, int Tk, int d, int k,
                     int bq, int bk, int causal, int mode, int chunks, int top_r, int jitter, uint64_t seed,
-                    int32_t *idx, int32_t *cnt, double *margin_min, double *emax)
+                    int gqa_shared, int32_t *idx, int32_t *cnt, double *margin_min, double *emax)
 {
     if (top_r < 0 || jitter < 0) return ORC_EINVAL;
     int rc = check_dims(B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal);
@@ -451,17 +464,18 @@ int oracle_mask_ext(const float *Q, const float *K, int B, int Hq, int Hkv, int 
     int n = k / bk;
     if (chunks < 1 || n % chunks) return ORC_EINVAL;
     int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
-    int64_t units = (int64_t)B * Hq * nqb;
+    int G = gqa_shared ? Hq / Hkv : 1, Hm = gqa_shared ? Hkv : Hq; /* heads scored together, mask heads */
+    int64_t units = (int64_t)B * Hm * nqb;
     int err = ORC_OK;
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t u = 0; u < units; ++u) {
         int64_t q = u % nqb, bh = u / nqb;
-        int64_t b = bh / Hq, h = bh % Hq, hk = h / (Hq / Hkv);
-        const float *Qh = Q + ((b * Hq + h) * (int64_t)Tq) * d;
+        int64_t b = bh / Hm, h = bh % Hm, hk = gqa_shared ? h : h / (Hq / Hkv);
+        const float *Qh = Q + ((b * Hq + h * G) * (int64_t)Tq) * d; /* first query head of the group */
         const float *Kh = K + ((b * Hkv + hk) * (int64_t)Tk) * d;
         orc_diag dg;
         int r = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, chunks, idx + u * n, cnt + u,
-                                  &dg, NULL, NULL, 0, top_r, jitter, seed, u);
+                                  &dg, NULL, NULL, 0, top_r, jitter, seed, u, G);
         if (r) {
 #pragma omp critical
             err = r;
@@ -476,7 +490,7 @@ int oracle_mask_chunked(const float *Q, const float *K, int B, int Hq, int Hkv, 
                         int bq, int bk, int causal, int mode, int chunks, int32_t *idx, int32_t *cnt,
                         double *margin_min, double *emax)
 {
-    return oracle_mask_ext(Q, K, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal, mode, chunks, 0, 0, 0, idx, cnt,
+    return oracle_mask_ext(Q, K, B, Hq, Hkv, Tq, Tk, d, k, bq, bk, causal, mode, chunks, 0, 0, 0, 0, idx, cnt,
                            margin_min, emax);
 }
 
@@ -497,7 +511,7 @@ int oracle_mask_trace_ext(const float *Q, const float *K, int B, int Hq, int Hkv
     orc_diag dg;
     rc = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, k / bk, bq, bk, causal, mode, 1, idx_out, cnt_out, &dg,
                            trace_nodes, trace_scores, max_trace, top_r, jitter, seed,
-                           ((int64_t)b * Hq + h) * nqb + q);
+                           ((int64_t)b * Hq + h) * nqb + q, 1);
     if (n_iter) *n_iter = dg.n_iter;
     if (n_scored) *n_scored = dg.n_scored;
     return rc;
@@ -518,7 +532,7 @@ int oracle_top_r_components(const float *Qb, int nrows, int d, int r, int32_t *o
     if (nrows < 1 || d < 1 || r < 1 || r > d) return ORC_EINVAL;
     int *tmp = (int *)malloc(sizeof(int) * (size_t)d);
     if (!tmp) return ORC_ENOMEM;
-    top_r_components(Qb, 0, nrows, d, r, tmp);
+    top_r_components(Qb, 0, nrows, 1, 0, d, r, tmp);
     for (int i = 0; i < r; ++i) out[i] = tmp[i];
     free(tmp);
     return ORC_OK;
@@ -832,7 +846,7 @@ int oracle_mask_paged_ext(const float *Q, const float *Kpages, int num_pages, in
                       const int32_t *block_table, int max_pages, const int32_t *seq_lens, int B, int Hq,
                       int Hkv, int Tq, int d, int k, int bq, int bk, int causal, int mode, int32_t *idx,
                       int32_t *cnt, double *margin_min, double *emax, int64_t *n_scored, int32_t *n_iter,
-                          int chunks, int top_r, int jitter, uint64_t seed)
+                          int chunks, int top_r, int jitter, uint64_t seed, int gqa_shared)
 {
     if (top_r < 0 || jitter < 0 || chunks < 1 || bk < 1 || (k / bk) % chunks) return ORC_EINVAL;
     if (page_size < 1 || page_size % bk != 0 || num_pages < 1) return ORC_EINVAL;
@@ -848,14 +862,16 @@ int oracle_mask_paged_ext(const float *Q, const float *Kpages, int num_pages, in
                                      &err);
             if (!Kh) break;
             int g = Hq / Hkv;
+            int gm = gqa_shared ? 1 : g; /* masks of this kv head: one shared (G25) or one per q head */
 #pragma omp parallel for schedule(dynamic, 1)
-            for (int64_t w = 0; w < (int64_t)g * nqb; ++w) {
-                int64_t h = (int64_t)hk * g + w / nqb, q = w % nqb;
-                int64_t u = ((int64_t)b * Hq + h) * nqb + q;
-                const float *Qh = Q + (((int64_t)b * Hq + h) * (int64_t)Tq) * d;
+            for (int64_t w = 0; w < (int64_t)gm * nqb; ++w) {
+                int64_t h = (int64_t)hk * gm + w / nqb, q = w % nqb; /* mask head */
+                int64_t u = ((int64_t)b * (gqa_shared ? Hkv : Hq) + h) * nqb + q;
+                const float *Qh = Q + (((int64_t)b * Hq + (gqa_shared ? h * g : h)) * (int64_t)Tq) * d;
                 orc_diag dg;
                 int r = mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, chunks, idx + u * n,
-                                          cnt + u, &dg, NULL, NULL, 0, top_r, jitter, seed, u);
+                                          cnt + u, &dg, NULL, NULL, 0, top_r, jitter, seed, u,
+                                          gqa_shared ? g : 1);
                 if (r) {
 #pragma omp critical
                     err = r;
@@ -878,7 +894,7 @@ int oracle_mask_paged(const float *Q, const float *Kpages, int num_pages, int pa
 {
     return oracle_mask_paged_ext(Q, Kpages, num_pages, page_size, block_table, max_pages, seq_lens, B, Hq, Hkv, Tq,
                                  d, k, bq, bk, causal, mode, idx, cnt, margin_min, emax, n_scored, n_iter, 1, 0, 0,
-                                 0);
+                                 0, 0);
 }
 
 int oracle_sparse_attention_paged_sw(const float *Q, const float *Kpages, const float *Vpages, int num_pages,

@@ -64,11 +64,11 @@ def lib():
         _lib.oracle_sparse_attention_paged_sw.argtypes = ([P, P, P, i32, i32, P, i32, P] + [i32] * 9
                                                           + [f64, P, P, i32, i32, P, P])
         u64 = ctypes.c_uint64
-        _lib.oracle_mask_ext.argtypes = [P, P] + [i32] * 14 + [u64] + [P] * 4
+        _lib.oracle_mask_ext.argtypes = [P, P] + [i32] * 14 + [u64, i32] + [P] * 4
         _lib.oracle_mask_trace_ext.argtypes = ([P, P] + [i32] * 11 + [i32] * 3 + [P, P, P, P, i32, P, P]
                                                + [i32, i32, u64])
         _lib.oracle_mask_paged_ext.argtypes = ([P, P, i32, i32, P, i32, P] + [i32] * 10 + [P] * 6
-                                               + [i32, i32, i32, u64])
+                                               + [i32, i32, i32, u64, i32])
         _lib.oracle_top_r_components.argtypes = [P, i32, i32, i32, P]
         _lib.oracle_splitmix64.argtypes = [u64]
         _lib.oracle_splitmix64.restype = u64
@@ -122,27 +122,30 @@ def n_blocks(k: int, bk: int) -> int:
 
 
 def mask(Q, K, k: int, bq: int, bk: int, causal: bool, mode: int = F32C, diag: bool = False, chunks: int = 1,
-         top_r: int = 0, jitter: int = 0, seed: int = 0):
+         top_r: int = 0, jitter: int = 0, seed: int = 0, gqa_shared: bool = False):
     """Alg. 1 mask. Q [B,Hq,Tq,d], K [B,Hkv,Tk,d] -> idx [B,Hq,Nqb,n] (asc, -1 pad), cnt [B,Hq,Nqb].
 
     diag=True also returns dict(margin_min, emax, n_scored, n_iter) per unit.  chunks = S > 1: the
     stridden partial top-k (reading G21; diag then carries margin_min and emax only).
     top_r = r in (0, d): top-r approximation (G22).  jitter = R > 0: an ensemble sample
-    with split offsets in [-R, R] from generator seed `seed` (G23)."""
+    with split offsets in [-R, R] from generator seed `seed` (G23).  gqa_shared: one mask
+    per GQA group over all its query heads' rows (G25) -> idx [B, Hkv, Nqb, n]."""
     Q, K = _f32(Q), _f32(K)
     B, Hq, Tq, d = Q.shape
     _, Hkv, Tk, _ = K.shape
     n = k // bk if bk > 0 else 0
     nqb = -(-Tq // bq) if bq > 0 else 0
-    idx = np.empty((B, Hq, nqb, max(n, 1)), np.int32)
-    cnt = np.empty((B, Hq, nqb), np.int32)
-    mg = np.empty((B, Hq, nqb), np.float64)
-    em = np.empty((B, Hq, nqb), np.float64)
-    ns = np.empty((B, Hq, nqb), np.int64)
-    ni = np.empty((B, Hq, nqb), np.int32)
-    if chunks != 1 or top_r or jitter:
+    Hm = Hkv if gqa_shared else Hq
+    idx = np.empty((B, Hm, nqb, max(n, 1)), np.int32)
+    cnt = np.empty((B, Hm, nqb), np.int32)
+    mg = np.empty((B, Hm, nqb), np.float64)
+    em = np.empty((B, Hm, nqb), np.float64)
+    ns = np.empty((B, Hm, nqb), np.int64)
+    ni = np.empty((B, Hm, nqb), np.int32)
+    if chunks != 1 or top_r or jitter or gqa_shared:
         rc = lib().oracle_mask_ext(_p(Q), _p(K), B, Hq, Hkv, Tq, Tk, d, k, bq, bk, int(causal), mode, int(chunks),
-                                   int(top_r), int(jitter), int(seed) & (2**64 - 1), _p(idx), _p(cnt), _p(mg), _p(em))
+                                   int(top_r), int(jitter), int(seed) & (2**64 - 1), int(bool(gqa_shared)), _p(idx),
+                                   _p(cnt), _p(mg), _p(em))
         _check(rc, "oracle_mask_ext")
         if diag:
             return idx, cnt, dict(margin_min=mg, emax=em)
@@ -239,7 +242,8 @@ def dense_attention(Q, K, V, causal: bool, sm_scale: float = 0.0):
 
 
 def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causal: bool, mode: int = F32C,
-               diag: bool = False, chunks: int = 1, top_r: int = 0, jitter: int = 0, seed: int = 0):
+               diag: bool = False, chunks: int = 1, top_r: int = 0, jitter: int = 0, seed: int = 0,
+               gqa_shared: bool = False):
     """Mask on a paged cache. Kpages [num_pages, Hkv, page_size, d]; block_table [B, max_pages]."""
     Q, Kp = _f32(Q), _f32(Kpages)
     bt, sl = _i32(block_table), _i32(seq_lens)
@@ -247,15 +251,17 @@ def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causa
     num_pages, Hkv, ps, _ = Kp.shape
     n = k // bk
     nqb = -(-Tq // bq)
-    idx = np.empty((B, Hq, nqb, n), np.int32)
-    cnt = np.empty((B, Hq, nqb), np.int32)
-    mg = np.empty((B, Hq, nqb), np.float64)
-    em = np.empty((B, Hq, nqb), np.float64)
-    ns = np.empty((B, Hq, nqb), np.int64)
-    ni = np.empty((B, Hq, nqb), np.int32)
+    Hm = Hkv if gqa_shared else Hq
+    idx = np.empty((B, Hm, nqb, n), np.int32)
+    cnt = np.empty((B, Hm, nqb), np.int32)
+    mg = np.empty((B, Hm, nqb), np.float64)
+    em = np.empty((B, Hm, nqb), np.float64)
+    ns = np.empty((B, Hm, nqb), np.int64)
+    ni = np.empty((B, Hm, nqb), np.int32)
     rc = lib().oracle_mask_paged_ext(_p(Q), _p(Kp), num_pages, ps, _p(bt), bt.shape[1], _p(sl), B, Hq, Hkv, Tq,
                                      d, k, bq, bk, int(causal), mode, _p(idx), _p(cnt), _p(mg), _p(em), _p(ns),
-                                     _p(ni), int(chunks), int(top_r), int(jitter), int(seed) & (2**64 - 1))
+                                     _p(ni), int(chunks), int(top_r), int(jitter), int(seed) & (2**64 - 1),
+                                     int(bool(gqa_shared)))
     _check(rc, "oracle_mask_paged")
     if diag:
         return idx, cnt, dict(margin_min=mg, emax=em, n_scored=ns, n_iter=ni)
@@ -312,3 +318,10 @@ def vote(idx_samples, cnt_samples, theta: int, tau: int, n_out: int | None = Non
     _check(lib().oracle_vote(n_e, units, n, _p(I), _p(C), int(theta), int(tau), int(n_out), _p(out), _p(oc)),
            "oracle_vote")
     return out, oc
+
+
+def expand_gqa(idx, cnt, Hq: int):
+    """A GQA-shared mask [B, Hkv, ...] as per-query-head masks [B, Hq, ...]: head h uses group h // G."""
+    idx, cnt = np.asarray(idx), np.asarray(cnt)
+    G = Hq // idx.shape[1]
+    return np.repeat(idx, G, axis=1), np.repeat(cnt, G, axis=1)

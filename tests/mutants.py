@@ -46,6 +46,10 @@ MUTANTS = {
     "vote truncation prefers larger blocks": ("return (a->j > b->j) - (a->j < b->j);\n}\n\nstatic int i32_cmp",
                                               "return (a->j < b->j) - (a->j > b->j);\n}\n\nstatic int i32_cmp"),
     "vote threshold strict": ("if (j - i >= theta)", "if (j - i > theta)"),
+    "GQA-shared tile over the first head only": ("for (int64_t gt = 0; gt < (int64_t)G * (t1 - t0); ++gt) {",
+                                                 "for (int64_t gt = 0; gt < (int64_t)1 * (t1 - t0); ++gt) {"),
+    "GQA-shared rows taken from consecutive heads' wrong rows": ("const float *q = Qh + (gt / (t1 - t0)) * hstride + t * d;",
+                                                                  "const float *q = Qh + (gt / (t1 - t0)) * d + t * d;"),
     "union keeps duplicates": ("if (w == 0 || tok[i] != tok[w - 1]) tok[w++] = tok[i];", "tok[w++] = tok[i];"),
 }
 

@@ -821,3 +821,64 @@ def test_ensemble_single_sample_is_plain(orc):
     s = orc.mask(Q, K, 64, 16, 2, True, jitter=0, seed=4)
     idx, cnt = orc.vote(s[0][None], s[1][None], 1, 1)
     assert np.array_equal(idx, a[0]) and np.array_equal(cnt, a[1])
+
+
+# --------------------------------------------------------------------------------------------
+# f3b: GQA-shared masks (reading G25): one mask per (b, kv head, query block), the
+# representative score being the max of the tile over the query rows of ALL H_q / H_kv heads of
+# the group.  Pinned by reduction to the plain mask on a stacked-row input and by brute force.
+# --------------------------------------------------------------------------------------------
+def test_gqa_shared_group_of_one_is_plain(orc):
+    Q, K, _ = synth.gen_qkv(1, 2, 2, 1500, 1500, 32, "llm", seed=90, dtype=torch.float32, make_v=False)
+    a = orc.mask(Q, K, 64, 16, 2, True)
+    b = orc.mask(Q, K, 64, 16, 2, True, gqa_shared=True)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_gqa_shared_equals_stacked_rows_noncausal(orc, mode):
+    """Non-causal: the shared mask of group g at query block q is the plain mask of ONE query block
+    holding the G heads' rows of block q (a stacked [Nqb * G * b_q, d] query, b_q' = G * b_q)."""
+    B, Hq, Hkv, Tq, Tk, d, bq, k, bk = 2, 6, 2, 200, 1800, 32, 8, 64, 2
+    G = Hq // Hkv
+    Q, K, _ = synth.gen_qkv(B, Hq, Hkv, Tq, Tk, d, "iid", seed=91, dtype=torch.float32, make_v=False)
+    si, sc = orc.mask(Q, K, k, bq, bk, False, mode=mode, gqa_shared=True)
+    nqb = Tq // bq
+    for b in range(B):
+        for g in range(Hkv):
+            rows = Q[b, g * G:(g + 1) * G].reshape(G, nqb, bq, d).permute(1, 0, 2, 3).reshape(1, 1, nqb * G * bq, d)
+            pi, pc = orc.mask(rows, K[b:b + 1, g:g + 1], k, G * bq, bk, False, mode=mode)
+            assert np.array_equal(si[b, g], pi[0, 0]) and np.array_equal(sc[b, g], pc[0, 0])
+
+
+def test_gqa_shared_decode_equals_stacked_rows(orc):
+    """Paged decode (T_q = 1, causal: every key visible): the shared mask = the plain non-causal mask
+    of the G query rows of the group as one block, on the sequence's keys."""
+    B, Hq, Hkv, d, ps, k, bk = 3, 8, 2, 32, 16, 64, 2
+    seq = [900, 40, 2001]
+    G = Hq // Hkv
+    Q = synth.gen_decode_q(B, Hq, d, seed=92, dtype=torch.float32)
+    _, K, V = synth.gen_qkv(B, Hkv, Hkv, 1, max(seq), d, "iid", seed=92, dtype=torch.float32)
+    kp, vp, bt, sl = synth.to_paged(K, V, seq, ps, seed=92)
+    si, sc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, gqa_shared=True)
+    assert si.shape[1] == Hkv
+    for b in range(B):
+        for g in range(Hkv):
+            rows = Q[b, g * G:(g + 1) * G].reshape(1, 1, G, d)
+            pi, pc = orc.mask(rows, K[b:b + 1, g:g + 1, :seq[b]], k, G, bk, False)
+            assert np.array_equal(si[b, g, 0], pi[0, 0, 0]) and sc[b, g, 0] == pc[0, 0, 0]
+
+
+def test_gqa_shared_one_level_is_exact_topn(orc):
+    """Causal, n < B_q <= 2n: exact top-n of the block maxima over the whole group's rows (brute force)."""
+    T, d, k, bq, bk, Hq, Hkv = 1024, 16, 128, 16, 2, 4, 1
+    Q, K, _ = synth.gen_qkv(1, Hq, Hkv, T, T, d, "int", seed=93, dtype=torch.float32, make_v=False)
+    si, _ = orc.mask(Q, K, k, bq, bk, True, gqa_shared=True)
+    bs = _brute_block_scores(Q, K, bq, bk, True).max(axis=1)  # max over the group's heads
+    n, checked = k // bk, 0
+    for q in range(T // bq):
+        vis = _visible(q, bq, bk, T, T, True)
+        if n < vis <= 2 * n:
+            assert np.array_equal(si[0, 0, q], _topn_sorted(bs[0, q, :vis], n))
+            checked += 1
+    assert checked == 8
