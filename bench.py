@@ -380,6 +380,35 @@ def bench_decode(args, device):
         "dense_roofline_us": round(kv_bytes / (pk["hbm_gbs"] * 1e9) * 1e6, 1),
         "step_bytes": mask_bytes + attn_bytes,
     }
+    # appendix / NEXT options of the same step (different masks, not Alg. 1's per-head mask):
+    # GQA-shared masks (reading G25) alone and with the stridden partial top-k (S = 4, G21)
+    variants = {}
+    for name, ex in (("gqa_shared", dict(gqa_shared=True)), ("gqa_shared_chunks4", dict(gqa_shared=True, chunks=4))):
+        try:
+            ti = torch.empty(c["B"], c["Hkv"], 1, n, dtype=torch.int32, device=device)
+            tc = torch.empty(c["B"], c["Hkv"], 1, dtype=torch.int32, device=device)
+            akw = dict(kw, gqa_shared=True)
+            for _ in range(3):
+                HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(ti, tc), **kw, **ex)
+                HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], ti, tc, out=o, **akw)
+            torch.cuda.synchronize(device)
+            vm, va = [], []
+            for _ in range(max(args.steps, 5)):
+                ev[0].record(st)
+                HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(ti, tc), **kw, **ex)
+                ev[1].record(st)
+                HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], ti, tc, out=o, **akw)
+                ev[2].record(st)
+                torch.cuda.synchronize(device)
+                vm.append(ev[0].elapsed_time(ev[1]))
+                va.append(ev[1].elapsed_time(ev[2]))
+            vmu, vau = 1e3 * statistics.median(vm), 1e3 * statistics.median(va)
+            variants[name] = {"mask_us": round(vmu, 2), "attn_us": round(vau, 2), "us_per_step": round(vmu + vau, 2),
+                              "mask_bytes": mask_bytes // (c["Hq"] // c["Hkv"]),
+                              "mask_gbs": round(mask_bytes / (c["Hq"] // c["Hkv"]) / (vmu * 1e-6) / 1e9, 1)}
+        except Exception as e:  # noqa: BLE001 - an option failing must not hide the headline
+            variants[name] = {"error": repr(e)}
+    res["options"] = variants
     del kp, vp
     return res
 

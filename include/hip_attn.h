@@ -40,7 +40,8 @@
 extern "C" {
 #endif
 
-#define HIP_ATTN_VERSION 110 /* 1.1.0: top_r, split_jitter, sample_seed, hip_mask_vote */
+#define HIP_ATTN_VERSION 120 /* 1.2.0: + HIP_FLAG_GQA_SHARED_MASK (1.1.0: top_r, split_jitter, sample_seed,
+                                 hip_mask_vote) */
 
 typedef enum {
     HIP_SUCCESS = 0,
@@ -59,6 +60,13 @@ typedef enum {
 #define HIP_FLAG_EXACT_SCORES 1u /* mask: score every branch with the canonical sequential fp32 fmaf
                                     chain on CUDA cores even for bf16 (bit-exact with the oracle's
                                     F32C mode on any input; slower)                                 */
+#define HIP_FLAG_GQA_SHARED_MASK 2u /* GQA-shared masks (reading G25): ONE mask per
+                                    (b, kv head, query block), its branch scores the max of the tile
+                                    over the b_q rows of ALL H_q / H_kv query heads of the group.
+                                    hip_mask_estimate then writes block_idx [B, H_kv, N_qb, n] and
+                                    block_cnt [B, H_kv, N_qb]; the attention calls given the same
+                                    flag read query head h's selection from kv head h / (H_q/H_kv).
+                                    Requires (H_q / H_kv) x min(b_q, T_q) <= 64 rows.               */
 
 typedef struct {
     int32_t k;        /* token budget per query block; n = k / b_k key blocks are kept (G1)    */

@@ -84,6 +84,9 @@ hip_status_t check_common(hip_dtype_t dt, int32_t B, int32_t Hq, int32_t Hkv, in
   if (((int64_t)Tk + p->b_k - 1) / p->b_k >= (1 << 22))
     return fail(HIP_ERROR_NOT_SUPPORTED, "ceil(T_k / b_k) >= 2^22 key blocks (T_k=%d, b_k=%d)", Tk, p->b_k);
   if (std::min(p->b_q, Tq) > 64) return fail(HIP_ERROR_NOT_SUPPORTED, "query block of %d rows > 64", std::min(p->b_q, Tq));
+  if ((p->flags & HIP_FLAG_GQA_SHARED_MASK) && (int64_t)std::min(p->b_q, Tq) * (Hq / Hkv) > 64)
+    return fail(HIP_ERROR_NOT_SUPPORTED, "GQA-shared mask: (H_q / H_kv) x b_q = %d x %d rows > 64", Hq / Hkv,
+                std::min(p->b_q, Tq));
   if (p->chunks < 0 || (p->chunks > 1 && (p->k / p->b_k) % p->chunks))
     return fail(HIP_ERROR_INVALID_VALUE, "chunks=%d must be >= 0 and divide n = k/b_k = %d", p->chunks,
                 p->k / p->b_k);
@@ -129,6 +132,7 @@ hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk
   s.chunks = p->chunks > 1 ? p->chunks : 1;
   s.top_r = p->top_r > 0 && p->top_r < d ? p->top_r : 0;
   s.jitter = p->split_jitter;
+  s.group = (p->flags & HIP_FLAG_GQA_SHARED_MASK) ? Hq / Hkv : 1;
   s.seed = p->sample_seed;
   s.seq_lens = seq_lens;
   return s;

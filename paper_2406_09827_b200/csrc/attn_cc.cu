@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kACThreads, RPWM <= 2 ? 4 : 1) attn_cc_kernel(
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
     const int Tk = seq_len(sh, b);
-    const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
+    const int64_t lin = mask_lin(sh, b, h, q);  // the unit's mask row (GQA-shared: its group's, G25)
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
     const int64_t tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
     const int nkb = (Tk + sh.bk - 1) / sh.bk;

@@ -67,6 +67,7 @@ struct Shape {
   int top_r;         // mask: top-r approximation (topr.cuh), 0 = all d components
   int jitter;        // mask: ensemble split jitter R (select.cuh SplitJitter), 0 = half-up split
   uint64_t seed;     // mask: ensemble sample seed
+  int group;         // query heads per mask: H_q / H_kv for GQA-shared masks (reading G25), else 1
   const int32_t* seq_lens;
 };
 
@@ -81,6 +82,23 @@ __device__ __forceinline__ void unit_coords(const Shape& sh, int64_t u, int& b, 
   q = sh.nqb - 1 - (int)(u - bh * sh.nqb);
   b = (int)(bh / sh.Hq);
   h = (int)(bh - (int64_t)b * sh.Hq);
+}
+
+// Mask heads: one mask per kv head when GQA-shared (G25), else one per query head.
+__device__ __forceinline__ int mask_heads(const Shape& sh) { return sh.group > 1 ? sh.Hkv : sh.Hq; }
+
+// Mask unit u -> (b, mask head hm, q), in unit_coords' order.
+__device__ __forceinline__ void mask_unit_coords(const Shape& sh, int64_t u, int& b, int& hm, int& q) {
+  const int Hm = mask_heads(sh);
+  int64_t bh = u / sh.nqb;
+  q = sh.nqb - 1 - (int)(u - bh * sh.nqb);
+  b = (int)(bh / Hm);
+  hm = (int)(bh - (int64_t)b * Hm);
+}
+
+// Row of block_idx / block_cnt that query head h of batch b reads at query block q.
+__device__ __forceinline__ int64_t mask_lin(const Shape& sh, int b, int h, int q) {
+  return sh.group > 1 ? ((int64_t)b * sh.Hkv + h / sh.group) * sh.nqb + q : ((int64_t)b * sh.Hq + h) * sh.nqb + q;
 }
 
 // Visible key blocks of query block q (a1; reading G7): all blocks if not causal, else the blocks

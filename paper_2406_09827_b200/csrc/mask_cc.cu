@@ -29,6 +29,7 @@ struct CCScorer {
   float* pairs;      // [rows_per_chunk][rows_q]
   RowSrc ks;
   int b, hk, Tk, d, bk, causal, rows_q, ch;  // ch = key blocks per chunk
+  int rph = 1;       // rows per query head: row t sits at position tpos0 + t % rph (GQA-shared, G25)
   int64_t tpos0;     // key position of query row 0 of the block: q*bq + Tk - Tq
   HIP_PT_MEMBER
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
@@ -64,7 +65,7 @@ struct CCScorer {
       for (int p = threadIdx.x; p < rows * rows_q; p += kCCThreads) {
         int t = p % rows_q, r = p / rows_q;
         int64_t s = (int64_t)rep[blk0 + r / bk] * bk + (r % bk);
-        bool valid = s < Tk && (!causal || s <= tpos0 + t);
+        bool valid = s < Tk && (!causal || s <= tpos0 + t % rph);
         float acc = -INFINITY;
         if (valid) {
           const float4* qr = reinterpret_cast<const float4*>(qs + t * qpitch);
@@ -118,30 +119,31 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
                                                                 int stage_bytes) {
   extern __shared__ __align__(16) char smem[];
   SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
-  const int rows_max = min(sh.bq, sh.Tq);
+  const int rows_max = min(sh.bq, sh.Tq) * sh.group;
   const int qpitch = sh.d + 4;
   float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
   char* stage0 = reinterpret_cast<char*>(qs + rows_max * qpitch);  // qpitch*4 is a multiple of 16
   float* pairs = reinterpret_cast<float*>(stage0 + kCCStages * stage_bytes);
 
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t units = (int64_t)sh.B * mask_heads(sh) * sh.nqb;
   const int S = max(sh.chunks, 1);
   for (int64_t jb = blockIdx.x; jb < units * S; jb += gridDim.x) {
     const int64_t u = jb / S;
     const int cs = (int)(jb - u * S);
-    int b, h, q;
-    unit_coords(sh, u, b, h, q);
-    const int hk = h / (sh.Hq / sh.Hkv);
+    int b, h, q;  // h: mask head (the kv head when GQA-shared, G25)
+    mask_unit_coords(sh, u, b, h, q);
+    const int hk = sh.group > 1 ? h : h / (sh.Hq / sh.Hkv);
     const int Tk = seq_len(sh, b);
     const int Bq = visible_blocks(sh, q, Tk);
-    const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
-    const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    const int64_t lin = ((int64_t)b * mask_heads(sh) + h) * sh.nqb + q;
+    const int rph = min(sh.bq, sh.Tq - q * sh.bq);  // rows per query head
+    const int rows_q = rph * sh.group;               // rows scored together (G heads x rph)
     int lo, len, nn, slot0;
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     if (Bq > sh.n) {
       for (int i = threadIdx.x; i < rows_q * sh.d; i += kCCThreads) {
         int t = i / sh.d, c = i - t * sh.d;
-        const T* src = reinterpret_cast<const T*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + t));
+        const T* src = reinterpret_cast<const T*>(q_ptr(qsrc, b, sh.group > 1 ? h * sh.group + t / rph : h, (int64_t)q * sh.bq + t % rph));
         float v;
         if constexpr (sizeof(T) == 4) v = src[c];
         else v = __bfloat162float(src[c]);
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
     sc.pairs = pairs; sc.ks = ks; sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.d = sh.d; sc.bk = sh.bk;
     sc.causal = sh.causal; sc.rows_q = rows_q; sc.ch = ch;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+    sc.rph = rph;
     tree_search<NMAX, kCCThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
                             make_jitter(sh.jitter, sh.seed, lin));
     if (cs == 0 && threadIdx.x == 0) cnt[lin] = min(Bq, sh.n);
@@ -169,7 +172,7 @@ static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
                              cudaStream_t stream, int num_sms) {
   const int esize = sizeof(T);
   const int kpitch = sh.d * esize + 16;
-  const int rows_max = std::min(sh.bq, sh.Tq);
+  const int rows_max = std::min(sh.bq, sh.Tq) * sh.group;
   // decode (a single query row) is HBM-latency-bound: small chunks, many in flight; prefill rows
   // amortise bigger chunks.
   const int target = rows_max <= 4 ? 10 * 1024 : 16 * 1024;
@@ -182,7 +185,7 @@ static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kCCThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   int64_t grid = std::min<int64_t>(units * std::max(sh.chunks, 1), (int64_t)num_sms * per_sm);
   kern<<<(unsigned)grid, kCCThreads, smem, stream>>>(sh, qs, ks, idx, cnt, ch, kpitch, stage_bytes);
   return cudaGetLastError();

@@ -31,6 +31,7 @@ struct LaneScorer {
   const char* kh;
   uint32_t row_bytes;
   int b, hk, Tk, lbk, causal, rows_q;
+  int rph = 1;  // rows per query head (GQA-shared, G25): row t sits at position tpos0 + t % rph
   int64_t tpos0;
   HIP_PT_MEMBER
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
@@ -95,7 +96,7 @@ struct LaneScorer {
             for (int e = 0; e < E; ++e) acc = __fmaf_rn(qv[t][e], kvv[e], acc);
 #pragma unroll
             for (int o = 8; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (sv[i] < Tk && (!causal || sv[i] <= tpos0 + t) && acc > best) best = acc;
+            if (sv[i] < Tk && (!causal || sv[i] <= tpos0 + t % rph) && acc > best) best = acc;
           }
         }
         // rows r0 + i of one block are consecutive inside this half-warp (b_k | U)
@@ -118,24 +119,25 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
   SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
   float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
   const int lbk = 31 - __clz(sh.bk);
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t units = (int64_t)sh.B * mask_heads(sh) * sh.nqb;
   const int S = max(sh.chunks, 1);
   for (int64_t jb = blockIdx.x; jb < units * S; jb += gridDim.x) {
     const int64_t u = jb / S;
     const int cs = (int)(jb - u * S);
-    int b, h, q;
-    unit_coords(sh, u, b, h, q);
-    const int hk = h / (sh.Hq / sh.Hkv);
+    int b, h, q;  // h: mask head (the kv head when GQA-shared, G25)
+    mask_unit_coords(sh, u, b, h, q);
+    const int hk = sh.group > 1 ? h : h / (sh.Hq / sh.Hkv);
     const int Tk = seq_len(sh, b);
     const int Bq = visible_blocks(sh, q, Tk);
-    const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
-    const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    const int64_t lin = ((int64_t)b * mask_heads(sh) + h) * sh.nqb + q;
+    const int rph = min(sh.bq, sh.Tq - q * sh.bq);  // rows per query head
+    const int rows_q = rph * sh.group;               // rows scored together (G heads x rph)
     int lo, len, nn, slot0;
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     if (Bq > sh.n) {
       for (int i = threadIdx.x; i < rows_q * D; i += kMDThreads) {
         const int t = i / D, c = i - t * D;
-        const T* src = reinterpret_cast<const T*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + t));
+        const T* src = reinterpret_cast<const T*>(q_ptr(qsrc, b, sh.group > 1 ? h * sh.group + t / rph : h, (int64_t)q * sh.bq + t % rph));
         float v;
         if constexpr (sizeof(T) == 4) v = src[c];
         else v = __bfloat162float(src[c]);
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
     sc.row_bytes = (uint32_t)(ks.st * ks.esize);
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+    sc.rph = rph;
     tree_search<NMAX, kMDThreads>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
                             make_jitter(sh.jitter, sh.seed, lin));
     if (cs == 0 && threadIdx.x == 0) cnt[lin] = min(Bq, sh.n);
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
 
 // <= 4 query rows per block, b_k a power of two <= 16 (a block inside one half-warp batch).
 bool mask_decode_supported(const Shape& sh) {
-  return std::min(sh.bq, sh.Tq) <= kMDRows && sh.bk <= kMDU && (sh.bk & (sh.bk - 1)) == 0 &&
+  return std::min(sh.bq, sh.Tq) * sh.group <= kMDRows && sh.bk <= kMDU && (sh.bk & (sh.bk - 1)) == 0 &&
          (sh.d == 64 || sh.d == 128);
 }
 
@@ -173,7 +176,7 @@ static cudaError_t launch_md(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kMDThreads, smem, 0, &per_sm);
   if (e != cudaSuccess) return e;
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int64_t grid = std::min<int64_t>(units * std::max(sh.chunks, 1), (int64_t)num_sms * per_sm);
   kern<<<(unsigned)grid, kMDThreads, smem, stream>>>(sh, qs, ks, idx, cnt);
   return cudaGetLastError();
@@ -182,7 +185,7 @@ static cudaError_t launch_md(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
 template <typename T, int D>
 static cudaError_t launch_md_n(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                                cudaStream_t stream, int num_sms) {
-  const bool one = std::min(sh.bq, sh.Tq) == 1;  // plain decode: one query row
+  const bool one = std::min(sh.bq, sh.Tq) * sh.group == 1;  // plain decode: one query row
   if (sh.n <= 256)
     return one ? launch_md<T, D, 256, 1>(sh, qs, ks, idx, cnt, stream, num_sms)
                : launch_md<T, D, 256, kMDRows>(sh, qs, ks, idx, cnt, stream, num_sms);

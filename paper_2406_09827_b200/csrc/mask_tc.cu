@@ -59,7 +59,7 @@ struct RingShare {
   uint32_t* phases;  // bit s = parity to wait for on slot s's MMA barrier
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared>
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kExt = false>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
@@ -74,6 +74,7 @@ struct TCScorer {
   const char* kh;        // contiguous: row 0 of this (b, kv head)
   uint32_t row_bytes;    // contiguous: bytes between key rows
   int b, hk, Tk, lbk, causal, rows_q, bpt;
+  int rph = 32;          // kExt: rows per query head (GQA-shared, G25): row j sits at tpos0 + j % rph
   int64_t tpos0;
   const int* pg;         // paged: page of each representative block (aliases the score output)
   const char* rp[RJ];    // this thread's source rows of the tile being issued
@@ -208,7 +209,7 @@ struct TCScorer {
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j < rows_q && (!causal || s <= tpos0 + j)) best = fmaxf(best, v[j]);
+              if (j < rows_q && (!causal || s <= tpos0 + (kExt ? j % rph : j))) best = fmaxf(best, v[j]);
           }
         }
       }
@@ -323,18 +324,24 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
   PhaseTimer ptimer;
 #endif
 
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int S = max(sh.chunks, 1);
   for (int64_t jb = (int64_t)blockIdx.x * TEAMS + team; jb < units * S; jb += (int64_t)gridDim.x * TEAMS) {
     const int64_t u = jb / S;
     const int cs = (int)(jb - u * S);
-    int b, h, q;
-    unit_coords(sh, u, b, h, q);
-    const int hk = h / (sh.Hq / sh.Hkv);
+    int b, h, q;  // h: mask head (the kv head when GQA-shared, G25)
+    mask_unit_coords(sh, u, b, h, q);
+    const int hk = sh.group > 1 ? h : h / (sh.Hq / sh.Hkv);
     const int Tk = seq_len(sh, b);
     const int Bq = visible_blocks(sh, q, Tk);
-    const int64_t lin = ((int64_t)b * sh.Hq + h) * sh.nqb + q;
-    const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
+    const int64_t lin = ((int64_t)b * mask_heads(sh) + h) * sh.nqb + q;
+    const int rph = min(sh.bq, sh.Tq - q * sh.bq);    // rows per query head
+    const int rows_q = kExt ? rph * sh.group : rph;   // rows scored together
+    // query row r of the tile: head qhead(r), position q * b_q + r % rph
+    auto qrow = [&](int r) -> const char* {
+      if constexpr (kExt) return q_ptr(qsrc, b, sh.group > 1 ? h * sh.group + r / rph : h, (int64_t)q * sh.bq + r % rph);
+      else return q_ptr(qsrc, b, h, (int64_t)q * sh.bq + r);
+    };
     int lo, len, nn, slot0;
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     const uint32_t q_s = sbase + L::q + team * kQTileBytes;
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
         const int c = Sync::tid();
         float m = 0.f;
         for (int t = 0; t < rows_q; ++t) {
-          const __nv_bfloat16 v = *reinterpret_cast<const __nv_bfloat16*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + t) + 2 * c);
+          const __nv_bfloat16 v = *reinterpret_cast<const __nv_bfloat16*>(qrow(t) + 2 * c);
           m = fmaxf(m, fabsf(__bfloat162float(v)));
         }
         a[c] = m;
@@ -360,7 +367,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       for (int p = Sync::tid(); p < 32 * 16; p += NT) {
         const int r = p >> 4, c16 = p & 15;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (r < rows_q) v = *reinterpret_cast<const uint4*>(q_ptr(qsrc, b, h, (int64_t)q * sh.bq + r) + c16 * 16);
+        if (r < rows_q) v = *reinterpret_cast<const uint4*>(qrow(r) + c16 * 16);
         const uint32_t kbyte = (kw[c16 >> 2] >> ((c16 & 3) * 8)) & 0xffu;
         uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -379,12 +386,12 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       for (int p = Sync::tid(); p < 32 * 16; p += NT) {
         const int r = p >> 4, c16 = p & 15;
         const bool ok = r < rows_q;
-        const char* src = q_ptr(qsrc, b, h, (int64_t)q * sh.bq + (ok ? r : 0)) + c16 * 16;
+        const char* src = qrow(ok ? r : 0) + c16 * 16;
         cp_async16(q_s + (c16 >> 3) * (32 * 128) + sw128_off(r, c16 & 7), src, ok ? 16u : 0u);
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, (TEAMS > 1)> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, (TEAMS > 1), kExt> sc;
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = mbar;
@@ -397,6 +404,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     sc.b = b; sc.hk = hk; sc.Tk = Tk; sc.lbk = lbk; sc.causal = sh.causal; sc.rows_q = rows_q;
     sc.bpt = 128 >> lbk;
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+    sc.rph = rph;
     sc.ckeep = ckeep;
 #ifdef HIPATTN_PHASES
     sc.pt = &ptimer;
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
 // swizzled half tiles keeps more bytes in flight than the register-staged GEMV (C3: 229 vs 404 us).
 // b_k must be a power of two <= 32 so that a block's rows sit in one warp's TMEM lanes.
 bool mask_tc_supported(const Shape& sh) {
-  return sh.d == 128 && sh.bq >= 1 && sh.bq <= 32 && sh.bk >= 1 && sh.bk <= 32 && (32 % sh.bk) == 0 &&
+  return sh.d == 128 && sh.bq >= 1 && sh.bq * sh.group <= 32 && sh.bk >= 1 && sh.bk <= 32 && (32 % sh.bk) == 0 &&
          sh.n <= kMTNmax;
 }
 
@@ -433,7 +441,7 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
   if (e != cudaSuccess) return e;
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int64_t jobs = units * std::max(sh.chunks, 1);
   int64_t grid = std::min<int64_t>((jobs + TEAMS - 1) / TEAMS, (int64_t)num_sms * per_sm);
   kern<<<(unsigned)grid, 128 * TEAMS, smem, stream>>>(sh, qs, ks, idx, cnt);
@@ -443,7 +451,8 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
   // HIPATTN_MASK_TC selects a variant (tuning aid, profiles/r01).
-  if (sh.top_r > 0 || sh.jitter > 0) return launch_v<2, 4, 1, 4, true>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (sh.top_r > 0 || sh.jitter > 0 || sh.group > 1)
+    return launch_v<2, 4, 1, 4, true>(sh, qs, ks, idx, cnt, stream, num_sms);
   const char* v = getenv("HIPATTN_MASK_TC");
   if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_PKG, "libhipattn.so")
 HIP_SUCCESS, HIP_ERROR_INVALID_VALUE, HIP_ERROR_NOT_SUPPORTED, HIP_ERROR_WORKSPACE, HIP_ERROR_CUDA = range(5)
 HIP_DTYPE_F32, HIP_DTYPE_BF16 = 0, 1
 HIP_FLAG_EXACT_SCORES = 1
+HIP_FLAG_GQA_SHARED_MASK = 2
 HIP_OP_MASK, HIP_OP_PREFILL, HIP_OP_DECODE = 0, 1, 2
 
 EXPORTS = ("hip_version", "hip_last_error", "hip_num_blocks", "hip_workspace_bytes", "hip_mask_estimate",
@@ -112,10 +113,11 @@ def _stream(t: torch.Tensor, stream=None) -> int:
 
 
 def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False, sink: int = 0,
-            window: int = 0, chunks: int = 1, top_r: int = 0, jitter: int = 0, seed: int = 0) -> Params:
-    return Params(int(k), int(b_q), int(b_k), int(bool(causal)), float(sm_scale or 0.0),
-                  HIP_FLAG_EXACT_SCORES if exact else 0, int(sink), int(window), int(chunks), int(top_r),
-                  int(jitter), int(seed) & (2**64 - 1))
+            window: int = 0, chunks: int = 1, top_r: int = 0, jitter: int = 0, seed: int = 0,
+            gqa_shared: bool = False) -> Params:
+    flags = (HIP_FLAG_EXACT_SCORES if exact else 0) | (HIP_FLAG_GQA_SHARED_MASK if gqa_shared else 0)
+    return Params(int(k), int(b_q), int(b_k), int(bool(causal)), float(sm_scale or 0.0), flags, int(sink),
+                  int(window), int(chunks), int(top_r), int(jitter), int(seed) & (2**64 - 1))
 
 
 def _require_cuda(*ts):
@@ -131,21 +133,24 @@ def num_blocks(k: int, b_k: int) -> int:
 
 def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
                   causal: bool = True, exact: bool = False, chunks: int = 1, top_r: int = 0, jitter: int = 0,
-                  seed: int = 0, out=None, stream=None):
+                  seed: int = 0, gqa_shared: bool = False, out=None, stream=None):
     """hip_mask_estimate on contiguous keys.  q [B,Hq,Tq,d], k [B,Hkv,Tk,d] -> (idx, cnt).  chunks = S:
     stridden partial top-k; top_r: top-r approximation; jitter / seed: one
-    ensemble sample (combine with mask_vote)."""
+    ensemble sample (combine with mask_vote); gqa_shared: one mask per kv head over the
+    group's query heads (reading G25) -> idx [B, Hkv, Nqb, n]."""
     _require_cuda(q, k)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
-    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed)
+    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed,
+                gqa_shared=gqa_shared)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq
+    Hm = Hkv if gqa_shared else Hq
     if out is None:
-        idx = torch.empty((B, Hq, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
-        cnt = torch.empty((B, Hq, nqb), dtype=torch.int32, device=q.device)
+        idx = torch.empty((B, Hm, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
+        cnt = torch.empty((B, Hm, nqb), dtype=torch.int32, device=q.device)
     else:
         idx, cnt = out
     with torch.cuda.device(q.device):
@@ -194,20 +199,22 @@ def _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len: int) -> PagedKV
 
 def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, k_budget: int = 512, b_q: int = 32,
                         b_k: int = 2, causal: bool = True, exact: bool = False, chunks: int = 1, top_r: int = 0,
-                        jitter: int = 0, seed: int = 0, out=None, stream=None):
+                        jitter: int = 0, seed: int = 0, gqa_shared: bool = False, out=None, stream=None):
     """hip_mask_estimate on a paged cache (decode: q [B,Hq,Tq,d], Tq rows at positions seq_len-Tq+t)."""
     _require_cuda(q, k_pages, block_table, seq_lens)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
-    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed)
+    p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed,
+                gqa_shared=gqa_shared)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq
     pg, bt = _paged(k_pages, None, block_table, seq_lens, max_seq_len)
+    Hm = Hkv if gqa_shared else Hq
     if out is None:
-        idx = torch.empty((B, Hq, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
-        cnt = torch.empty((B, Hq, nqb), dtype=torch.int32, device=q.device)
+        idx = torch.empty((B, Hm, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
+        cnt = torch.empty((B, Hm, nqb), dtype=torch.int32, device=q.device)
     else:
         idx, cnt = out
     with torch.cuda.device(q.device):
@@ -220,14 +227,14 @@ def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, 
 
 def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2,
                              causal: bool = True, sm_scale=None, sink: int = 0, window: int = 0, out=None,
-                             return_lse: bool = False, stream=None):
+                             return_lse: bool = False, gqa_shared: bool = False, stream=None):
     """hip_sparse_attention_prefill.  Returns o (and lse fp32 [B,Hq,Tq] if return_lse).  sink/window
     add StreamingLLM sink and sliding-window tokens to every row (the paper: 32 / 128)."""
     _require_cuda(q, k, v, idx, cnt)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
-    p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window)
+    p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window, gqa_shared=gqa_shared)
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
     with torch.cuda.device(q.device):
@@ -239,13 +246,15 @@ def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int
 
 def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, idx, cnt, *,
                             k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True, sm_scale=None,
-                            sink: int = 0, window: int = 0, out=None, return_lse: bool = False, stream=None):
-    """hip_sparse_attention_decode on a paged cache.  q [B,Hq,Tq,d] -> o (and lse)."""
+                            sink: int = 0, window: int = 0, out=None, return_lse: bool = False,
+                            gqa_shared: bool = False, stream=None):
+    """hip_sparse_attention_decode on a paged cache.  q [B,Hq,Tq,d] -> o (and lse).  gqa_shared: idx/cnt
+    hold one mask per kv head (mask_estimate_paged(..., gqa_shared=True))."""
     _require_cuda(q, k_pages, v_pages, block_table, seq_lens, idx, cnt)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
-    p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window)
+    p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window, gqa_shared=gqa_shared)
     pg, bt = _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len)
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
@@ -259,9 +268,11 @@ def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_
 
 
 def hip_attention(q, k, v, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True,
-                  sm_scale=None, sink: int = 0, window: int = 0, out=None, stream=None):
+                  sm_scale=None, sink: int = 0, window: int = 0, gqa_shared: bool = False, out=None, stream=None):
     """One HiP attention layer (prefill): mask estimation then block-sparse attention (with the
-    optional sink / sliding-window tokens)."""
-    idx, cnt = mask_estimate(q, k, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal, stream=stream)
+    optional sink / sliding-window tokens and GQA-shared masks)."""
+    idx, cnt = mask_estimate(q, k, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal, gqa_shared=gqa_shared,
+                             stream=stream)
     return sparse_attention_prefill(q, k, v, idx, cnt, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal,
-                                    sm_scale=sm_scale, sink=sink, window=window, out=out, stream=stream)
+                                    sm_scale=sm_scale, sink=sink, window=window, gqa_shared=gqa_shared, out=out,
+                                    stream=stream)

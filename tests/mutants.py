@@ -15,8 +15,7 @@ MUTANTS = {
                                       "if (a->f > b->f) return -1;\n    if (a->f < b->f) return 1;"),
     "no causal mask inside the tile": ("if (causal && s > t + delta) continue;\n            const float *kk",
                                        "const float *kk"),
-    "tile max over the first query row only": ("for (int64_t t = t0; t < t1; ++t) {\n        const float *q = Qh",
-                                               "for (int64_t t = t0; t < t0 + 1; ++t) {\n        const float *q = Qh"),
+    "tile max over the first query row only": ("int64_t t = t0 + gt % (t1 - t0);", "int64_t t = t0;"),
     "causal bound off by one block": ("int64_t v = (tlast + (Tk - Tq)) / bk + 1;", "int64_t v = (tlast + (Tk - Tq)) / bk;"),
     "initial partition rounds down": ("int64_t fj = lo + (2 * (int64_t)j * L + n) / (2 * (int64_t)n);",
                                       "int64_t fj = lo + (2 * (int64_t)j * L) / (2 * (int64_t)n);"),
@@ -35,8 +34,8 @@ MUTANTS = {
     "window one token too long": ("for (int64_t s = p - window + 1; s <= p; ++s)", "for (int64_t s = p - window; s <= p; ++s)"),
     "sink ignores causality": ("for (int64_t s = 0; s < imin64(sink, Tk); ++s)\n                    if (!causal || s <= p) tok[ntok++] = s;",
                                "for (int64_t s = 0; s < imin64(sink, Tk); ++s)\n                    tok[ntok++] = s;"),
-    "top-r reduces |q| over the first row only": ("for (int64_t t = t0; t < t1; ++t) {\n            double v = fabs(",
-                                                 "for (int64_t t = t0; t < t0 + 1; ++t) {\n            double v = fabs("),
+    "top-r reduces |q| over the first row only": ("for (int64_t t = t0; t < t1; ++t) {\n                double v = fabs(",
+                                                 "for (int64_t t = t0; t < t0 + 1; ++t) {\n                double v = fabs("),
     "top-r ties toward the larger component": ("if (!taken[c] && (best < 0 || a[c] > a[best])) best = c;",
                                                "if (!taken[c] && (best < 0 || a[c] >= a[best])) best = c;"),
     "top-r score ignores the component list": ("int c = comp ? comp[i] : i;\n                    acc = fmaf(q[c], kk[c], acc);",

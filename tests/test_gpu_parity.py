@@ -590,3 +590,42 @@ def test_attention_wide_selection_parity(orc, paged):
     torch.cuda.synchronize()
     assert int(cnt.max()) > 256
     assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
+
+
+# ------------------------------------------------------------------------------------------------
+# f3b: GQA-shared masks (reading G25): one mask per kv head, scored over all its query heads' rows
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dt,dist,bq", [(torch.float32, "llm", 8), (torch.bfloat16, "int", 8), (torch.bfloat16, "int", 4)])
+def test_mask_gqa_shared_prefill_parity(orc, dt, dist, bq):
+    B, Hq, Hkv, Tq, Tk, k, bk = 1, 8, 2, 1200, 1300, 256, 2
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, Tq, Tk, 128, dist, seed=95, dtype=dt)
+    idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, gqa_shared=True)
+    o = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx, cnt, k_budget=k, b_q=bq, b_k=bk, gqa_shared=True)
+    torch.cuda.synchronize()
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, gqa_shared=True)
+    assert idx.shape[1] == Hkv
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    ei, ec = orc.expand_gqa(oi, oc, Hq)
+    Oo, _ = orc.sparse_attention(Q, K, V, k, bq, bk, True, ei, ec)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+
+
+@pytest.mark.parametrize("dt,dist", [(torch.float32, "iid"), (torch.bfloat16, "int")])
+@pytest.mark.parametrize("chunks", [1, 4])
+def test_mask_gqa_shared_decode_parity(orc, dt, dist, chunks):
+    B, Hq, Hkv, d, k, bk, ps = 3, 8, 2, 128, 512, 2, 64
+    seq = [6000, 77, 3333]
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=96, dtype=dt, dist=dist)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=96, dtype=dt, dist=dist)
+    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk,
+                                     chunks=chunks, gqa_shared=True)
+    o = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T, idx, cnt, k_budget=k, b_q=1,
+                                  b_k=bk, gqa_shared=True)
+    torch.cuda.synchronize()
+    mode = orc.F32L if dt == torch.float32 else orc.F32C
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=mode, chunks=chunks, gqa_shared=True)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    ei, ec = orc.expand_gqa(oi, oc, Hq)
+    Oo, _ = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, ei, ec)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
