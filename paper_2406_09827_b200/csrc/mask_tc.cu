@@ -455,6 +455,7 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
     return launch_v<2, 4, 1, 4, true>(sh, qs, ks, idx, cnt, stream, num_sms);
   const char* v = getenv("HIPATTN_MASK_TC");
   if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "s3")) return launch_v<3, 4, 1, 3>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   return launch_v<2, 4, 1, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
