@@ -276,3 +276,71 @@ def hip_attention(q, k, v, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, 
     return sparse_attention_prefill(q, k, v, idx, cnt, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal,
                                     sm_scale=sm_scale, sink=sink, window=window, gqa_shared=gqa_shared, out=out,
                                     stream=stream)
+
+
+def hip_attention_host(q, k, v, out, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True,
+                       sm_scale=None, sink: int = 0, window: int = 0, device=None, kv_heads_per_chunk: int = 2):
+    """One HiP prefill layer on PINNED HOST tensors q [B,Hq,T,d], k/v [B,Hkv,T,d] -> out (pinned host,
+    like q).  The kv heads (with their query heads) stream through the device in chunks on three CUDA
+    streams — host->device copy, mask + attention kernels, device->host copy — double-buffered, so the
+    PCIe transfers of one chunk overlap the kernels of its neighbours.  Returns an event recorded on
+    the copy-out stream when `out` is complete (the caller synchronises on it).  Marshalling and
+    scheduling only: all arithmetic runs in the library's kernels."""
+    if q.is_cuda or k.is_cuda or v.is_cuda or out.is_cuda:
+        raise ValueError("hip_attention_host takes host tensors (pinned for asynchronous copies)")
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    B, Hq, Tq, d = q.shape
+    _, Hkv, Tk, _ = k.shape
+    G = Hq // Hkv
+    ck = max(1, min(int(kv_heads_per_chunk), Hkv))
+    chunks = [(h, min(h + ck, Hkv)) for h in range(0, Hkv, ck)]
+    bq = max(1, min(int(b_q), Tq))
+    nqb = (Tq + bq - 1) // bq
+    n = k_budget // b_k
+    mk = lambda shape, dt: [torch.empty(shape, dtype=dt, device=device) for _ in range(2)]  # noqa: E731
+    Qd, Od = mk((B, G * ck, Tq, d), q.dtype), mk((B, G * ck, Tq, d), q.dtype)
+    Kd, Vd = mk((B, ck, Tk, d), k.dtype), mk((B, ck, Tk, d), v.dtype)
+    Id, Cd = mk((B, G * ck, nqb, n), torch.int32), mk((B, G * ck, nqb), torch.int32)
+    s_in, s_run, s_out = (torch.cuda.Stream(device) for _ in range(3))
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    run_done, out_done = [None, None], [None, None]
+    with torch.cuda.device(device):
+        for c, (g0, g1) in enumerate(chunks):
+            i, hq0, hq1, w = c % 2, g0 * G, g1 * G, g1 - g0
+            with torch.cuda.stream(s_in):
+                if run_done[i] is not None:
+                    s_in.wait_event(run_done[i])  # the kernels of chunk c - 2 have read buffer i
+                for b in range(B):
+                    Qd[i][b, :G * w].copy_(q[b, hq0:hq1], non_blocking=True)
+                    Kd[i][b, :w].copy_(k[b, g0:g1], non_blocking=True)
+                    Vd[i][b, :w].copy_(v[b, g0:g1], non_blocking=True)
+                in_done = ev()
+                in_done.record(s_in)
+            with torch.cuda.stream(s_run):
+                s_run.wait_event(in_done)
+                if out_done[i] is not None:
+                    s_run.wait_event(out_done[i])  # chunk c - 2's output has left buffer i
+                qq, kk, vv, oo = Qd[i][:, :G * w], Kd[i][:, :w], Vd[i][:, :w], Od[i][:, :G * w]
+                # mask outputs: contiguous [B, G*w, N_qb, n] views at the start of the buffers
+                ii = Id[i].view(-1)[:B * G * w * nqb * n].view(B, G * w, nqb, n)
+                cc = Cd[i].view(-1)[:B * G * w * nqb].view(B, G * w, nqb)
+                mask_estimate(qq, kk, k_budget=k_budget, b_q=b_q, b_k=b_k, causal=causal, out=(ii, cc), stream=s_run)
+                sparse_attention_prefill(qq, kk, vv, ii, cc, k_budget=k_budget,
+                                         b_q=b_q, b_k=b_k, causal=causal, sm_scale=sm_scale, sink=sink,
+                                         window=window, out=oo, stream=s_run)
+                run_done[i] = ev()
+                run_done[i].record(s_run)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(run_done[i])
+                for b in range(B):
+                    out[b, hq0:hq1].copy_(Od[i][b, :G * w], non_blocking=True)
+                out_done[i] = ev()
+                out_done[i].record(s_out)
+    done = ev()
+    done.record(s_out)
+    # the caching allocator must not hand these buffers out again before the three streams are done
+    for bufs in (Qd, Kd, Vd, Od, Id, Cd):
+        for t in bufs:
+            for s_ in (s_in, s_run, s_out):
+                t.record_stream(s_)
+    return done

@@ -629,3 +629,18 @@ def test_mask_gqa_shared_decode_parity(orc, dt, dist, chunks):
     ei, ec = orc.expand_gqa(oi, oc, Hq)
     Oo, _ = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, ei, ec)
     assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[dt]
+
+
+@pytest.mark.parametrize("chunk", [1, 3])
+def test_hip_attention_host_pipelined_equals_device(chunk):
+    """The pinned-host pipelined layer (3 streams, double-buffered head chunks) gives bit-for-bit the
+    device layer's output (results never depend on launch composition, PIN-9)."""
+    B, Hq, Hkv, T = 2, 8, 4, 1500
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, T, T, 128, "llm", seed=97, dtype=torch.bfloat16)
+    ref = H.hip_attention(Q.cuda(), K.cuda(), V.cuda(), k_budget=256, b_q=32, b_k=2)
+    Qh, Kh, Vh = Q.pin_memory(), K.pin_memory(), V.pin_memory()
+    Oh = torch.empty_like(Q).pin_memory()
+    done = H.hip_attention_host(Qh, Kh, Vh, Oh, k_budget=256, b_q=32, b_k=2, kv_heads_per_chunk=chunk)
+    done.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(Oh, ref.cpu())
