@@ -282,6 +282,48 @@ def bench_prefill(cfg, args, rank, world, device, pg):
                 clocks=clk.summary(), heads_per_rank=len(hs), tensors=(Q, K, V, O, idx, cnt))
 
 
+def mask_quality(Q, K, idx, cnt, cfg, n_samples=64, seed=0):
+    """Quality of the HiP mask on sampled query blocks (SURVEY 8(d) C4 "mask recall vs exact top-k";
+    SPEC S:131-135), measured with plain torch on the GPU (a measurement, not the product path):
+      block_recall   |HiP blocks  and  exact top-n blocks of the block-max scores| / n
+      token_recall   |HiP tokens  and  exact top-k tokens of the row scores| / k   (mean over rows)
+      attn_mass      softmax(q K^T / sqrt d) mass on the HiP tokens (mean over rows)
+    over query blocks with B_q > n (where the mask is an approximation)."""
+    import torch
+    T, bq, bk, k, d = cfg["T"], cfg["bq"], cfg["bk"], cfg["k"], cfg["d"]
+    n, H = k // bk, Q.shape[1]
+    g = torch.Generator().manual_seed(seed)
+    nqb = (T + bq - 1) // bq
+    q_lo = (n * bk) // bq + 1  # first query block with B_q > n
+    hs = torch.randint(0, H, (n_samples,), generator=g).tolist()
+    qs = torch.randint(q_lo, nqb, (n_samples,), generator=g).tolist()
+    br, tr, am = [], [], []
+    for h, qb in zip(hs, qs):
+        t0, t1 = qb * bq, min((qb + 1) * bq, T)
+        S = Q[0, h, t0:t1].float() @ K[0, h, :t1].float().T  # [rows, t1]
+        pos = torch.arange(t1, device=S.device)
+        rows = torch.arange(t0, t1, device=S.device)[:, None]
+        S = S.masked_fill(pos[None, :] > rows, float("-inf"))
+        nblk = (t1 + bk - 1) // bk
+        Sp = torch.nn.functional.pad(S, (0, nblk * bk - t1), value=float("-inf"))
+        bmax = Sp.view(S.shape[0], nblk, bk).amax(dim=(0, 2))
+        exact = set(torch.topk(bmax, n).indices.tolist())
+        sel = idx[0, h, qb, :int(cnt[0, h, qb])]
+        br.append(len(exact & set(sel.tolist())) / n)
+        tok = (sel[:, None] * bk + torch.arange(bk, device=sel.device)[None, :]).flatten()
+        tok = tok[tok < t1]
+        selmask = torch.zeros(t1, dtype=torch.bool, device=S.device)
+        selmask[tok] = True
+        top = torch.topk(S, k, dim=1).indices
+        tr.append(float(selmask[top].float().mean()))
+        P = torch.softmax(S / math.sqrt(d), dim=1)
+        am.append(float((P * selmask[None, :]).sum(dim=1).mean()))
+    return {"block_recall": round(sum(br) / len(br), 4), "token_topk_recall": round(sum(tr) / len(tr), 4),
+            "attention_mass": round(sum(am) / len(am), 4),
+            "sample": f"{n_samples} random query blocks with B_q > n across heads (seed {seed}); exact "
+                      "references by torch matmul on the GPU"}
+
+
 def dense_ms(Q, K, V, reps=3):
     import torch
     import torch.nn.functional as F
@@ -533,6 +575,7 @@ def main():
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
         Q, K, V = r["tensors"][:3]
+        extras["mask_quality"] = mask_quality(Q, K, r["tensors"][4], r["tensors"][5], cfg)
         extras["dense_sdpa_ms"] = round(dense_ms(Q, K, V), 3)
         extras["speedup_vs_dense"] = round(extras["dense_sdpa_ms"] / r["ms"], 2)
         del Q, K, V
@@ -547,15 +590,18 @@ def main():
         if cfg_name != "c4":
             try:
                 a2 = argparse.Namespace(**vars(args))
+                a2.no_e2e = True
                 a2.steps = 3
                 a2.warmup = 3
                 c4 = CONFIGS["c4"]
                 r4 = bench_prefill(c4, a2, 0, 1, device, None)
                 Q, K, V = r4["tensors"][:3]
+                q4 = mask_quality(Q, K, r4["tensors"][4], r4["tensors"][5], c4)
                 d4 = dense_ms(Q, K, V, reps=2)
                 extras["c4_128k"] = {"workload": c4["workload"], "ms": round(r4["ms"], 3),
                                      "mask_ms": round(r4["mask_ms"], 3), "attn_ms": round(r4["attn_ms"], 3),
                                      "dense_sdpa_ms": round(d4, 3), "speedup_vs_dense": round(d4 / r4["ms"], 2),
+                                     "mask_quality": q4,
                                      "roofline": roofline_obj(c4, c4["H"], r4["mask_ms"], r4["attn_ms"], pk)}
                 del Q, K, V, r4
             except Exception as e:  # noqa: BLE001

@@ -10,10 +10,13 @@ Distributions
   int  Q, K uniform integers in [-4, 4]; V ~ N(0, 1).         (every fp32 score sum is exact)
   llm  block-local, sink-heavy, partly long-range structure like LLaMA attention (P:90-95,
        P:1082-1084): segment topics u_g ~ N(0, I) for segments of 128 tokens; keys
-       k~_s = z_s + u_{g(s)}; queries q~_t = z'_t + u_{src(t)} with src(t) = g(t) w.p. 0.7, else
-       uniform over [0, g(t)]; z, z' ~ N(0, 0.5^2 I); a sink direction w ~ N(0, I) is added as
-       +3 w to the first 4 keys and +0.5 w to every query; everything is scaled by 1/2 and then
-       rotated with RoPE (NeoX pairing (c, c + d/2), base 10 000 or 500 000).
+       k~_s = z_s + u_{g(s)}; queries q~_t = z'_t + u_{src(t)}, where the source segment is drawn per
+       16-token phrase of queries (neighbouring queries attend to the same places — the locality
+       HiP's b_q blocks rely on, P:90-95): src = g(t) w.p. 0.7, else uniform over [0, g(t)];
+       z, z' ~ N(0, 0.5^2 I); a sink direction w ~ N(0, I) is added as +2.5 w to the first 4 keys
+       and +0.5 w to every query; RoPE (NeoX pairing (c, c + d/2), base 10 000 or 500 000).
+       At d = 128 a query's own-topic logit q.k / sqrt(d) is ~11 above the rest and the 4 sink keys
+       carry a share comparable to a whole topic segment: peaked, LLM-like attention rows.
 Seeds: sub-seed = seed * 16 + {0: Q, 1: K, 2: V, 3: page permutation, 4: indices}.
 """
 from __future__ import annotations
@@ -24,9 +27,10 @@ SEGMENT = 128
 P_LOCAL = 0.7
 NOISE = 0.5
 SINK_KEYS = 4
-SINK_K = 3.0
+SINK_K = 2.5
 SINK_Q = 0.5
-LLM_SCALE = 0.5
+LLM_SCALE = 1.0
+PHRASE = 16
 
 
 def _gen(seed: int, sub: int, device) -> torch.Generator:
@@ -70,8 +74,12 @@ def gen_qkv(B: int, Hq: int, Hkv: int, Tq: int, Tk: int, d: int, dist: str = "ii
         K[:, :, :nsink] += SINK_K * sink
         qpos = torch.arange(Tq, device=device) + (Tk - Tq)
         g = (qpos // SEGMENT).clamp(max=nseg - 1)
-        local = torch.rand(B, Hq, Tq, generator=gq, device=device) < P_LOCAL
-        far = (torch.rand(B, Hq, Tq, generator=gq, device=device) * (g + 1).float()).floor().long()
+        # one source draw per 16-token phrase of query positions
+        nph = (int(qpos[-1]) // PHRASE) + 1 if Tq > 0 else 1
+        ph = qpos // PHRASE
+        local = (torch.rand(B, Hq, nph, generator=gq, device=device) < P_LOCAL)[:, :, ph]
+        u = torch.rand(B, Hq, nph, generator=gq, device=device)[:, :, ph]
+        far = (u * (g + 1).float()).floor().long()
         src = torch.where(local, g.expand(B, Hq, Tq), far)
         grp = Hq // Hkv
         kvh = torch.arange(Hq, device=device) // grp
