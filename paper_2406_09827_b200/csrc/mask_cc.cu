@@ -118,10 +118,10 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
                                                                 int32_t* __restrict__ cnt, int ch, int kpitch,
                                                                 int stage_bytes) {
   extern __shared__ __align__(16) char smem[];
-  SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
+  SelState<NMAX, kCCThreads / 32>& st = *reinterpret_cast<SelState<NMAX, kCCThreads / 32>*>(smem);
   const int rows_max = min(sh.bq, sh.Tq) * sh.group;
   const int qpitch = sh.d + 4;
-  float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
+  float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX, kCCThreads / 32>), 128));
   char* stage0 = reinterpret_cast<char*>(qs + rows_max * qpitch);  // qpitch*4 is a multiple of 16
   float* pairs = reinterpret_cast<float*>(stage0 + kCCStages * stage_bytes);
 
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc q
       }
       __syncthreads();
       if (sh.top_r > 0 && sh.top_r < sh.d)  // top-r approximation (G22)
-        top_r_zero_f32<kCCThreads>(qs, qpitch, rows_q, sh.d, sh.top_r, st.rep_s);
+        top_r_zero_f32<kCCThreads>(qs, qpitch, rows_q, sh.d, sh.top_r, st.scores());
     }
     CCScorer<T> sc;
     sc.qs = qs; sc.qpitch = qpitch; sc.stage0 = stage0; sc.stage_bytes = stage_bytes; sc.kpitch = kpitch;
@@ -178,7 +178,7 @@ static cudaError_t launch_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   const int target = rows_max <= 4 ? 10 * 1024 : 16 * 1024;
   const int ch = std::max(1, target / (sh.bk * kpitch));
   const int stage_bytes = (int)align_up((size_t)ch * sh.bk * kpitch, 128);
-  size_t smem = align_up(sizeof(SelState<NMAX>), 128) + (size_t)rows_max * (sh.d + 4) * 4 +
+  size_t smem = align_up(sizeof(SelState<NMAX, kCCThreads / 32>), 128) + (size_t)rows_max * (sh.d + 4) * 4 +
                 (size_t)kCCStages * stage_bytes + (size_t)ch * sh.bk * rows_max * 4;
   smem = align_up(smem, 16);
   auto kern = mask_cc_kernel<T, NMAX>;

@@ -116,8 +116,8 @@ template <typename T, int D, int NMAX, int RM, bool kPaged>
 __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                  int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) char smem[];
-  SelState<NMAX>& st = *reinterpret_cast<SelState<NMAX>*>(smem);
-  float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX>), 128));
+  SelState<NMAX, kMDThreads / 32>& st = *reinterpret_cast<SelState<NMAX, kMDThreads / 32>*>(smem);
+  float* qs = reinterpret_cast<float*>(smem + align_up(sizeof(SelState<NMAX, kMDThreads / 32>), 128));
   const int lbk = 31 - __clz(sh.bk);
   const int64_t units = (int64_t)sh.B * mask_heads(sh) * sh.nqb;
   const int S = max(sh.chunks, 1);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QS
       }
       __syncthreads();
       if (sh.top_r > 0 && sh.top_r < D)  // top-r approximation (G22)
-        top_r_zero_f32<kMDThreads>(qs, D, rows_q, D, sh.top_r, st.rep_s);
+        top_r_zero_f32<kMDThreads>(qs, D, rows_q, D, sh.top_r, st.scores());
     }
     LaneScorer<T, D, RM, kPaged> sc;
     sc.qs = qs;
@@ -171,7 +171,7 @@ bool mask_decode_supported(const Shape& sh) {
 template <typename T, int D, int NMAX, int RM>
 static cudaError_t launch_md(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                              cudaStream_t stream, int num_sms) {
-  const size_t smem = align_up(sizeof(SelState<NMAX>), 128) + kMDRows * D * 4;
+  const size_t smem = align_up(sizeof(SelState<NMAX, kMDThreads / 32>), 128) + kMDRows * D * 4;
   auto kern = ks.paged ? mask_decode_kernel<T, D, NMAX, RM, true> : mask_decode_kernel<T, D, NMAX, RM, false>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kMDThreads, smem, 0, &per_sm);

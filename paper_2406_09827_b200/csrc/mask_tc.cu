@@ -48,7 +48,7 @@ struct MaskTCSmemLayout {
   static constexpr uint32_t k0 = 0;                                        // ring (1024-aligned)
   static constexpr uint32_t q = k0 + SLOTS * kMTSlot;                      // [TEAMS] Q tiles
   static constexpr uint32_t sel = q + TEAMS * kQTileBytes;                 // [TEAMS] SelState
-  static constexpr uint32_t sel_stride = (uint32_t)align_up(sizeof(SelState<kMTNmax>), 128);
+  static constexpr uint32_t sel_stride = (uint32_t)align_up(sizeof(SelState<kMTNmax, 4>), 128);
   static constexpr uint32_t misc = sel + TEAMS * sel_stride;               // mbarriers, lock, ...
   static constexpr uint32_t total = misc + 128;
 };
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
   const uint32_t sbase = raw + pad;
   using L = MaskTCSmemLayout<SLOTS, TEAMS>;
   const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / NT);
-  SelState<kMTNmax>& st = *reinterpret_cast<SelState<kMTNmax>*>(base + L::sel + team * L::sel_stride);
+  SelState<kMTNmax, 4>& st = *reinterpret_cast<SelState<kMTNmax, 4>*>(base + L::sel + team * L::sel_stride);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
   int* lock = reinterpret_cast<int*>(tmem_slot + 1);

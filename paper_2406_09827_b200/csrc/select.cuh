@@ -26,15 +26,19 @@ namespace hip {
 constexpr int kFirstBits = 22;                       // first block < 2^22 (T_k <= 4M * b_k)
 constexpr uint32_t kFirstMax = (1u << kFirstBits) - 1;
 
-template <int NMAX>
+// Selection state of one unit in shared memory.  NW = warps of the team.  The representatives'
+// scores (2 NMAX floats, written by the Scorer) alias the node arrays nf / nl: nodes are read into
+// registers at the start of an iteration and rewritten only by the compaction, after every score has
+// been turned into a ranking key, so the two never live at the same time.
+template <int NMAX, int NW = 32>
 struct SelState {
-  static constexpr int kRep = 2 * NMAX > 768 ? 2 * NMAX : 768;
-  int nf[NMAX], nl[NMAX];            // nodes (first, last block), position order
+  static constexpr int kRep = 2 * NMAX > 384 ? 2 * NMAX : 384;
+  int nf[NMAX], nl[NMAX];            // nodes (first, last block), position order | scores (scoring)
   uint32_t ns[NMAX];                 // their orderable scores
-  int rep[kRep];                     // representative blocks to score; 3 radix histograms after scoring
-  float rep_s[2 * NMAX];             // their scores (written by the Scorer)
-  unsigned long long red[64];        // per-warp OR / AND of the keys
-  int warp_tot[32];
+  int rep[kRep];                     // representative blocks to score; 3 packed radix histograms after
+  unsigned long long red[2 * NW];    // per-warp OR / AND of the keys
+  int warp_tot[NW];
+  __device__ __forceinline__ float* scores() { return reinterpret_cast<float*>(nf); }
 };
 
 // Barrier scope of the selection: the whole CTA (one unit per CTA), or one 128-thread team of a
@@ -96,12 +100,14 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
 // barrier per pass suffices: pass p fills H[p % 3] and clears H[(p + 2) % 3], whose last readers
 // (pass p - 1's scans) are behind pass p's barrier.  Requires 1 <= need <= number of valid keys.
 // Returns the number of histogram passes.
-template <int NT, int EC, int NMAX, class Sync>
-__device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t valid, int need, SelState<NMAX>& st,
+template <int NT, int EC, int NMAX, class Sync, int NW>
+__device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t valid, int need, SelState<NMAX, NW>& st,
                                          uint64_t& prefix, uint64_t& mask) {
   const int tid = Sync::tid(), lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = NT / 32;
-  int* hist = st.rep;
+  static_assert(NW == NT / 32, "SelState sized for the team");
+  // three histograms of 256 bins, two 16-bit counts per word (bin 2w low, 2w + 1 high): counts <=
+  // 2 NMAX < 2^16
+  uint32_t* hist = reinterpret_cast<uint32_t*>(st.rep);
   uint32_t olo = 0u, ohi = 0u, alo = ~0u, ahi = ~0u;
 #pragma unroll
   for (int k = 0; k < EC; ++k)
@@ -117,15 +123,15 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
   ahi = __reduce_and_sync(0xffffffffu, ahi);
   if (lane == 0) {
     st.red[warp] = ((uint64_t)ohi << 32) | olo;
-    st.red[32 + warp] = ((uint64_t)ahi << 32) | alo;
+    st.red[NW + warp] = ((uint64_t)ahi << 32) | alo;
   }
-  for (int i = tid; i < 512; i += NT) hist[i] = 0;  // H[0], H[1]
+  for (int i = tid; i < 256; i += NT) hist[i] = 0u;  // H[0], H[1]
   Sync::sync();
   uint64_t o = 0ull, a = ~0ull;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     o |= st.red[w];
-    a &= st.red[32 + w];
+    a &= st.red[NW + w];
   }
   const uint64_t diff = o ^ a;
   if (diff == 0ull) {  // a single distinct key
@@ -140,20 +146,24 @@ __device__ __forceinline__ int radix_top(const uint64_t (&key)[EC], uint32_t val
   for (int pass = 0;; ++pass) {
     const int s = top >= 7 ? top - 7 : 0;
     const uint32_t dmask = (1u << (top - s + 1)) - 1u;
-    int* h = hist + (pass % 3) * 256;
+    uint32_t* h = hist + (pass % 3) * 128;
 #pragma unroll
     for (int k = 0; k < EC; ++k)
-      if ((valid & (1u << k)) && (key[k] & mask) == prefix) atomicAdd(h + (uint32_t)((key[k] >> s) & dmask), 1);
+      if ((valid & (1u << k)) && (key[k] & mask) == prefix) {
+        const uint32_t bin = (uint32_t)((key[k] >> s) & dmask);
+        atomicAdd(h + (bin >> 1), 1u << ((bin & 1u) * 16));
+      }
     Sync::sync();
     {
-      int* hz = hist + ((pass + 2) % 3) * 256;  // clear the histogram of pass + 2
-      for (int i = tid; i < 256; i += NT) hz[i] = 0;
+      uint32_t* hz = hist + ((pass + 2) % 3) * 128;  // clear the histogram of pass + 2
+      for (int i = tid; i < 128; i += NT) hz[i] = 0u;
     }
-    // lane L owns bins [248 - 8L, 255 - 8L], walked from the top (every warp, same result)
+    // lane L owns bins [248 - 8L, 255 - 8L] (words [124 - 4L, 127 - 4L]), walked from the top
+    // (every warp, same result)
     const int b0 = 248 - 8 * lane;
-    const int4 v0 = *reinterpret_cast<const int4*>(h + b0);
-    const int4 v1 = *reinterpret_cast<const int4*>(h + b0 + 4);
-    const int c[8] = {v1.w, v1.z, v1.y, v1.x, v0.w, v0.z, v0.y, v0.x};
+    const uint4 v = *reinterpret_cast<const uint4*>(h + (b0 >> 1));
+    const int c[8] = {(int)(v.w >> 16), (int)(v.w & 0xffffu), (int)(v.z >> 16), (int)(v.z & 0xffffu),
+                      (int)(v.y >> 16), (int)(v.y & 0xffffu), (int)(v.x >> 16), (int)(v.x & 0xffffu)};
     int sum = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) sum += c[i];
@@ -237,8 +247,8 @@ __device__ __forceinline__ bool chunk_job(int Bq, int n, int S, int s, int& lo, 
 // selected blocks (ascending, -1 padded) to out_idx and, if out_cnt, the count.  All NT threads
 // call it.  Scorer::score(rep, n_rep, rep_s) must fill rep_s[i] = tile score of key block rep[i] and
 // end with a Sync::sync(); Scorer::mark(p) is a profiling hook (no-op in product builds).
-template <int NMAX, int NT, class Scorer, class Sync = CtaSync>
-__device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& scorer, int32_t* out_idx,
+template <int NMAX, int NT, class Scorer, class Sync = CtaSync, int NW = NT / 32>
+__device__ void tree_search(SelState<NMAX, NW>& st, int n, int lo, int Bq, Scorer& scorer, int32_t* out_idx,
                             int32_t* out_cnt, const SplitJitter& jit = SplitJitter()) {
   static_assert(NMAX % NT == 0 || NT % NMAX == 0, "NMAX and NT must nest");
   constexpr int E = NMAX >= NT ? NMAX / NT : 1;  // nodes per thread (contiguous)
@@ -326,19 +336,19 @@ __device__ void tree_search(SelState<NMAX>& st, int n, int lo, int Bq, Scorer& s
     Sync::sync();
     scorer.mark(0);  // split + scan
     // --- representative scores (Alg. 1 lines 10-13)
-    scorer.score(st.rep, first ? C : nB, st.rep_s);
+    scorer.score(st.rep, first ? C : nB, st.scores());
     // --- top-n (Alg. 1 lines 14-15)
     uint64_t key[EC];
 #pragma unroll
     for (int k = 0; k < EC; ++k)
-      key[k] = make_key(kr[k] >= 0 ? ord_score(st.rep_s[kr[k]]) : ks[k], kf[k]);
+      key[k] = make_key(kr[k] >= 0 ? ord_score(st.scores()[kr[k]]) : ks[k], kf[k]);
     uint64_t prefix, mask;
     scorer.mark(8);  // keys
     uint32_t live = valid;
 #pragma unroll
     for (int k = 0; k < EC; ++k)
       if (key[k] < lb) live &= ~(1u << k);
-    const int passes = radix_top<NT, EC, NMAX, Sync>(key, live, n, st, prefix, mask);
+    const int passes = radix_top<NT, EC, NMAX, Sync, NW>(key, live, n, st, prefix, mask);
     valid = live;
     lb = prefix;
     scorer.mark(4);  // radix select
