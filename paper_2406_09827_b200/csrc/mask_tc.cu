@@ -43,10 +43,12 @@ constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 r
 constexpr uint32_t kMTSlot = 128 * 128;          // one item: 128 rows x 64 bf16
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
-template <int SLOTS, int TEAMS>
+// RINGS = 1 (one ring, shared by the teams when TEAMS > 1) or TEAMS (a private ring per team).
+template <int SLOTS, int TEAMS, int RINGS = 1>
 struct MaskTCSmemLayout {
-  static constexpr uint32_t k0 = 0;                                        // ring (1024-aligned)
-  static constexpr uint32_t q = k0 + SLOTS * kMTSlot;                      // [TEAMS] Q tiles
+  static constexpr uint32_t k0 = 0;                                        // ring(s) (1024-aligned)
+  static constexpr uint32_t ring_stride = SLOTS * kMTSlot;
+  static constexpr uint32_t q = k0 + RINGS * ring_stride;                  // [TEAMS] Q tiles
   static constexpr uint32_t sel = q + TEAMS * kQTileBytes;                 // [TEAMS] SelState
   static constexpr uint32_t sel_stride = (uint32_t)align_up(sizeof(SelState<kMTNmax, 4>), 128);
   static constexpr uint32_t misc = sel + TEAMS * sel_stride;               // mbarriers, lock, ...
@@ -281,32 +283,39 @@ struct TCScorer {
   }
 };
 
-// TEAMS units per CTA (NT = 128 threads each); TEAMS = 2 shares the ring (see the header).
+// TEAMS units per CTA (NT = 128 threads each); RINGS = 1 with TEAMS = 2 shares the ring (ping-pong,
+// see the header), RINGS = TEAMS gives every team a private ring (TEAMS = 5: five units per SM in
+// one CTA — one CTA saves the per-CTA shared-memory reservation that keeps separate CTAs at 4).
 // kExt: the appendix options (top-r, ensemble split jitter) — a separate instantiation, so the plain
 // Alg. 1 kernel carries none of their code or registers.
-template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, bool kExt>
+template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, bool kExt, int RINGS = 1>
 __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
   constexpr int NT = 128;
-  constexpr uint32_t kCols = 32 * TT * TEAMS;
+  constexpr bool kSharedRing = TEAMS > 1 && RINGS == 1;
+  constexpr uint32_t kColsUsed = 32 * TT * TEAMS;
+  constexpr uint32_t kCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
+                             : kColsUsed <= 256 ? 256 : 512;  // allocation: a power of two
+  static_assert(kColsUsed <= 512, "TMEM columns");
   using Sync = typename std::conditional<TEAMS == 1, CtaSync, TeamSync<NT>>::type;
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<SLOTS, TEAMS>;
+  using L = MaskTCSmemLayout<SLOTS, TEAMS, RINGS>;
   const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / NT);
   SelState<kMTNmax, 4>& st = *reinterpret_cast<SelState<kMTNmax, 4>*>(base + L::sel + team * L::sel_stride);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
+  uint64_t* mbar_all = reinterpret_cast<uint64_t*>(base + L::misc);
+  uint64_t* mbar = mbar_all + (RINGS > 1 ? team * SLOTS : 0);  // this team's ring barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS * RINGS);
   int* lock = reinterpret_cast<int*>(tmem_slot + 1);
   uint32_t* ring_phases = tmem_slot + 2;
   const int warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < SLOTS; ++s) mbar_init(mbar + s, 1);
+    for (int s = 0; s < SLOTS * RINGS; ++s) mbar_init(mbar_all + s, 1);
     *lock = -1;
     *ring_phases = 0u;
     fence_mbar_init();
@@ -391,9 +400,9 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, (TEAMS > 1), kExt> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kExt> sc;
     sc.q_s = q_s;
-    sc.k_s0 = sbase + L::k0;
+    sc.k_s0 = sbase + L::k0 + (RINGS > 1 ? team * L::ring_stride : 0u);
     sc.mbar = mbar;
     sc.phase = phase;
     sc.tmem = tmem;
@@ -432,12 +441,12 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int SLOTS, int TT, int TEAMS, int MINB, bool kExt = false>
+template <int SLOTS, int TT, int TEAMS, int MINB, bool kExt = false, int RINGS = 1>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
-  const size_t smem = MaskTCSmemLayout<SLOTS, TEAMS>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, kExt>
-                       : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, kExt>;
+  const size_t smem = MaskTCSmemLayout<SLOTS, TEAMS, RINGS>::total + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, kExt, RINGS>
+                       : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, kExt, RINGS>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
   if (e != cudaSuccess) return e;
@@ -456,6 +465,7 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
   const char* v = getenv("HIPATTN_MASK_TC");
   if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "s3")) return launch_v<3, 4, 1, 3>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "t5")) return launch_v<2, 3, 5, 1, false, 5>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   return launch_v<2, 4, 1, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
