@@ -61,7 +61,7 @@ struct RingShare {
   uint32_t* phases;  // bit s = parity to wait for on slot s's MMA barrier
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kExt = false>
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kGrp = false>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
@@ -76,7 +76,7 @@ struct TCScorer {
   const char* kh;        // contiguous: row 0 of this (b, kv head)
   uint32_t row_bytes;    // contiguous: bytes between key rows
   int b, hk, Tk, lbk, causal, rows_q, bpt;
-  int rph = 32;          // kExt: rows per query head (GQA-shared, G25): row j sits at tpos0 + j % rph
+  int rph = 32;          // kGrp: rows per query head (GQA-shared, G25): row j sits at tpos0 + j % rph
   int64_t tpos0;
   const int* pg;         // paged: page of each representative block (aliases the score output)
   const char* rp[RJ];    // this thread's source rows of the tile being issued
@@ -208,10 +208,14 @@ struct TCScorer {
               m0 = fmaxf(m0, v[j]); m1 = fmaxf(m1, v[j + 1]); m2 = fmaxf(m2, v[j + 2]); m3 = fmaxf(m3, v[j + 3]);
             }
             best = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+          } else if constexpr (kGrp) {  // rows of G heads: row j sits at position tpos0 + j % rph
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < rows_q && (!causal || s <= tpos0 + j % rph)) best = fmaxf(best, v[j]);
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j < rows_q && (!causal || s <= tpos0 + (kExt ? j % rph : j))) best = fmaxf(best, v[j]);
+              if (j < rows_q && (!causal || s <= tpos0 + j)) best = fmaxf(best, v[j]);
           }
         }
       }
@@ -286,13 +290,15 @@ struct TCScorer {
 // TEAMS units per CTA (NT = 128 threads each); RINGS = 1 with TEAMS = 2 shares the ring (ping-pong,
 // see the header), RINGS = TEAMS gives every team a private ring (TEAMS = 5: five units per SM in
 // one CTA — one CTA saves the per-CTA shared-memory reservation that keeps separate CTAs at 4).
-// kExt: the appendix options (top-r, ensemble split jitter) — a separate instantiation, so the plain
-// Alg. 1 kernel carries none of their code or registers.
-template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, bool kExt, int RINGS = 1>
+// EXT: the mask options, each a separate instantiation so that the plain Alg. 1 kernel (EXT = 0)
+// carries none of their code or registers: bit 0 ensemble split jitter (G23), bit 1 top-r (G22),
+// bit 2 GQA-shared rows (G25).
+template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, int EXT, int RINGS = 1>
 __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
   constexpr int NT = 128;
+  constexpr bool kJit = (EXT & 1) != 0, kTopR = (EXT & 2) != 0, kGrp = (EXT & 4) != 0;
   constexpr bool kSharedRing = TEAMS > 1 && RINGS == 1;
   constexpr uint32_t kColsUsed = 32 * TT * TEAMS;
   constexpr uint32_t kCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
@@ -345,17 +351,19 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     const int Bq = visible_blocks(sh, q, Tk);
     const int64_t lin = ((int64_t)b * mask_heads(sh) + h) * sh.nqb + q;
     const int rph = min(sh.bq, sh.Tq - q * sh.bq);    // rows per query head
-    const int rows_q = kExt ? rph * sh.group : rph;   // rows scored together
+    const int rows_q = kGrp ? rph * sh.group : rph;   // rows scored together
     // query row r of the tile: head qhead(r), position q * b_q + r % rph
     auto qrow = [&](int r) -> const char* {
-      if constexpr (kExt) return q_ptr(qsrc, b, sh.group > 1 ? h * sh.group + r / rph : h, (int64_t)q * sh.bq + r % rph);
-      else return q_ptr(qsrc, b, h, (int64_t)q * sh.bq + r);
+      if constexpr (kGrp) {
+        if (sh.group > 1) return q_ptr(qsrc, b, h * sh.group + r / rph, (int64_t)q * sh.bq + r % rph);
+      }
+      return q_ptr(qsrc, b, h, (int64_t)q * sh.bq + r);
     };
     int lo, len, nn, slot0;
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
     const uint32_t q_s = sbase + L::q + team * kQTileBytes;
     uint32_t ckeep = 3u;  // bit h: this thread's 16-byte key chunk of d-half h holds a kept component
-    if (kExt && Bq > sh.n && sh.top_r > 0 && sh.top_r < 128) {
+    if (kTopR && Bq > sh.n && sh.top_r > 0 && sh.top_r < 128) {
       // top-r approximation (G22; topr.cuh): a_c = max_t |q_tc| (thread c), keep bits by
       // rank -> st.warp_tot[c / 32]; the query tile is stored with the dropped components zeroed
       float* a = reinterpret_cast<float*>(st.rep);
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kExt> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp> sc;
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0 + (RINGS > 1 ? team * L::ring_stride : 0u);
     sc.mbar = mbar;
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     ptimer.mark(7);  // unit setup / Q load / exact units
 #endif
     tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
-                                                 kExt ? make_jitter(sh.jitter, sh.seed, lin) : SplitJitter());
+                                                 kJit ? make_jitter(sh.jitter, sh.seed, lin) : SplitJitter());
     if (cs == 0 && Sync::tid() == 0) cnt[lin] = min(Bq, sh.n);
     Sync::sync();
   }
@@ -441,12 +449,12 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int SLOTS, int TT, int TEAMS, int MINB, bool kExt = false, int RINGS = 1>
+template <int SLOTS, int TT, int TEAMS, int MINB, int EXT = 0, int RINGS = 1>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
   const size_t smem = MaskTCSmemLayout<SLOTS, TEAMS, RINGS>::total + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, kExt, RINGS>
-                       : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, kExt, RINGS>;
+  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, EXT, RINGS>
+                       : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, EXT, RINGS>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
   if (e != cudaSuccess) return e;
@@ -460,12 +468,18 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
   // HIPATTN_MASK_TC selects a variant (tuning aid, profiles/r01).
-  if (sh.top_r > 0 || sh.jitter > 0 || sh.group > 1)
-    return launch_v<2, 4, 1, 4, true>(sh, qs, ks, idx, cnt, stream, num_sms);
+  const int ext = (sh.jitter > 0 ? 1 : 0) | (sh.top_r > 0 ? 2 : 0) | (sh.group > 1 ? 4 : 0);
+  switch (ext) {  // one instantiation per single option, one for combinations
+    case 0: break;
+    case 1: return launch_v<2, 4, 1, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
+    case 2: return launch_v<2, 4, 1, 4, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+    case 4: return launch_v<2, 4, 1, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+    default: return launch_v<2, 4, 1, 4, 7>(sh, qs, ks, idx, cnt, stream, num_sms);
+  }
   const char* v = getenv("HIPATTN_MASK_TC");
   if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "s3")) return launch_v<3, 4, 1, 3>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "t5")) return launch_v<2, 3, 5, 1, false, 5>(sh, qs, ks, idx, cnt, stream, num_sms);
+  if (v && !strcmp(v, "t5")) return launch_v<2, 3, 5, 1, 0, 5>(sh, qs, ks, idx, cnt, stream, num_sms);
   if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
   return launch_v<2, 4, 1, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }

@@ -23,11 +23,15 @@ class HipDecoder:
     """Cached-mask HiP attention for one layer of a decoder (Alg. 2 lines 8-12)."""
 
     def __init__(self, r_m: int = 8, k_budget: int = 512, b_k: int = 2, b_q: int = 32, causal: bool = True,
-                 sink: int = 0, window: int = 0, sm_scale=None):
+                 sink: int = 0, window: int = 0, sm_scale=None, gqa_shared: bool = False, chunks: int = 1):
+        """gqa_shared / chunks: the mask options of SURVEY §8 f3 — one mask per GQA group (reading
+        G25) and the stridden partial top-k with S chunks (G21) — the low-latency decode
+        configuration when the batch gives fewer units than the GPU has CTA slots."""
         if r_m < 1:
             raise ValueError("r_m must be >= 1")
         self.r_m, self.k_budget, self.b_k, self.b_q = int(r_m), int(k_budget), int(b_k), int(b_q)
         self.causal, self.sink, self.window, self.sm_scale = bool(causal), int(sink), int(window), sm_scale
+        self.gqa_shared, self.chunks = bool(gqa_shared), int(chunks)
         self.idx = None
         self.cnt = None
         self.refreshes = 0  # number of steps that ran the mask estimation (for tests / stats)
@@ -44,7 +48,8 @@ class HipDecoder:
         rows = self.refresh_rows(seq_lens_host)
         if any(rows):
             idx, cnt = H.mask_estimate_paged(q, k_pages, block_table, seq_lens, max_len, k_budget=self.k_budget,
-                                             b_q=self.b_q, b_k=self.b_k, causal=self.causal, stream=stream)
+                                             b_q=self.b_q, b_k=self.b_k, causal=self.causal,
+                                             gqa_shared=self.gqa_shared, chunks=self.chunks, stream=stream)
             if self.idx is None or self.idx.shape != idx.shape or all(rows):
                 self.idx, self.cnt = idx, cnt
             else:
@@ -55,4 +60,4 @@ class HipDecoder:
         return H.sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_len, self.idx, self.cnt,
                                          k_budget=self.k_budget, b_q=self.b_q, b_k=self.b_k, causal=self.causal,
                                          sm_scale=self.sm_scale, sink=self.sink, window=self.window,
-                                         return_lse=return_lse, stream=stream)
+                                         return_lse=return_lse, gqa_shared=self.gqa_shared, stream=stream)

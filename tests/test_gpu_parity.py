@@ -411,15 +411,17 @@ def test_multi_query_decode_parity(orc, dt, dist, Tq):
     assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
 
 
-def test_decoder_rm_cache_schedule(orc):
+@pytest.mark.parametrize("shared,chunks", [(False, 1), (True, 2)])
+def test_decoder_rm_cache_schedule(orc, shared, chunks):
     """HipDecoder: the mask is re-estimated exactly when a sequence's length is divisible by r_m
     (Alg. 2 line 8) and reused in between; every step's output is the oracle's attention over the
-    cached selection at the current length (the steps 'append' tokens already present in pages)."""
+    cached selection at the current length (the steps 'append' tokens already present in pages).
+    Also with the GQA-shared + chunked mask options."""
     from paper_2406_09827_b200.decode import HipDecoder
     B, Hq, Hkv, d, k, bk, ps, r_m = 2, 4, 2, 128, 128, 2, 16, 4
     full = [700, 901]
     kp, vp, bt, _ = synth.gen_paged_direct(B, Hkv, full, d, ps, seed=31, dist="int")
-    dec = HipDecoder(r_m=r_m, k_budget=k, b_k=bk, b_q=1, sink=4, window=16)
+    dec = HipDecoder(r_m=r_m, k_budget=k, b_k=bk, b_q=1, sink=4, window=16, gqa_shared=shared, chunks=chunks)
     lens = [690, 893]
     cached = None
     for step in range(8):
@@ -429,7 +431,8 @@ def test_decoder_rm_cache_schedule(orc):
         expect_refresh = [cached is None or t % r_m == 0 for t in cur]
         o = dec.step(q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), cur)
         torch.cuda.synchronize()
-        oi, oc = orc.mask_paged(q, kp, bt, sl, k, 1, bk, True)  # integer inputs: exact in any order
+        # integer inputs: exact in any order
+        oi, oc = orc.mask_paged(q, kp, bt, sl, k, 1, bk, True, gqa_shared=shared, chunks=chunks)
         gi, gc = dec.idx.cpu().numpy(), dec.cnt.cpu().numpy()
         for b in range(B):
             if expect_refresh[b]:
@@ -437,7 +440,8 @@ def test_decoder_rm_cache_schedule(orc):
             else:
                 assert np.array_equal(gi[b], cached[0][b]) and np.array_equal(gc[b], cached[1][b])
         cached = (gi.copy(), gc.copy())
-        Oo, _ = orc.sparse_attention_paged(q, kp, vp, bt, sl, k, 1, bk, True, gi, gc, sink=4, window=16)
+        ei, ec = orc.expand_gqa(gi, gc, Hq) if shared else (gi, gc)
+        Oo, _ = orc.sparse_attention_paged(q, kp, vp, bt, sl, k, 1, bk, True, ei, ec, sink=4, window=16)
         assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
     assert 1 < dec.refreshes < 8
 
@@ -644,3 +648,38 @@ def test_hip_attention_host_pipelined_equals_device(chunk):
     done.synchronize()
     torch.cuda.synchronize()
     assert torch.equal(Oh, ref.cpu())
+
+
+def test_vote_edge_cases(orc):
+    """Empty sample rows, all-identical samples, theta = n_e with disjoint samples (empty result)."""
+    n, units = 8, 4
+    I = torch.full((3, units, n), -1, dtype=torch.int32)
+    C = torch.zeros((3, units), dtype=torch.int32)
+    I[:, 1, :3] = torch.tensor([2, 5, 9], dtype=torch.int32)       # identical in every sample
+    C[:, 1] = 3
+    for e in range(3):                                              # disjoint
+        I[e, 2, :2] = torch.tensor([10 * e, 10 * e + 1], dtype=torch.int32)
+        C[e, 2] = 2
+    I[0, 3, :n] = torch.arange(n, dtype=torch.int32)                # one full row, others empty
+    C[0, 3] = n
+    for theta, tau in ((1, 0), (1, 1), (3, 1), (2, 0)):
+        gi, gc = H.mask_vote(I.cuda(), C.cuda(), theta=theta, tau=tau)
+        oi, oc = orc.vote(I, C, theta, tau)
+        torch.cuda.synchronize()
+        assert np.array_equal(gi.cpu().numpy(), oi) and np.array_equal(gc.cpu().numpy(), oc)
+    assert oc[0] == 0
+
+
+def test_gqa_shared_with_sinkwin_prefill(orc):
+    """GQA-shared mask + sink / window tokens in the prefill attention (the two options compose)."""
+    B, Hq, Hkv, T, k, bq, bk = 1, 4, 2, 900, 128, 16, 2
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, T, T, 128, "int", seed=98, dtype=torch.bfloat16)
+    idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, gqa_shared=True)
+    o = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx, cnt, k_budget=k, b_q=bq, b_k=bk, sink=32,
+                                   window=128, gqa_shared=True)
+    torch.cuda.synchronize()
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, gqa_shared=True)
+    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
+    ei, ec = orc.expand_gqa(oi, oc, Hq)
+    Oo, _ = orc.sparse_attention(Q, K, V, k, bq, bk, True, ei, ec, sink=32, window=128)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
