@@ -378,12 +378,16 @@ def ncu_traffic(kernel_key: str, config: str):
         return None
 
 
-def bench_decode(args, device):
-    """C3: one decode step (r_m = 1): paged mask estimation + paged sparse attention."""
+def bench_decode(args, device, T=None, options=True):
+    """C3: one decode step (r_m = 1): paged mask estimation + paged sparse attention (T = 128k, or
+    the given context length, e.g. 32k — BASELINE's decode metric is quoted at both)."""
     import torch
     from paper_2406_09827_b200 import hipattn as HA
     from paper_2406_09827_b200 import synth
-    c = DECODE
+    c = dict(DECODE)
+    if T is not None:
+        c["T"] = int(T)
+        c["workload"] = c["workload"].replace("T=128k", f"T={T // 1024}k")
     seq = [c["T"]] * c["B"]
     q = synth.gen_decode_q(c["B"], c["Hq"], c["d"], seed=args.seed, device=device)
     kp, vp, bt, sl = synth.gen_paged_direct(c["B"], c["Hkv"], seq, c["d"], c["page"], seed=args.seed, device=device)
@@ -434,7 +438,8 @@ def bench_decode(args, device):
     # appendix / NEXT options of the same step (different masks, not Alg. 1's per-head mask):
     # GQA-shared masks (reading G25) alone and with the stridden partial top-k (S = 4, G21)
     variants = {}
-    for name, ex in (("gqa_shared", dict(gqa_shared=True)), ("gqa_shared_chunks4", dict(gqa_shared=True, chunks=4))):
+    for name, ex in ((("gqa_shared", dict(gqa_shared=True)), ("gqa_shared_chunks4", dict(gqa_shared=True, chunks=4)))
+                     if options else ()):
         try:
             ti = torch.empty(c["B"], c["Hkv"], 1, n, dtype=torch.int32, device=device)
             tc = torch.empty(c["B"], c["Hkv"], 1, dtype=torch.int32, device=device)
@@ -459,7 +464,8 @@ def bench_decode(args, device):
                               "mask_gbs": round(mask_bytes / (c["Hq"] // c["Hkv"]) / (vmu * 1e-6) / 1e9, 1)}
         except Exception as e:  # noqa: BLE001 - an option failing must not hide the headline
             variants[name] = {"error": repr(e)}
-    res["options"] = variants
+    if options:
+        res["options"] = variants
     del kp, vp
     return res
 
@@ -584,6 +590,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_extras:
         try:
             extras["decode"] = bench_decode(args, device)
+            extras["decode_32k"] = bench_decode(args, device, T=32768, options=False)
         except Exception as e:  # noqa: BLE001 - report, do not hide the headline
             extras["decode"] = {"error": repr(e)}
         torch.cuda.empty_cache()

@@ -278,6 +278,9 @@ def hip_attention(q, k, v, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, 
                                     stream=stream)
 
 
+_HOST_CTX: dict = {}
+
+
 def hip_attention_host(q, k, v, out, *, k_budget: int = 512, b_q: int = 32, b_k: int = 2, causal: bool = True,
                        sm_scale=None, sink: int = 0, window: int = 0, device=None, kv_heads_per_chunk: int = 2):
     """One HiP prefill layer on PINNED HOST tensors q [B,Hq,T,d], k/v [B,Hkv,T,d] -> out (pinned host,
@@ -297,11 +300,24 @@ def hip_attention_host(q, k, v, out, *, k_budget: int = 512, b_q: int = 32, b_k:
     bq = max(1, min(int(b_q), Tq))
     nqb = (Tq + bq - 1) // bq
     n = k_budget // b_k
-    mk = lambda shape, dt: [torch.empty(shape, dtype=dt, device=device) for _ in range(2)]  # noqa: E731
-    Qd, Od = mk((B, G * ck, Tq, d), q.dtype), mk((B, G * ck, Tq, d), q.dtype)
-    Kd, Vd = mk((B, ck, Tk, d), k.dtype), mk((B, ck, Tk, d), v.dtype)
-    Id, Cd = mk((B, G * ck, nqb, n), torch.int32), mk((B, G * ck, nqb), torch.int32)
-    s_in, s_run, s_out = (torch.cuda.Stream(device) for _ in range(3))
+    key = (device, B, Hq, Hkv, Tq, Tk, d, q.dtype, k.dtype, ck, nqb, n)
+    ctx = _HOST_CTX.get(key)
+    if ctx is None:  # device buffers (double-buffered) and the three streams, reused across calls
+        mk = lambda shape, dt: [torch.empty(shape, dtype=dt, device=device) for _ in range(2)]  # noqa: E731
+        ctx = dict(Q=mk((B, G * ck, Tq, d), q.dtype), O=mk((B, G * ck, Tq, d), q.dtype),
+                   K=mk((B, ck, Tk, d), k.dtype), V=mk((B, ck, Tk, d), v.dtype),
+                   I=mk((B, G * ck, nqb, n), torch.int32), C=mk((B, G * ck, nqb), torch.int32),
+                   streams=tuple(torch.cuda.Stream(device) for _ in range(3)))
+        _HOST_CTX.clear()  # keep one configuration's buffers alive at a time
+        _HOST_CTX[key] = ctx
+    Qd, Od, Kd, Vd, Id, Cd = ctx["Q"], ctx["O"], ctx["K"], ctx["V"], ctx["I"], ctx["C"]
+    s_in, s_run, s_out = ctx["streams"]
+    # the previous call's work on these buffers must be finished before they are rewritten
+    cur = torch.cuda.current_stream(device)
+    for st_ in (s_in, s_run, s_out):
+        st_.wait_stream(cur)
+    s_in.wait_stream(s_out)
+    s_in.wait_stream(s_run)
     ev = lambda: torch.cuda.Event()  # noqa: E731
     run_done, out_done = [None, None], [None, None]
     with torch.cuda.device(device):
@@ -338,9 +354,4 @@ def hip_attention_host(q, k, v, out, *, k_budget: int = 512, b_q: int = 32, b_k:
                 out_done[i].record(s_out)
     done = ev()
     done.record(s_out)
-    # the caching allocator must not hand these buffers out again before the three streams are done
-    for bufs in (Qd, Kd, Vd, Od, Id, Cd):
-        for t in bufs:
-            for s_ in (s_in, s_run, s_out):
-                t.record_stream(s_)
     return done
