@@ -22,12 +22,14 @@
 // the tensor-core ridge; the kernel is bound by L2 gather latency (~1.2 us loaded, so ~128 KB must
 // be in flight per SM for the ~15 TB/s L2 gather ceiling) and by the selection's serial chain.
 //
-// Two launch shapes:
+// Launch shapes (the first is the default; the others are measured variants, profiles/r01/notes.md):
 //  * TEAMS = 1: one unit per 128-thread CTA, private 2-slot ring, 4 CTAs per SM.
-//  * TEAMS = 2 ("ping-pong"): a 256-thread CTA runs two units side by side, one per 128-thread team
-//    (named barriers), sharing ONE ring of SLOTS slots under a lock: a team holds the ring only while
-//    it gathers and scores, so while one team selects the other gathers with the whole ring — twice
-//    the bytes in flight per gathering unit at the same shared memory per SM.
+//  * TEAMS = 2, RINGS = 1 ("ping-pong", HIPATTN_MASK_TC=pp4/pp3): a 256-thread CTA runs two units
+//    side by side, one per 128-thread team (named barriers), sharing ONE ring of SLOTS slots under a
+//    lock: a team holds the ring only while it gathers and scores.  Slower (4.00 vs 3.43 ms at C2).
+//  * TEAMS = 5, RINGS = 5 (t5): five units per SM in one 640-thread CTA with private rings; capped at
+//    96 registers, slower (3.83 ms).
+//  * 3 slots x 3 CTAs (s3): deeper rings, fewer units; slower (3.97 ms).
 // TMA was measured and rejected for these gathers: one {64 x b_k} box per block (the only box shape
 // that lands in a UMMA layout) runs at ~half the cp.async rate (profiles/r01/notes.md).
 #include <type_traits>
