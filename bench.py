@@ -510,6 +510,16 @@ def cpu_baseline_prefill(cfg, budget_s: float, seed: int):
                       f"{tot_t:.1f}s of CPU work, extrapolated to {units} query blocks ({cfg['H']} heads)"}
 
 
+def config_obj(cfg, world):
+    """The `config` of the JSON line — identical for both arms."""
+    return {"workload": cfg["workload"], "model": "attention layer only", "global_batch": cfg["B"],
+            "seq_len": cfg["T"], "heads": cfg["H"], "head_dim": cfg["d"], "k": cfg["k"],
+            "b_q": cfg["bq"], "b_k": cfg["bk"], "causal": True, "dist": cfg["dist"],
+            "parallelism": f"heads/{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (Q,K,V,O = %.2f GB)" % (4 * cfg["B"] * cfg["H"] * cfg["T"] * cfg["d"] *
+                                                                (4 if cfg["dtype"] == "f32" else 2) / 1e9)}
+
+
 def reference_arm(args, cfg):
     """--impl reference: the CPU oracle on the box's host cores, same config/metric/unit."""
     W, K = args.warmup, args.steps
@@ -525,8 +535,7 @@ def reference_arm(args, cfg):
     return {"impl": "reference", "metric": "prefill_ms_per_layer", "value": round(v, 1), "unit": "ms",
             "higher_is_better": False, "n_gpus": args.gpus, "steps": K, "warmup": W,
             "ms_per_step": round(v, 1), "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
-            "data": "synthetic", "config": {"workload": cfg["workload"], "T": cfg["T"], "heads": cfg["H"],
-                                            "k": cfg["k"], "b_q": cfg["bq"], "b_k": cfg["bk"]},
+            "data": "synthetic", "config": config_obj(cfg, args.gpus),
             "cpu_baseline": base,
             "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -625,12 +634,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"], 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic",
-            "config": {"workload": cfg["workload"], "model": "attention layer only", "global_batch": cfg["B"],
-                       "seq_len": cfg["T"], "heads": cfg["H"], "head_dim": cfg["d"], "k": cfg["k"],
-                       "b_q": cfg["bq"], "b_k": cfg["bk"], "causal": True, "dist": cfg["dist"],
-                       "parallelism": f"heads/{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (Q,K,V,O = %.2f GB)" % (4 * cfg["B"] * cfg["H"] * cfg["T"] *
-                                                                           cfg["d"] * (4 if cfg["dtype"] == "f32" else 2) / 1e9)},
+            "config": config_obj(cfg, world),
             "mask_ms": round(r["mask_ms"], 4), "attn_ms": round(r["attn_ms"], 4),
             "e2e": ({"value": round(r["e2e_ms"], 3), "unit": "ms", "h2d_bytes_per_step": r["h2d"],
                      "d2h_bytes_per_step": r["d2h"],
