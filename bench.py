@@ -363,7 +363,30 @@ def roofline_obj(cfg, heads, mask_ms, attn_ms, pk, traffic=None):
                        "peak_source": "measured L2 random 512-B gather ceiling, profiles/r01/gather_ceiling.json",
                        "note": "algorithmic L2->SM gather of representative / selected key blocks; the "
                                "kernel's real bound (32 FLOP per gathered byte, DESIGN.md)"},
+            "hbm": {"algorithmic_gbs": round(gbytes / t / 1e9, 1),
+                    "dram_gbs": round(traffic / t / 1e9, 1) if traffic else None, "peak_gbs": pk["hbm_gbs"],
+                    "dram_frac": round(traffic / t / 1e9 / pk["hbm_gbs"], 4) if traffic else None,
+                    "note": "north_star's HBM view of the mask: algorithmic gather bytes / time (L2 hits can "
+                            "exceed the HBM peak) and the DRAM bytes ncu measured (traffic) / time"},
             "flops_per_launch": flops}
+
+
+def tensor_util(cfg, heads, mask_ms, attn_ms, pk):
+    """Tensor-pipe utilisation of the prefill layer (north_star): useful MMA FLOPs of mask + attention
+    over the layer time and the bf16 peak, with ncu's tensor-pipe-active % of each kernel."""
+    w = work_model(cfg, heads)
+    f = w["mask_flops"] + w["attn_flops"]
+    t = (mask_ms + attn_ms) / 1e3
+    res = {"layer_flops": f, "achieved_tflops": round(f / t / 1e12, 2), "peak_tflops": pk["bf16_tflops"],
+           "frac": round(f / t / 1e12 / pk["bf16_tflops"], 4)}
+    p = os.path.join(ROOT, "profiles", "r01", "ncu_c2_v4_summary.txt")
+    if os.path.exists(p):
+        import re
+        pct = re.findall(r"sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active\s+([0-9.]+)", open(p).read())
+        if len(pct) >= 2:
+            res["ncu_tensor_pipe_active_pct"] = {"mask": float(pct[0]), "attention": float(pct[1]),
+                                                 "source": "profiles/r01/ncu_c2_v4_summary.txt (C2)"}
+    return res
 
 
 def ncu_traffic(kernel_key: str, config: str):
@@ -643,6 +666,7 @@ def main():
                      "sequential_ms": round(r["e2e_seq_ms"], 3)} if r["e2e_ms"] is not None else None),
             "gpu_launches": 2 * args.steps,
             "roofline": roof,
+            "tensor_util": tensor_util(cfg, heads if world == 1 else r["heads_per_rank"], r["mask_ms"], r["attn_ms"], pk),
             "clocks": r["clocks"],
             "cpu_baseline": cpu,
         }
