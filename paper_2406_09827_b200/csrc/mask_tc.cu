@@ -63,7 +63,7 @@ struct RingShare {
   uint32_t* phases;  // bit s = parity to wait for on slot s's MMA barrier
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kGrp = false>
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kGrp = false, bool kRow1 = false>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
@@ -101,7 +101,7 @@ struct TCScorer {
   __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
     const int c = c0 + (i >> 1), h = i & 1;
     const int tid = Sync::tid(), c8 = tid & 7, r0 = tid >> 3;
-    if constexpr (!kPaged && NT == 128) {
+    if constexpr (NT == 128) {
       if (lbk == 1) {  // b_k = 2 (the paper's setting): thread (c8, g) owns the 8 consecutive rows 8g..8g+7
         issue_bk2(rep, n_rep, c, h, c8, r0, i);
         return;
@@ -128,20 +128,27 @@ struct TCScorer {
   }
 
   // b_k = 2: rows 8g..8g+7 of the tile are the 4 blocks 4g..4g+3, so one 16-byte load brings their
-  // representatives and the second row of a block is the first plus one row stride.  A warp
-  // instruction j still moves 4 whole 128-byte half rows (rows 8g + j, g = 4w..4w+3).
+  // representatives (and, paged, their pages) and the second row of a block is the first plus one
+  // row stride (a block never straddles a page).  A warp instruction j still moves 4 whole 128-byte
+  // half rows (rows 8g + j, g = 4w..4w+3).
   __device__ __forceinline__ void issue_bk2(const int* rep, int n_rep, int c, int h, int c8, int g, int i) {
     if (h == 0) {
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int4 rv = *reinterpret_cast<const int4*>(rep + blk0 + 4 * g);
       const int r4[4] = {rv.x, rv.y, rv.z, rv.w};
+      int p4[4] = {0, 0, 0, 0};
+      if constexpr (kPaged) {
+        const int4 pv = *reinterpret_cast<const int4*>(pg + blk0 + 4 * g);
+        p4[0] = pv.x; p4[1] = pv.y; p4[2] = pv.z; p4[3] = pv.w;
+      }
       rok = 0;
 #pragma unroll
       for (int b2 = 0; b2 < 4; ++b2) {
         const bool inb = 4 * g + b2 < nblk;
         const int s = inb ? r4[b2] << 1 : 0;
         const bool ok0 = inb && s < Tk, ok1 = inb && s + 1 < Tk;
-        rp[2 * b2] = row(ok0 ? s : 0) + c8 * 16;
+        if constexpr (kPaged) rp[2 * b2] = (ok0 ? paged_row(p4[b2], s) : ks.base) + c8 * 16;
+        else rp[2 * b2] = row(ok0 ? s : 0) + c8 * 16;
         rp[2 * b2 + 1] = rp[2 * b2] + (ok1 ? row_bytes : 0u);
         rok |= ((uint32_t)ok0 << (2 * b2)) | ((uint32_t)ok1 << (2 * b2 + 1));
       }
@@ -195,11 +202,21 @@ struct TCScorer {
     const int r = 32 * warp + lane, bm = (1 << lbk) - 1;
     for (int cc = 0; cc < nt; ++cc) {
       const int c = c0 + cc;
-      float v[32];
-      tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * warp) << 16) + 32 * cc, v);
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int lb = r >> lbk;
       float best = -INFINITY;
+      if constexpr (kRow1) {  // decode (rows_q == 1): one query row, one TMEM column per key
+        const float v0 = tmem_ld_32x32b_x1(tmem + ((uint32_t)(32 * warp) << 16) + 32 * cc);
+        if (lb < nblk) {
+          const int s = (rep[blk0 + lb] << lbk) + (r & bm);
+          if (s < Tk && (!causal || s <= tpos0)) best = v0;
+        }
+        for (int off = 1; off <= bm; off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
+        if (lb < nblk && (r & bm) == 0) out[blk0 + lb] = best;
+        continue;
+      }
+      float v[32];
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * warp) << 16) + 32 * cc, v);
       if (lb < nblk) {
         const int s = (rep[blk0 + lb] << lbk) + (r & bm);
         if (s < Tk) {
@@ -294,13 +311,14 @@ struct TCScorer {
 // one CTA — one CTA saves the per-CTA shared-memory reservation that keeps separate CTAs at 4).
 // EXT: the mask options, each a separate instantiation so that the plain Alg. 1 kernel (EXT = 0)
 // carries none of their code or registers: bit 0 ensemble split jitter (G23), bit 1 top-r (G22),
-// bit 2 GQA-shared rows (G25).
+// bit 2 GQA-shared rows (G25); bit 3 = one query row per unit (decode), whose epilogue reads a single
+// TMEM column per key.
 template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, int EXT, int RINGS = 1>
 __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
   constexpr int NT = 128;
-  constexpr bool kJit = (EXT & 1) != 0, kTopR = (EXT & 2) != 0, kGrp = (EXT & 4) != 0;
+  constexpr bool kJit = (EXT & 1) != 0, kTopR = (EXT & 2) != 0, kGrp = (EXT & 4) != 0, kRow1 = (EXT & 8) != 0;
   constexpr bool kSharedRing = TEAMS > 1 && RINGS == 1;
   constexpr uint32_t kColsUsed = 32 * TT * TEAMS;
   constexpr uint32_t kCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
@@ -410,7 +428,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp, kRow1> sc;
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0 + (RINGS > 1 ? team * L::ring_stride : 0u);
     sc.mbar = mbar;
@@ -472,7 +490,9 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
   // HIPATTN_MASK_TC selects a variant (tuning aid, profiles/r01).
   const int ext = (sh.jitter > 0 ? 1 : 0) | (sh.top_r > 0 ? 2 : 0) | (sh.group > 1 ? 4 : 0);
   switch (ext) {  // one instantiation per single option, one for combinations
-    case 0: break;
+    case 0:
+      if (sh.bq == 1) return launch_v<2, 4, 1, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);  // decode
+      break;
     case 1: return launch_v<2, 4, 1, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
     case 2: return launch_v<2, 4, 1, 4, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
     case 4: return launch_v<2, 4, 1, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
