@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     const int64_t lin = mask_lin(sh, b, h, q);  // the unit's mask row (GQA-shared: its group's, G25)
     const int rows_q = min(sh.bq, sh.Tq - q * sh.bq);
     const int64_t tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
+    const bool tail1 = rows_q == 1 && tpos0 >= Tk - 1;  // decode row at the end of its sequence
     const int nkb = (Tk + sh.bk - 1) / sh.bk;
     const int c = min(max(__ldg(cnt + lin), 0), sh.n);
     const int nkeys = c * sh.bk;
@@ -251,9 +252,13 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
             s = -1;
             extra = kSW && k >= nkeys;
             if (k < nkeys) {
-              const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
-              s = (j << lbk) + (k & ((1 << lbk) - 1));
-              if (s >= Tk) s = -1;
+              if (!kSW && tail1) {  // one row at the last position: every staged key is visible to it
+                s = tok[k] >= 0 ? (int)tpos0 : -1;
+              } else {
+                const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
+                s = (j << lbk) + (k & ((1 << lbk) - 1));
+                if (s >= Tk) s = -1;
+              }
             } else if (kSW && k < nall) {
               s = xlist[k - nkeys];
             }
@@ -268,6 +273,12 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         if (all_vis) {  // the common case: this key is visible to all 32 rows
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= scale_log2;
+        } else if (rows_q == 1) {  // decode: query column 0 only
+          const bool ok = s >= 0 && (!sh.causal || s <= tpos0) &&
+                          (!extra || extra_visible(s, tpos0, sh.causal, sh.sink, sh.window));
+          v[0] = ok ? v[0] * scale_log2 : -INFINITY;
+#pragma unroll
+          for (int j = 1; j < 32; ++j) v[j] = -INFINITY;
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
