@@ -161,6 +161,7 @@ hip::RowSrc make_paged(const hip_paged_kv_t& pg, const void* pages, int esz) {
   r.sp_rows = (pg.stride_t > 0 && pg.stride_page % pg.stride_t == 0) ? pg.stride_page / pg.stride_t : 0;
   for (int sh = 0; sh < 31; ++sh)
     if ((1 << sh) == pg.page_size) r.page_shift = sh;
+  r.bt16 = pg.num_pages > 0 && pg.num_pages <= 65536 && pg.max_pages_per_seq <= hip::kBt16Max;
   return r;
 }
 

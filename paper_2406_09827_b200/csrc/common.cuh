@@ -30,7 +30,10 @@ struct RowSrc {
   int64_t sp_rows;           // paged: sp / st when integral (page stride in rows), else 0
   int32_t paged;
   int32_t esize;             // bytes per element
+  int32_t bt16;              // paged: physical page ids fit 16 bits and a sequence's block-table row
+                             // fits kBt16Max entries (kernels may stage it in shared memory)
 };
+constexpr int kBt16Max = 3072;
 
 __device__ __forceinline__ const char* row_ptr(const RowSrc& r, int b, int hk, int64_t s) {
   if (!r.paged) return r.base + (b * r.sb + hk * r.sh + s * r.st) * r.esize;

@@ -46,14 +46,16 @@ constexpr uint32_t kMTSlot = 128 * 128;          // one item: 128 rows x 64 bf16
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
 // RINGS = 1 (one ring, shared by the teams when TEAMS > 1) or TEAMS (a private ring per team).
-template <int SLOTS, int TEAMS, int RINGS = 1>
+template <int SLOTS, int TEAMS, int RINGS = 1, bool PAGED = false>
 struct MaskTCSmemLayout {
   static constexpr uint32_t k0 = 0;                                        // ring(s) (1024-aligned)
   static constexpr uint32_t ring_stride = SLOTS * kMTSlot;
   static constexpr uint32_t q = k0 + RINGS * ring_stride;                  // [TEAMS] Q tiles
   static constexpr uint32_t sel = q + TEAMS * kQTileBytes;                 // [TEAMS] SelState
   static constexpr uint32_t sel_stride = (uint32_t)align_up(sizeof(SelState<kMTNmax, 4>), 128);
-  static constexpr uint32_t misc = sel + TEAMS * sel_stride;               // mbarriers, lock, ...
+  static constexpr uint32_t bt = sel + TEAMS * sel_stride;                 // [TEAMS] paged: block-table row
+  static constexpr uint32_t bt_stride = PAGED ? (uint32_t)align_up(kBt16Max * 2, 128) : 0u;  // uint16
+  static constexpr uint32_t misc = bt + TEAMS * bt_stride;                 // mbarriers, lock, ...
   static constexpr uint32_t total = misc + 128;
 };
 
@@ -81,6 +83,7 @@ struct TCScorer {
   int rph = 32;          // kGrp: rows per query head (GQA-shared, G25): row j sits at tpos0 + j % rph
   int64_t tpos0;
   const int* pg;         // paged: page of each representative block (aliases the score output)
+  const uint16_t* bt16 = nullptr;  // paged: the sequence's block-table row staged in shared memory
   const char* rp[RJ];    // this thread's source rows of the tile being issued
   uint32_t rok;          // bit j: rp[j] is a real row (< T_k, block < n_rep)
   uint32_t ckeep = 3u;   // top-r: bit h = this thread's chunk of d-half h has a kept component
@@ -255,7 +258,7 @@ struct TCScorer {
       for (int i = Sync::tid(); i < n_rep; i += NT) {
         const uint32_t s0 = (uint32_t)rep[i] << lbk;
         const uint32_t pi = ks.page_shift >= 0 ? (s0 >> ks.page_shift) : (s0 / (uint32_t)ks.page_size);
-        pgw[i] = __ldg(bt + pi);
+        pgw[i] = bt16 ? (int)bt16[pi] : __ldg(bt + pi);  // staged row: no global round trip
       }
       Sync::sync();
       pg = pgw;
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<SLOTS, TEAMS, RINGS>;
+  using L = MaskTCSmemLayout<SLOTS, TEAMS, RINGS, kPaged>;
   const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / NT);
   SelState<kMTNmax, 4>& st = *reinterpret_cast<SelState<kMTNmax, 4>*>(base + L::sel + team * L::sel_stride);
   uint64_t* mbar_all = reinterpret_cast<uint64_t*>(base + L::misc);
@@ -443,6 +446,15 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     sc.tpos0 = (int64_t)q * sh.bq + (Tk - sh.Tq);
     sc.rph = rph;
     sc.ckeep = ckeep;
+    if constexpr (kPaged) {
+      if (ks.bt16 && Bq > sh.n) {  // stage this sequence's block-table row (uint16) for the lookups
+        uint16_t* tb = reinterpret_cast<uint16_t*>(base + L::bt + team * L::bt_stride);
+        const int32_t* row = ks.block_table + (int64_t)b * ks.max_pages;
+        const int np = min(ks.max_pages, (Tk + ks.page_size - 1) / ks.page_size);
+        for (int i = Sync::tid(); i < np; i += NT) tb[i] = (uint16_t)__ldg(row + i);
+        sc.bt16 = tb;  // visible to the team after tree_search's first barrier
+      }
+    }
 #ifdef HIPATTN_PHASES
     sc.pt = &ptimer;
     ptimer.mark(7);  // unit setup / Q load / exact units
@@ -472,7 +484,8 @@ bool mask_tc_supported(const Shape& sh) {
 template <int SLOTS, int TT, int TEAMS, int MINB, int EXT = 0, int RINGS = 1>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
-  const size_t smem = MaskTCSmemLayout<SLOTS, TEAMS, RINGS>::total + 1024;
+  const size_t smem = (ks.paged ? MaskTCSmemLayout<SLOTS, TEAMS, RINGS, true>::total
+                                : MaskTCSmemLayout<SLOTS, TEAMS, RINGS, false>::total) + 1024;
   auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, EXT, RINGS>
                        : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, EXT, RINGS>;
   int per_sm = 1;
