@@ -65,7 +65,8 @@ struct RingShare {
   uint32_t* phases;  // bit s = parity to wait for on slot s's MMA barrier
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kGrp = false, bool kRow1 = false>
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kGrp = false, bool kRow1 = false,
+          bool kBk2 = false>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
@@ -84,7 +85,9 @@ struct TCScorer {
   int64_t tpos0;
   const int* pg;         // paged: page of each representative block (aliases the score output)
   const uint16_t* bt16 = nullptr;  // paged: the sequence's block-table row staged in shared memory
-  const char* rp[RJ];    // this thread's source rows of the tile being issued
+  // this thread's source rows of the tile being issued (kBk2: the first row of each of its 4 blocks;
+  // the second row is the first plus one row stride)
+  const char* rp[kBk2 ? 4 : RJ];
   uint32_t rok;          // bit j: rp[j] is a real row (< T_k, block < n_rep)
   uint32_t ckeep = 3u;   // top-r: bit h = this thread's chunk of d-half h has a kept component
                          // (else the chunk is zero-filled without a global read, topr.cuh)
@@ -104,12 +107,10 @@ struct TCScorer {
   __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
     const int c = c0 + (i >> 1), h = i & 1;
     const int tid = Sync::tid(), c8 = tid & 7, r0 = tid >> 3;
-    if constexpr (NT == 128) {
-      if (lbk == 1) {  // b_k = 2 (the paper's setting): thread (c8, g) owns the 8 consecutive rows 8g..8g+7
-        issue_bk2(rep, n_rep, c, h, c8, r0, i);
-        return;
-      }
-    }
+    if constexpr (kBk2) {  // b_k = 2 (the paper's setting): thread (c8, g) owns the 8 consecutive rows 8g..8g+7
+      issue_bk2(rep, n_rep, c, h, c8, r0, i);
+      return;
+    } else {
     if (h == 0) {
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int bmask = (1 << lbk) - 1;
@@ -128,6 +129,7 @@ struct TCScorer {
 #pragma unroll
     for (int j = 0; j < RJ; ++j)  // rows r0 + RPP j share r0's swizzle phase (RPP % 8 == 0)
       cp_async16(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
+    }
   }
 
   // b_k = 2: rows 8g..8g+7 of the tile are the 4 blocks 4g..4g+3, so one 16-byte load brings their
@@ -150,9 +152,8 @@ struct TCScorer {
         const bool inb = 4 * g + b2 < nblk;
         const int s = inb ? r4[b2] << 1 : 0;
         const bool ok0 = inb && s < Tk, ok1 = inb && s + 1 < Tk;
-        if constexpr (kPaged) rp[2 * b2] = (ok0 ? paged_row(p4[b2], s) : ks.base) + c8 * 16;
-        else rp[2 * b2] = row(ok0 ? s : 0) + c8 * 16;
-        rp[2 * b2 + 1] = rp[2 * b2] + (ok1 ? row_bytes : 0u);
+        if constexpr (kPaged) rp[b2] = (ok0 ? paged_row(p4[b2], s) : ks.base) + c8 * 16;
+        else rp[b2] = row(ok0 ? s : 0) + c8 * 16;
         rok |= ((uint32_t)ok0 << (2 * b2)) | ((uint32_t)ok1 << (2 * b2 + 1));
       }
     }
@@ -160,7 +161,8 @@ struct TCScorer {
     const uint32_t x = (uint32_t)c8;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      cp_async16(dst + j * 128 + ((x ^ j) << 4), rp[j] + h * 128, ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
+      cp_async16(dst + j * 128 + ((x ^ j) << 4), rp[j >> 1] + ((j & 1) ? row_bytes : 0u) + h * 128,
+                 ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
   }
 
   __device__ __forceinline__ void wait_slot(int slot) {
@@ -315,13 +317,14 @@ struct TCScorer {
 // EXT: the mask options, each a separate instantiation so that the plain Alg. 1 kernel (EXT = 0)
 // carries none of their code or registers: bit 0 ensemble split jitter (G23), bit 1 top-r (G22),
 // bit 2 GQA-shared rows (G25); bit 3 = one query row per unit (decode), whose epilogue reads a single
-// TMEM column per key.
+// TMEM column per key; bit 4 = b_k = 2, the gather mapping with 4 blocks per thread.
 template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, int EXT, int RINGS = 1>
 __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
   constexpr int NT = 128;
   constexpr bool kJit = (EXT & 1) != 0, kTopR = (EXT & 2) != 0, kGrp = (EXT & 4) != 0, kRow1 = (EXT & 8) != 0;
+  constexpr bool kBk2 = (EXT & 16) != 0;  // b_k = 2 gather mapping (the caller checked b_k == 2)
   constexpr bool kSharedRing = TEAMS > 1 && RINGS == 1;
   constexpr uint32_t kColsUsed = 32 * TT * TEAMS;
   constexpr uint32_t kCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp, kRow1> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp, kRow1, kBk2 && NT == 128> sc;
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0 + (RINGS > 1 ? team * L::ring_stride : 0u);
     sc.mbar = mbar;
@@ -504,7 +507,12 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
   const int ext = (sh.jitter > 0 ? 1 : 0) | (sh.top_r > 0 ? 2 : 0) | (sh.group > 1 ? 4 : 0);
   switch (ext) {  // one instantiation per single option, one for combinations
     case 0:
-      if (sh.bq == 1) return launch_v<2, 4, 1, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);  // decode
+      if (sh.bk == 2) {
+        if (sh.bq == 1) return launch_v<2, 4, 1, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);  // decode
+        if (!getenv("HIPATTN_MASK_TC")) return launch_v<2, 4, 1, 4, 16>(sh, qs, ks, idx, cnt, stream, num_sms);
+      } else if (sh.bq == 1) {
+        return launch_v<2, 4, 1, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);
+      }
       break;
     case 1: return launch_v<2, 4, 1, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
     case 2: return launch_v<2, 4, 1, 4, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
