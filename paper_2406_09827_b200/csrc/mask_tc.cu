@@ -72,8 +72,8 @@ struct TCScorer {
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
   static constexpr int RJ = 128 / RPP;      // rows per thread per tile
   uint32_t q_s, k_s0;
-  uint64_t* mbar;     // [SLOTS], MMA-completion barrier of each ring slot
-  uint32_t* phase;    // [SLOTS], this thread's copy
+  uint32_t mbar;      // shared address of [SLOTS] MMA-completion barriers, one per ring slot
+  uint32_t phase;     // bit s: the parity to wait for on slot s's barrier (this thread's copy)
   uint32_t pend = 0;  // slots whose MMA has been committed but not yet waited
   uint32_t tmem;      // this team's first accumulator column
   RingShare ring;
@@ -167,8 +167,8 @@ struct TCScorer {
 
   __device__ __forceinline__ void wait_slot(int slot) {
     if (pend & (1u << slot)) {
-      mbar_wait(mbar + slot, phase[slot]);
-      phase[slot] ^= 1u;
+      mbar_wait_u32(mbar + 8u * slot, (phase >> slot) & 1u);
+      phase ^= 1u << slot;
       pend &= ~(1u << slot);
     }
   }
@@ -181,9 +181,7 @@ struct TCScorer {
         __threadfence_block();
       }
       Sync::sync();
-      const uint32_t bits = *reinterpret_cast<volatile uint32_t*>(ring.phases);
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s) phase[s] = (bits >> s) & 1u;
+      phase = *reinterpret_cast<volatile uint32_t*>(ring.phases) & ((1u << SLOTS) - 1u);
     }
   }
   // Give the ring back once every MMA that read it has completed (pend == 0) and every thread of
@@ -192,10 +190,7 @@ struct TCScorer {
     if constexpr (kShared) {
       Sync::sync();
       if (Sync::tid() == 0) {
-        uint32_t bits = 0;
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) bits |= phase[s] << s;
-        *reinterpret_cast<volatile uint32_t*>(ring.phases) = bits;
+        *reinterpret_cast<volatile uint32_t*>(ring.phases) = phase;
         __threadfence_block();
         atomicExch(ring.lock, -1);
       }
@@ -287,7 +282,7 @@ struct TCScorer {
             uint64_t bq = smem_desc(q_s + h * (32 * 128) + s * 32, 16, 1024, kLayoutSw128);
             umma_bf16(tmem + 32 * cc, a, bq, kIdescS, (h | s) ? 1u : 0u);
           }
-          umma_commit(mbar + slot);
+          umma_commit_u32(mbar + 8u * slot);
         }
         pend |= 1u << slot;
         // refill this slot with item i + SLOTS as soon as MMA(i) has read it
@@ -357,9 +352,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot + 32 * TT * team;
-  uint32_t phase[SLOTS];
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s) phase[s] = 0u;
+  uint32_t phase = 0u;  // bit s: parity of ring slot s's barrier (carried across units)
   const int lbk = 31 - __clz(sh.bk);
 #ifdef HIPATTN_PHASES
   PhaseTimer ptimer;
@@ -437,7 +430,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp, kRow1, kBk2 && NT == 128> sc;
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0 + (RINGS > 1 ? team * L::ring_stride : 0u);
-    sc.mbar = mbar;
+    sc.mbar = smem_u32(mbar);
     sc.phase = phase;
     sc.tmem = tmem;
     sc.ring = RingShare{lock, ring_phases};
@@ -464,6 +457,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
 #endif
     tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
                                                  kJit ? make_jitter(sh.jitter, sh.seed, lin) : SplitJitter());
+    phase = sc.phase;
     if (cs == 0 && Sync::tid() == 0) cnt[lin] = min(Bq, sh.n);
     Sync::sync();
   }
