@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // S^T at columns [0, 32), O^T at [32, 64)
   const uint32_t tmem_lane = tmem + ((uint32_t)(32 * warp) << 16);
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phase = 0u;                  // bit s: parity of ring slot s's MMA barrier
+  const uint32_t mbar_a = smem_u32(mbar);  // shared address of the two barriers
   const int lbk = 31 - __clz(sh.bk);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
@@ -216,12 +217,12 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         }
       }
     };
-    bool pend[2] = {false, false};
+    uint32_t pend = 0u;  // bit s: slot s has an MMA committed but not yet waited
     auto wait_slot = [&](int sl) {
-      if (pend[sl]) {
-        mbar_wait(mbar + sl, phase[sl]);
-        phase[sl] ^= 1u;
-        pend[sl] = false;
+      if (pend & (1u << sl)) {
+        mbar_wait_u32(mbar_a + 8u * sl, (phase >> sl) & 1u);
+        phase ^= 1u << sl;
+        pend &= ~(1u << sl);
       }
     };
 
@@ -383,9 +384,9 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
             umma_bf16(tmem + 32, a, bp, kIdescPV, (ch > 0 || hk2 > 0 || s > 0) ? 1u : 0u);
           }
         }
-        umma_commit(mbar + (it & 1));
+        umma_commit_u32(mbar_a + 8u * (it & 1));
       }
-      pend[it & 1] = true;
+      pend |= 1u << (it & 1);
       // refill this slot with item it + 2 as soon as MMA(it) has read it (two items in flight)
       if (it + 2 < nitems) {
         wait_slot(it & 1);
