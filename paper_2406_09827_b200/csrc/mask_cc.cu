@@ -114,7 +114,7 @@ struct CCScorer {
 };
 
 template <typename T, int NMAX>
-__global__ void __launch_bounds__(kCCThreads, 4) mask_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(kCCThreads, 2) mask_cc_kernel(Shape sh, QSrc qsrc, RowSrc ks, int32_t* __restrict__ idx,
                                                                 int32_t* __restrict__ cnt, int ch, int kpitch,
                                                                 int stage_bytes) {
   extern __shared__ __align__(16) char smem[];
