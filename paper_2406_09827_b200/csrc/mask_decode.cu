@@ -113,7 +113,7 @@ struct LaneScorer {
 };
 
 template <typename T, int D, int NMAX, int RM, bool kPaged>
-__global__ void __launch_bounds__(kMDThreads, 4) mask_decode_kernel(Shape sh, QSrc qsrc, RowSrc ks,
+__global__ void __launch_bounds__(kMDThreads, 2) mask_decode_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                  int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) char smem[];
   SelState<NMAX, kMDThreads / 32>& st = *reinterpret_cast<SelState<NMAX, kMDThreads / 32>*>(smem);
