@@ -338,6 +338,35 @@ def dense_ms(Q, K, V, reps=3):
     return t0.elapsed_time(t1) / reps
 
 
+def dense_decode_us(kp, vp, bt, q, c):
+    """Measured dense decode of the same step: torch SDPA (GQA) over every cached token of every
+    sequence, on a contiguous copy of the paged cache (the copy is outside the timing)."""
+    import torch
+    import torch.nn.functional as F
+    try:
+        B, T, ps = c["B"], c["T"], c["page"]
+        npg = T // ps
+        rows = bt[:, :npg].long()
+        # [pages, Hkv, ps, d] -> per sequence [Hkv, T, d]
+        K = kp[rows].permute(0, 2, 1, 3, 4).reshape(B, c["Hkv"], T, c["d"])
+        V = vp[rows].permute(0, 2, 1, 3, 4).reshape(B, c["Hkv"], T, c["d"])
+        fn = lambda: F.scaled_dot_product_attention(q, K, V, enable_gqa=True)  # noqa: E731
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(10):
+            fn()
+        t1.record()
+        torch.cuda.synchronize()
+        us = 1e3 * t0.elapsed_time(t1) / 10
+        del K, V
+        return round(us, 1)
+    except Exception as e:  # noqa: BLE001 - a comparator must not hide the measurement
+        return repr(e)[:120]
+
+
 def l2_gather_peak() -> float:
     """Best measured random 512-byte L2->SMEM gather rate (GB/s) on this B200 pool
     (profiles/gather_bench.py); 16500 if the committed measurement is missing."""
@@ -456,6 +485,7 @@ def bench_decode(args, device, T=None, options=True):
                           "frac": round(attn_bytes / (attn_us * 1e-6) / 1e9 / pk["hbm_gbs"], 4),
                           "bytes_per_launch": attn_bytes},
         "dense_roofline_us": round(kv_bytes / (pk["hbm_gbs"] * 1e9) * 1e6, 1),
+        "dense_decode_us": dense_decode_us(kp, vp, bt, q, c),
         "step_bytes": mask_bytes + attn_bytes,
     }
     # appendix / NEXT options of the same step (different masks, not Alg. 1's per-head mask):
