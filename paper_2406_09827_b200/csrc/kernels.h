@@ -39,11 +39,12 @@ inline cudaError_t persistent_ctas(K kernel, int threads, size_t smem, int tmem_
   n = std::min(n, thr_sm / threads);
   if (tmem_cols > 0) n = std::min(n, 512 / tmem_cols);
   n = std::min(n, 32);
-  if (const char* cap = getenv("HIPATTN_CTAS_PER_SM")) n = std::min(n, atoi(cap));  // tuning aid
+#ifdef HIPATTN_TUNING  // profiling builds only: cap the residency, print the launch shape
+  if (const char* cap = getenv("HIPATTN_CTAS_PER_SM")) n = std::min(n, atoi(cap));
+  fprintf(stderr, "[hipattn] launch: threads=%d smem=%zu regs=%d -> %d CTAs/SM\n", threads, smem, fa.numRegs,
+          std::max(n, 1));
+#endif
   *per_sm = std::max(n, 1);
-  if (getenv("HIPATTN_VERBOSE"))
-    fprintf(stderr, "[hipattn] launch: threads=%d smem=%zu regs=%d -> %d CTAs/SM\n", threads, smem, fa.numRegs,
-            *per_sm);
   return cudaSuccess;
 }
 

@@ -3,7 +3,7 @@
 //
 // Block approximation makes every representative score a small dense contraction:
 // the b_q x d query block against the b_k x d rows of each representative key block.  Per iteration
-// a team of 128 threads gathers the (up to 2n, then n) representative key blocks of its query block,
+// a CTA of 128 threads gathers the (up to 2n, then n) representative key blocks of its query block,
 // 128 key rows per tile, straight from L2/HBM into 128-byte-swizzled K-major shared memory
 // (coalesced 16-byte cp.async, 8 threads per 128-byte half row, so every warp instruction moves
 // whole 32-byte sectors), and one thread issues
@@ -22,18 +22,11 @@
 // the tensor-core ridge; the kernel is bound by L2 gather latency (~1.2 us loaded, so ~128 KB must
 // be in flight per SM for the ~15 TB/s L2 gather ceiling) and by the selection's serial chain.
 //
-// Launch shapes (the first is the default; the others are measured variants, profiles/r01/notes.md):
-//  * TEAMS = 1: one unit per 128-thread CTA, private 2-slot ring, 4 CTAs per SM.
-//  * TEAMS = 2, RINGS = 1 ("ping-pong", HIPATTN_MASK_TC=pp4/pp3): a 256-thread CTA runs two units
-//    side by side, one per 128-thread team (named barriers), sharing ONE ring of SLOTS slots under a
-//    lock: a team holds the ring only while it gathers and scores.  Slower (4.00 vs 3.43 ms at C2).
-//  * TEAMS = 5, RINGS = 5 (t5): five units per SM in one 640-thread CTA with private rings; capped at
-//    96 registers, slower (3.83 ms).
-//  * 3 slots x 3 CTAs (s3): deeper rings, fewer units; slower (3.97 ms).
-// TMA was measured and rejected for these gathers: one {64 x b_k} box per block (the only box shape
-// that lands in a UMMA layout) runs at ~half the cp.async rate (profiles/r01/notes.md).
-#include <type_traits>
-
+// Launch shape: one unit (b, h, query block) per 128-thread CTA with a private 2-slot ring, 4 CTAs
+// per SM.  Round 1 measured and rejected deeper rings with fewer units (3 slots x 3 CTAs), two units
+// sharing one ring ("ping-pong") and five units per SM under a 96-register cap; TMA was measured and
+// rejected for these gathers as well: one {64 x b_k} box per block (the only box shape that lands
+// in a UMMA layout) runs at ~half the cp.async rate (profiles/r01/notes.md).
 #include "kernels.h"
 #include "select.cuh"
 #include "topr.cuh"
@@ -45,28 +38,18 @@ constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 r
 constexpr uint32_t kMTSlot = 128 * 128;          // one item: 128 rows x 64 bf16
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
-// RINGS = 1 (one ring, shared by the teams when TEAMS > 1) or TEAMS (a private ring per team).
-template <int SLOTS, int TEAMS, int RINGS = 1, bool PAGED = false>
+template <int SLOTS, bool PAGED = false>
 struct MaskTCSmemLayout {
-  static constexpr uint32_t k0 = 0;                                        // ring(s) (1024-aligned)
-  static constexpr uint32_t ring_stride = SLOTS * kMTSlot;
-  static constexpr uint32_t q = k0 + RINGS * ring_stride;                  // [TEAMS] Q tiles
-  static constexpr uint32_t sel = q + TEAMS * kQTileBytes;                 // [TEAMS] SelState
-  static constexpr uint32_t sel_stride = (uint32_t)align_up(sizeof(SelState<kMTNmax, 4>), 128);
-  static constexpr uint32_t bt = sel + TEAMS * sel_stride;                 // [TEAMS] paged: block-table row
-  static constexpr uint32_t bt_stride = PAGED ? (uint32_t)align_up(kBt16Max * 2, 128) : 0u;  // uint16
-  static constexpr uint32_t misc = bt + TEAMS * bt_stride;                 // mbarriers, lock, ...
-  static constexpr uint32_t total = misc + 128;
+  static constexpr uint32_t k0 = 0;                                        // ring (1024-aligned)
+  static constexpr uint32_t q = k0 + SLOTS * kMTSlot;                      // Q tile
+  static constexpr uint32_t sel = q + kQTileBytes;                         // SelState
+  static constexpr uint32_t bt = sel + (uint32_t)align_up(sizeof(SelState<kMTNmax, 4>), 128);
+  static constexpr uint32_t bt_bytes = PAGED ? (uint32_t)align_up(kBt16Max * 2, 128) : 0u;  // uint16 row
+  static constexpr uint32_t misc = bt + bt_bytes;                          // mbarriers, TMEM address
+  static constexpr uint32_t total = misc + 64;
 };
 
-// Shared ring state for TEAMS = 2 (lock word + the slots' mbarrier phase bits between owners).
-struct RingShare {
-  int* lock;         // -1 free, else owning team
-  uint32_t* phases;  // bit s = parity to wait for on slot s's MMA barrier
-};
-
-template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kShared, bool kGrp = false, bool kRow1 = false,
-          bool kBk2 = false>
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kGrp = false, bool kRow1 = false, bool kBk2 = false>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
@@ -75,8 +58,7 @@ struct TCScorer {
   uint32_t mbar;      // shared address of [SLOTS] MMA-completion barriers, one per ring slot
   uint32_t phase;     // bit s: the parity to wait for on slot s's barrier (this thread's copy)
   uint32_t pend = 0;  // slots whose MMA has been committed but not yet waited
-  uint32_t tmem;      // this team's first accumulator column
-  RingShare ring;
+  uint32_t tmem;      // the CTA's first accumulator column
   RowSrc ks;
   const char* kh;        // contiguous: row 0 of this (b, kv head)
   uint32_t row_bytes;    // contiguous: bytes between key rows
@@ -173,30 +155,6 @@ struct TCScorer {
     }
   }
 
-  // TEAMS = 2: take the ring (spin on the lock word) and the slots' barrier parities.
-  __device__ __forceinline__ void acquire() {
-    if constexpr (kShared) {
-      if (Sync::tid() == 0) {
-        while (atomicCAS(ring.lock, -1, 0) != -1) __nanosleep(64);
-        __threadfence_block();
-      }
-      Sync::sync();
-      phase = *reinterpret_cast<volatile uint32_t*>(ring.phases) & ((1u << SLOTS) - 1u);
-    }
-  }
-  // Give the ring back once every MMA that read it has completed (pend == 0) and every thread of
-  // the team is past its last cp.async wait.
-  __device__ __forceinline__ void release() {
-    if constexpr (kShared) {
-      Sync::sync();
-      if (Sync::tid() == 0) {
-        *reinterpret_cast<volatile uint32_t*>(ring.phases) = phase;
-        __threadfence_block();
-        atomicExch(ring.lock, -1);
-      }
-    }
-  }
-
   __device__ void epilogue(const int* rep, int n_rep, int c0, int nt, float* out) {
     const int warp = Sync::tid() >> 5, lane = threadIdx.x & 31;
     const int r = 32 * warp + lane, bm = (1 << lbk) - 1;
@@ -245,7 +203,6 @@ struct TCScorer {
 
   __device__ void score(const int* rep, int n_rep, float* out) {
     const int ntiles = (n_rep + bpt - 1) / bpt;
-    acquire();
     if constexpr (kPaged) {
       // one block-table lookup per representative block for the whole call (a block never straddles
       // a page), so the gathers below carry no dependent global load.  pg[i] is read only before
@@ -295,7 +252,6 @@ struct TCScorer {
       mark(1);  // gathers + MMA issue
 #pragma unroll
       for (int sl = 0; sl < SLOTS; ++sl) wait_slot(sl);  // drain the round's MMAs
-      if (c0 + TT >= ntiles) release();  // last round: the ring is free for the other team
       mark(2);  // MMA drain
       tc_fence_after();
       epilogue(rep, n_rep, c0, nt, out);
@@ -306,52 +262,43 @@ struct TCScorer {
   }
 };
 
-// TEAMS units per CTA (NT = 128 threads each); RINGS = 1 with TEAMS = 2 shares the ring (ping-pong,
-// see the header), RINGS = TEAMS gives every team a private ring (TEAMS = 5: five units per SM in
-// one CTA — one CTA saves the per-CTA shared-memory reservation that keeps separate CTAs at 4).
+// One unit per 128-thread CTA (persistent: CTAs stride over the units).
 // EXT: the mask options, each a separate instantiation so that the plain Alg. 1 kernel (EXT = 0)
 // carries none of their code or registers: bit 0 ensemble split jitter (G23), bit 1 top-r (G22),
 // bit 2 GQA-shared rows (G25); bit 3 = one query row per unit (decode), whose epilogue reads a single
 // TMEM column per key; bit 4 = b_k = 2, the gather mapping with 4 blocks per thread.
-template <int SLOTS, int TT, int TEAMS, bool kPaged, int MINB, int EXT, int RINGS = 1>
-__global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
+template <int SLOTS, int TT, bool kPaged, int MINB, int EXT>
+__global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
   constexpr int NT = 128;
   constexpr bool kJit = (EXT & 1) != 0, kTopR = (EXT & 2) != 0, kGrp = (EXT & 4) != 0, kRow1 = (EXT & 8) != 0;
   constexpr bool kBk2 = (EXT & 16) != 0;  // b_k = 2 gather mapping (the caller checked b_k == 2)
-  constexpr bool kSharedRing = TEAMS > 1 && RINGS == 1;
-  constexpr uint32_t kColsUsed = 32 * TT * TEAMS;
+  constexpr uint32_t kColsUsed = 32 * TT;
   constexpr uint32_t kCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
                              : kColsUsed <= 256 ? 256 : 512;  // allocation: a power of two
   static_assert(kColsUsed <= 512, "TMEM columns");
-  using Sync = typename std::conditional<TEAMS == 1, CtaSync, TeamSync<NT>>::type;
+  using Sync = CtaSync;
   extern __shared__ __align__(16) char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<SLOTS, TEAMS, RINGS, kPaged>;
-  const int team = TEAMS == 1 ? 0 : (int)(threadIdx.x / NT);
-  SelState<kMTNmax, 4>& st = *reinterpret_cast<SelState<kMTNmax, 4>*>(base + L::sel + team * L::sel_stride);
-  uint64_t* mbar_all = reinterpret_cast<uint64_t*>(base + L::misc);
-  uint64_t* mbar = mbar_all + (RINGS > 1 ? team * SLOTS : 0);  // this team's ring barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS * RINGS);
-  int* lock = reinterpret_cast<int*>(tmem_slot + 1);
-  uint32_t* ring_phases = tmem_slot + 2;
+  using L = MaskTCSmemLayout<SLOTS, kPaged>;
+  SelState<kMTNmax, 4>& st = *reinterpret_cast<SelState<kMTNmax, 4>*>(base + L::sel);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);  // one MMA-completion barrier per slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
   const int warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < SLOTS * RINGS; ++s) mbar_init(mbar_all + s, 1);
-    *lock = -1;
-    *ring_phases = 0u;
+    for (int s = 0; s < SLOTS; ++s) mbar_init(mbar + s, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<kCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot + 32 * TT * team;
+  const uint32_t tmem = *tmem_slot;
   uint32_t phase = 0u;  // bit s: parity of ring slot s's barrier (carried across units)
   const int lbk = 31 - __clz(sh.bk);
 #ifdef HIPATTN_PHASES
@@ -360,7 +307,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
 
   const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int S = max(sh.chunks, 1);
-  for (int64_t jb = (int64_t)blockIdx.x * TEAMS + team; jb < units * S; jb += (int64_t)gridDim.x * TEAMS) {
+  for (int64_t jb = blockIdx.x; jb < units * S; jb += gridDim.x) {
     const int64_t u = jb / S;
     const int cs = (int)(jb - u * S);
     int b, h, q;  // h: mask head (the kv head when GQA-shared, G25)
@@ -380,7 +327,7 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     };
     int lo, len, nn, slot0;
     if (!chunk_job(Bq, sh.n, S, cs, lo, len, nn, slot0)) continue;
-    const uint32_t q_s = sbase + L::q + team * kQTileBytes;
+    const uint32_t q_s = sbase + L::q;
     uint32_t ckeep = 3u;  // bit h: this thread's 16-byte key chunk of d-half h holds a kept component
     if (kTopR && Bq > sh.n && sh.top_r > 0 && sh.top_r < 128) {
       // top-r approximation (G22; topr.cuh): a_c = max_t |q_tc| (thread c), keep bits by
@@ -427,13 +374,12 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, kSharedRing, kGrp, kRow1, kBk2 && NT == 128> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, kGrp, kRow1, kBk2> sc;
     sc.q_s = q_s;
-    sc.k_s0 = sbase + L::k0 + (RINGS > 1 ? team * L::ring_stride : 0u);
+    sc.k_s0 = sbase + L::k0;
     sc.mbar = smem_u32(mbar);
     sc.phase = phase;
     sc.tmem = tmem;
-    sc.ring = RingShare{lock, ring_phases};
     sc.ks = ks;
     sc.kh = ks.base + (b * ks.sb + hk * ks.sh) * (int64_t)ks.esize;
     sc.row_bytes = (uint32_t)(ks.st * ks.esize);
@@ -444,11 +390,11 @@ __global__ void __launch_bounds__(128 * TEAMS, MINB) mask_tc_kernel(Shape sh, QS
     sc.ckeep = ckeep;
     if constexpr (kPaged) {
       if (ks.bt16 && Bq > sh.n) {  // stage this sequence's block-table row (uint16) for the lookups
-        uint16_t* tb = reinterpret_cast<uint16_t*>(base + L::bt + team * L::bt_stride);
+        uint16_t* tb = reinterpret_cast<uint16_t*>(base + L::bt);
         const int32_t* row = ks.block_table + (int64_t)b * ks.max_pages;
         const int np = min(ks.max_pages, (Tk + ks.page_size - 1) / ks.page_size);
         for (int i = Sync::tid(); i < np; i += NT) tb[i] = (uint16_t)__ldg(row + i);
-        sc.bt16 = tb;  // visible to the team after tree_search's first barrier
+        sc.bt16 = tb;  // visible to the CTA after tree_search's first barrier
       }
     }
 #ifdef HIPATTN_PHASES
@@ -478,47 +424,40 @@ bool mask_tc_supported(const Shape& sh) {
          sh.n <= kMTNmax;
 }
 
-template <int SLOTS, int TT, int TEAMS, int MINB, int EXT = 0, int RINGS = 1>
+template <int SLOTS, int TT, int MINB, int EXT>
 static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                             cudaStream_t stream, int num_sms) {
-  const size_t smem = (ks.paged ? MaskTCSmemLayout<SLOTS, TEAMS, RINGS, true>::total
-                                : MaskTCSmemLayout<SLOTS, TEAMS, RINGS, false>::total) + 1024;
-  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, TEAMS, true, MINB, EXT, RINGS>
-                       : mask_tc_kernel<SLOTS, TT, TEAMS, false, MINB, EXT, RINGS>;
+  const size_t smem = (ks.paged ? MaskTCSmemLayout<SLOTS, true>::total : MaskTCSmemLayout<SLOTS, false>::total) + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, true, MINB, EXT> : mask_tc_kernel<SLOTS, TT, false, MINB, EXT>;
   int per_sm = 1;
-  cudaError_t e = persistent_ctas(kern, 128 * TEAMS, smem, 32 * TT * TEAMS, &per_sm);
+  cudaError_t e = persistent_ctas(kern, 128, smem, 32 * TT, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int64_t jobs = units * std::max(sh.chunks, 1);
-  int64_t grid = std::min<int64_t>((jobs + TEAMS - 1) / TEAMS, (int64_t)num_sms * per_sm);
-  kern<<<(unsigned)grid, 128 * TEAMS, smem, stream>>>(sh, qs, ks, idx, cnt);
+  int64_t grid = std::min<int64_t>(jobs, (int64_t)num_sms * per_sm);
+  kern<<<(unsigned)grid, 128, smem, stream>>>(sh, qs, ks, idx, cnt);
   return cudaGetLastError();
 }
 
+// One instantiation per mask option (EXT bits above), so none inflates another's registers; the
+// b_k = 2 gather mapping (bit 4) and the single-row decode epilogue (bit 3) are specialisations of
+// Alg. 1 itself.  Dispatch depends on the arguments only.
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
-  // HIPATTN_MASK_TC selects a variant (tuning aid, profiles/r01).
   const int ext = (sh.jitter > 0 ? 1 : 0) | (sh.top_r > 0 ? 2 : 0) | (sh.group > 1 ? 4 : 0);
-  switch (ext) {  // one instantiation per single option, one for combinations
+  switch (ext) {
     case 0:
       if (sh.bk == 2) {
-        if (sh.bq == 1) return launch_v<2, 4, 1, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);  // decode
-        if (!getenv("HIPATTN_MASK_TC")) return launch_v<2, 4, 1, 4, 16>(sh, qs, ks, idx, cnt, stream, num_sms);
-      } else if (sh.bq == 1) {
-        return launch_v<2, 4, 1, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);
+        if (sh.bq == 1) return launch_v<2, 4, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);  // decode
+        return launch_v<2, 4, 4, 16>(sh, qs, ks, idx, cnt, stream, num_sms);
       }
-      break;
-    case 1: return launch_v<2, 4, 1, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
-    case 2: return launch_v<2, 4, 1, 4, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-    case 4: return launch_v<2, 4, 1, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
-    default: return launch_v<2, 4, 1, 4, 7>(sh, qs, ks, idx, cnt, stream, num_sms);
+      if (sh.bq == 1) return launch_v<2, 4, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);
+      return launch_v<2, 4, 4, 0>(sh, qs, ks, idx, cnt, stream, num_sms);
+    case 1: return launch_v<2, 4, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
+    case 2: return launch_v<2, 4, 4, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
+    case 4: return launch_v<2, 4, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+    default: return launch_v<2, 4, 4, 7>(sh, qs, ks, idx, cnt, stream, num_sms);
   }
-  const char* v = getenv("HIPATTN_MASK_TC");
-  if (v && !strcmp(v, "pp4")) return launch_v<4, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "s3")) return launch_v<3, 4, 1, 3>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "t5")) return launch_v<2, 3, 5, 1, 0, 5>(sh, qs, ks, idx, cnt, stream, num_sms);
-  if (v && !strcmp(v, "pp3")) return launch_v<3, 4, 2, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-  return launch_v<2, 4, 1, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
 }
 
 #ifdef HIPATTN_PHASES

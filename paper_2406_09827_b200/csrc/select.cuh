@@ -41,18 +41,10 @@ struct SelState {
   __device__ __forceinline__ float* scores() { return reinterpret_cast<float*>(nf); }
 };
 
-// Barrier scope of the selection: the whole CTA (one unit per CTA), or one 128-thread team of a
-// CTA that runs two units side by side (named barrier 1 + team; mask_tc.cu ping-pong).
+// Barrier scope of the selection: the whole CTA (one unit per CTA).
 struct CtaSync {
   static __device__ __forceinline__ void sync() { __syncthreads(); }
   static __device__ __forceinline__ int tid() { return threadIdx.x; }
-};
-template <int NT>
-struct TeamSync {
-  static __device__ __forceinline__ void sync() {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (int)(threadIdx.x / NT)), "n"(NT) : "memory");
-  }
-  static __device__ __forceinline__ int tid() { return threadIdx.x % NT; }
 };
 
 __device__ __forceinline__ uint32_t ord_score(float s) {

@@ -23,12 +23,19 @@ class HipDecoder:
     """Cached-mask HiP attention for one layer of a decoder (Alg. 2 lines 8-12)."""
 
     def __init__(self, r_m: int = 8, k_budget: int = 512, b_k: int = 2, b_q: int = 32, causal: bool = True,
-                 sink: int = 0, window: int = 0, sm_scale=None, gqa_shared: bool = False, chunks: int = 1):
-        """gqa_shared / chunks: the mask options of SURVEY §8 f3 — one mask per GQA group (reading
+                 sink: int = 32, window: int = 128, sm_scale=None, gqa_shared: bool = False, chunks: int = 1):
+        """sink / window: StreamingLLM sink and sliding-window tokens added to every row; the paper
+        fixes (window, sink) = (128, 32) for every experiment (SPEC's defaults too).  With
+        a cached mask (r_m > 1) the window is what covers the up to r_m - 1 tokens generated since
+        the last refresh and the current token itself, so it must span at least r_m tokens.
+        gqa_shared / chunks: the mask options of SURVEY §8 f3 — one mask per GQA group (reading
         G25) and the stridden partial top-k with S chunks (G21) — the low-latency decode
         configuration when the batch gives fewer units than the GPU has CTA slots."""
         if r_m < 1:
             raise ValueError("r_m must be >= 1")
+        if r_m > 1 and window < r_m:
+            raise ValueError(f"window={window} < r_m={r_m}: tokens generated since the last mask refresh "
+                             "(including the current one) would never be attended")
         self.r_m, self.k_budget, self.b_k, self.b_q = int(r_m), int(k_budget), int(b_k), int(b_q)
         self.causal, self.sink, self.window, self.sm_scale = bool(causal), int(sink), int(window), sm_scale
         self.gqa_shared, self.chunks = bool(gqa_shared), int(chunks)

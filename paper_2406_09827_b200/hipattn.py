@@ -126,6 +126,36 @@ def _require_cuda(*ts):
             raise ValueError("all tensors must be CUDA tensors (no CPU path)")
 
 
+def _same_as_q(q, **ts):
+    """The C ABI takes ONE dtype for q, k, v, o and the pages: every one must match q's dtype and
+    device (a mismatch would be read as the wrong element type)."""
+    for name, t in ts.items():
+        if t is None:
+            continue
+        if t.dtype != q.dtype:
+            raise TypeError(f"{name} is {t.dtype}, q is {q.dtype}: q, k, v, o (and pages) share one dtype")
+        if t.device != q.device:
+            raise ValueError(f"{name} is on {t.device}, q on {q.device}")
+
+
+def _int32_buffer(name, t, shape, device):
+    """idx / cnt buffers are read and written as contiguous int32 of exactly `shape`."""
+    if t.dtype != torch.int32:
+        raise TypeError(f"{name} must be int32, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+
+
+def _mask_shape(B, Hm, Tq, b_q, n):
+    bq = max(1, min(int(b_q), Tq))
+    nqb = (Tq + bq - 1) // bq
+    return (B, Hm, nqb, max(n, 1)), (B, Hm, nqb)
+
+
 def num_blocks(k: int, b_k: int) -> int:
     p = _params(k, 1, b_k, False)
     return int(load().hip_num_blocks(ctypes.byref(p)))
@@ -139,20 +169,21 @@ def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q:
     ensemble sample (combine with mask_vote); gqa_shared: one mask per kv head over the
     group's query heads (reading G25) -> idx [B, Hkv, Nqb, n]."""
     _require_cuda(q, k)
+    _same_as_q(q, k=k)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
     p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed,
                 gqa_shared=gqa_shared)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
-    bq = max(1, min(int(b_q), Tq))
-    nqb = (Tq + bq - 1) // bq
-    Hm = Hkv if gqa_shared else Hq
+    ishape, cshape = _mask_shape(B, Hkv if gqa_shared else Hq, Tq, b_q, n)
     if out is None:
-        idx = torch.empty((B, Hm, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
-        cnt = torch.empty((B, Hm, nqb), dtype=torch.int32, device=q.device)
+        idx = torch.empty(ishape, dtype=torch.int32, device=q.device)
+        cnt = torch.empty(cshape, dtype=torch.int32, device=q.device)
     else:
         idx, cnt = out
+        _int32_buffer("out idx", idx, ishape, q.device)
+        _int32_buffer("out cnt", cnt, cshape, q.device)
     with torch.cuda.device(q.device):
         _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, Tk, d, _desc(q), _desc(k), None,
                                      ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), None, 0, _stream(q, stream)))
@@ -167,8 +198,12 @@ def mask_vote(idx_samples: torch.Tensor, cnt_samples: torch.Tensor, *, theta: in
     _require_cuda(idx_samples, cnt_samples)
     if idx_samples.dtype != torch.int32 or cnt_samples.dtype != torch.int32:
         raise TypeError("int32 indices / counts")
+    if not (idx_samples.is_contiguous() and cnt_samples.is_contiguous()):
+        raise ValueError("idx_samples / cnt_samples must be contiguous")  # no temporaries freed under a kernel
+    if tuple(cnt_samples.shape) != tuple(idx_samples.shape[:-1]):
+        raise ValueError("cnt_samples must have idx_samples' shape without the last axis")
     lib = load()
-    I, C = idx_samples.contiguous(), cnt_samples.contiguous()
+    I, C = idx_samples, cnt_samples
     n_e, n = I.shape[0], I.shape[-1]
     lead = tuple(I.shape[1:-1])
     units = 1
@@ -191,10 +226,20 @@ def _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len: int) -> PagedKV
         raise ValueError("k_pages and v_pages must share strides")
     if block_table.dtype != torch.int32 or seq_lens.dtype != torch.int32:
         raise TypeError("block_table and seq_lens must be int32")
-    bt = block_table.contiguous()
+    # no contiguous() temporaries: a copy freed right after the enqueue could be reused by the
+    # allocator while the kernel (possibly on another stream) still reads it
+    if block_table.dim() != 2 or not block_table.is_contiguous():
+        raise ValueError("block_table must be a contiguous [B, max_pages_per_seq] int32 tensor")
+    if seq_lens.dim() != 1 or not seq_lens.is_contiguous():
+        raise ValueError("seq_lens must be a contiguous [B] int32 tensor")
+    if v_pages is not None and (v_pages.dtype != k_pages.dtype or v_pages.device != k_pages.device):
+        raise TypeError("k_pages and v_pages must share dtype and device")
+    for t in (block_table, seq_lens):
+        if t.device != k_pages.device:
+            raise ValueError("block_table / seq_lens must be on the pages' device")
     return PagedKV(k_pages.data_ptr(), v_pages.data_ptr() if v_pages is not None else None, k_pages.stride(0),
-                   k_pages.stride(1), k_pages.stride(2), bt.data_ptr(), seq_lens.data_ptr(), k_pages.shape[2],
-                   bt.shape[1], k_pages.shape[0], int(max_seq_len)), bt
+                   k_pages.stride(1), k_pages.stride(2), block_table.data_ptr(), seq_lens.data_ptr(),
+                   k_pages.shape[2], block_table.shape[1], k_pages.shape[0], int(max_seq_len))
 
 
 def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, k_budget: int = 512, b_q: int = 32,
@@ -202,26 +247,26 @@ def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, 
                         jitter: int = 0, seed: int = 0, gqa_shared: bool = False, out=None, stream=None):
     """hip_mask_estimate on a paged cache (decode: q [B,Hq,Tq,d], Tq rows at positions seq_len-Tq+t)."""
     _require_cuda(q, k_pages, block_table, seq_lens)
+    _same_as_q(q, k_pages=k_pages)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
     p = _params(k_budget, b_q, b_k, causal, exact=exact, chunks=chunks, top_r=top_r, jitter=jitter, seed=seed,
                 gqa_shared=gqa_shared)
     n = int(lib.hip_num_blocks(ctypes.byref(p)))
-    bq = max(1, min(int(b_q), Tq))
-    nqb = (Tq + bq - 1) // bq
-    pg, bt = _paged(k_pages, None, block_table, seq_lens, max_seq_len)
-    Hm = Hkv if gqa_shared else Hq
+    pg = _paged(k_pages, None, block_table, seq_lens, max_seq_len)
+    ishape, cshape = _mask_shape(B, Hkv if gqa_shared else Hq, Tq, b_q, n)
     if out is None:
-        idx = torch.empty((B, Hm, nqb, max(n, 1)), dtype=torch.int32, device=q.device)
-        cnt = torch.empty((B, Hm, nqb), dtype=torch.int32, device=q.device)
+        idx = torch.empty(ishape, dtype=torch.int32, device=q.device)
+        cnt = torch.empty(cshape, dtype=torch.int32, device=q.device)
     else:
         idx, cnt = out
+        _int32_buffer("out idx", idx, ishape, q.device)
+        _int32_buffer("out cnt", cnt, cshape, q.device)
     with torch.cuda.device(q.device):
         _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, int(max_seq_len), d, _desc(q),
                                      TensorDesc(None, 0, 0, 0), ctypes.byref(pg), ctypes.byref(p), idx.data_ptr(),
                                      cnt.data_ptr(), None, 0, _stream(q, stream)))
-    del bt
     return idx, cnt
 
 
@@ -231,10 +276,14 @@ def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int
     """hip_sparse_attention_prefill.  Returns o (and lse fp32 [B,Hq,Tq] if return_lse).  sink/window
     add StreamingLLM sink and sliding-window tokens to every row (the paper: 32 / 128)."""
     _require_cuda(q, k, v, idx, cnt)
+    _same_as_q(q, k=k, v=v, out=out)
     lib = load()
     B, Hq, Tq, d = q.shape
     _, Hkv, Tk, _ = k.shape
     p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window, gqa_shared=gqa_shared)
+    ishape, cshape = _mask_shape(B, Hkv if gqa_shared else Hq, Tq, b_q, int(lib.hip_num_blocks(ctypes.byref(p))))
+    _int32_buffer("idx", idx, ishape, q.device)
+    _int32_buffer("cnt", cnt, cshape, q.device)
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
     with torch.cuda.device(q.device):
@@ -251,11 +300,15 @@ def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_
     """hip_sparse_attention_decode on a paged cache.  q [B,Hq,Tq,d] -> o (and lse).  gqa_shared: idx/cnt
     hold one mask per kv head (mask_estimate_paged(..., gqa_shared=True))."""
     _require_cuda(q, k_pages, v_pages, block_table, seq_lens, idx, cnt)
+    _same_as_q(q, k_pages=k_pages, v_pages=v_pages, out=out)
     lib = load()
     B, Hq, Tq, d = q.shape
     Hkv = k_pages.shape[1]
     p = _params(k_budget, b_q, b_k, causal, sm_scale, sink=sink, window=window, gqa_shared=gqa_shared)
-    pg, bt = _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len)
+    ishape, cshape = _mask_shape(B, Hkv if gqa_shared else Hq, Tq, b_q, int(lib.hip_num_blocks(ctypes.byref(p))))
+    _int32_buffer("idx", idx, ishape, q.device)
+    _int32_buffer("cnt", cnt, cshape, q.device)
+    pg = _paged(k_pages, v_pages, block_table, seq_lens, max_seq_len)
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
     with torch.cuda.device(q.device):
@@ -263,7 +316,6 @@ def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_
                                                ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), _desc(o),
                                                lse.data_ptr() if lse is not None else None, None, 0,
                                                _stream(q, stream)))
-    del bt
     return (o, lse) if return_lse else o
 
 
@@ -308,7 +360,10 @@ def hip_attention_host(q, k, v, out, *, k_budget: int = 512, b_q: int = 32, b_k:
                    K=mk((B, ck, Tk, d), k.dtype), V=mk((B, ck, Tk, d), v.dtype),
                    I=mk((B, G * ck, nqb, n), torch.int32), C=mk((B, G * ck, nqb), torch.int32),
                    streams=tuple(torch.cuda.Stream(device) for _ in range(3)))
-        _HOST_CTX.clear()  # keep one configuration's buffers alive at a time
+        for old in _HOST_CTX.values():  # keep one configuration's buffers alive at a time: the old
+            for st_ in old["streams"]:    # buffers are freed only once their side streams are done
+                st_.synchronize()
+        _HOST_CTX.clear()
         _HOST_CTX[key] = ctx
     Qd, Od, Kd, Vd, Id, Cd = ctx["Q"], ctx["O"], ctx["K"], ctx["V"], ctx["I"], ctx["C"]
     s_in, s_run, s_out = ctx["streams"]

@@ -1,7 +1,8 @@
 """Experiment: does running the mask estimation of head group g+1 concurrently with the sparse
 attention of head group g (two streams) beat the sequential layer?  Profiling aid only.
 
-usage: HIPATTN_CTAS_PER_SM=<c> python profiles/overlap_exp.py [groups]"""
+usage: HIPATTN_CTAS_PER_SM=<c> python profiles/overlap_exp.py [groups]
+(needs a -DHIPATTN_TUNING build of the library: the product build reads no environment)"""
 import os
 import sys
 

@@ -160,6 +160,16 @@ def test_decoder_refresh_rule_host():
     import pytest
     with pytest.raises(ValueError):
         HipDecoder(r_m=0)
+    # the paper's (window, sink) = (128, 32) by default; a cached mask needs a window
+    # covering the tokens generated since the refresh
+    d = HipDecoder()
+    assert (d.r_m, d.window, d.sink) == (8, 128, 32)
+    with pytest.raises(ValueError):
+        HipDecoder(r_m=8, window=0, sink=0)
+    with pytest.raises(ValueError):
+        HipDecoder(r_m=8, window=7)
+    HipDecoder(r_m=8, window=8)
+    HipDecoder(r_m=1, window=0, sink=0)
 
 
 def test_params_struct_layout_matches_header(tmp_path):

@@ -696,22 +696,3 @@ def test_vote_max_size(orc):
         oi, oc = orc.vote(I, C, theta, tau)
         torch.cuda.synchronize()
         assert np.array_equal(gi.cpu().numpy(), oi) and np.array_equal(gc.cpu().numpy(), oc)
-
-
-@pytest.mark.parametrize("variant", ["pp4", "pp3", "s3", "t5"])
-def test_mask_tc_variants_bitexact(orc, variant, monkeypatch):
-    """The tuning variants of the tcgen05 mask kernel (HIPATTN_MASK_TC) compute the same masks:
-    bit-exact vs the oracle on integer inputs (prefill and paged decode)."""
-    monkeypatch.setenv("HIPATTN_MASK_TC", variant)
-    Q, K, _ = synth.gen_qkv(1, 3, 1, 3001, 3333, 128, "int", seed=99, dtype=torch.bfloat16, make_v=False)
-    gi, gc = _gpu_mask(Q, K, 256, 32, 2, True)
-    oi, oc = orc.mask(Q, K, 256, 32, 2, True)
-    _assert_mask_equal(gi, gc, oi, oc)
-    B, Hq, Hkv, d = 3, 4, 2, 128
-    seq = [4000, 50, 2500]
-    q = synth.gen_decode_q(B, Hq, d, seed=99, dist="int")
-    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, 64, seed=99, dist="int")
-    idx, cnt = H.mask_estimate_paged(q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), max(seq), k_budget=256, b_q=1, b_k=2)
-    torch.cuda.synchronize()
-    oi, oc = orc.mask_paged(q, kp, bt, sl, 256, 1, 2, True)
-    _assert_mask_equal(idx.cpu().numpy(), cnt.cpu().numpy(), oi, oc)
