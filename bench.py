@@ -4,17 +4,22 @@
 Contract (driver): `python bench.py --gpus N --steps K --warmup W` (torchrun for N > 1, one rank per
 GPU over NCCL) prints ONE JSON line from rank 0.  A step is one HiP attention layer on the
 headline workload: hip_mask_estimate + hip_sparse_attention_prefill over all heads (and, for
-N > 1, the NCCL all-gather of the head-sharded output).  Default workload: BASELINE.json
-configs[1] = C2, Llama-2-7B-shaped prefill (32 heads, d=128, T=32k, k=512, b_q=32, b_k=2, bf16,
-causal) on synthetic "llm"-structured inputs.
+N > 1, the NCCL all-gather of the head-sharded output, overlapped per head chunk).  Default
+workload: C4 = BASELINE.json configs[3], the Llama-2-13B-shaped prefill at T = 128k (40 heads, d=128,
+k=512, b_q=32, b_k=2, bf16, causal) that north_star's ">= 5x dense" target is stated at, on
+synthetic "llm"-structured inputs.  `--config c2` selects configs[1].
 
-  value        ms per layer (max over ranks, CUDA events on the launching stream), lower is better
+  value        ms per layer: sum over the K timed steps of CUDA-event device time on the launching
+               stream, max over ranks; the L2 is flushed (256 MB write) before every timed step
+  dense        the same layer as dense causal flash attention (torch SDPA) and the speedup
   e2e          the same through the public API with pinned HOST buffers: H2D of Q/K/V + the layer
                + D2H of O inside the timed region
   roofline     dominant kernel: algorithmic FLOPs / its mean event-timed duration vs the measured
                bf16 peak (MEASURED_PEAKS.json), plus its gather bandwidth (the real bound)
   cpu_baseline the CPU oracle on a bounded sample of the same layer, extrapolated (rank 0, N = 1)
-  extras (N=1) decode step at C3 (paged KV, 128k x 16 seqs) and the C4 128k prefill vs dense SDPA
+  extras (N=1) C2 32k layer; decode step at C3 (paged KV, 128k and 32k x 16 seqs; r_m = 1 kernels, and
+               the Alg. 2 loop HipDecoder measured at r_m = 1 and 8); mask quality
+  N > 1        also a decode line: C3 sharded by batch (16 / N sequences per rank) + O all-gather
 
 `--impl reference` runs the CPU oracle (the tier's reference arm) instead, on the same config.
 """
@@ -45,6 +50,8 @@ CONFIGS = {
 }
 DECODE = dict(workload="C3 Llama-3-8B-shaped GQA decode, paged KV T=128k, batch 16", B=16, Hq=32, Hkv=8, T=131072,
               d=128, k=512, bk=2, page=64, dtype="bf16")
+DEFAULT_CONFIG = "c4"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
 
 
@@ -172,6 +179,19 @@ def make_prefill_inputs(cfg, heads, seed, device):
     return Q, K, V
 
 
+def prefill_chunks(heads_per_rank: int, world: int) -> int:
+    """Head chunks per rank for N > 1: one head per chunk up to 8 heads per rank (each chunk's
+    all-gather overlaps the next chunk's kernels), else chunks of ~4 heads."""
+    if world == 1:
+        return 1
+    if heads_per_rank <= 8:
+        return heads_per_rank
+    for c in range(heads_per_rank // 4, heads_per_rank + 1):
+        if heads_per_rank % c == 0:
+            return c
+    return heads_per_rank
+
+
 def bench_prefill(cfg, args, rank, world, device, pg):
     import torch
     import torch.distributed as dist
@@ -179,7 +199,10 @@ def bench_prefill(cfg, args, rank, world, device, pg):
 
     from paper_2406_09827_b200 import dist as hd
 
-    hs = list(hd.head_range(cfg["H"], world, rank))  # heads shard (dist.py), no exchange in the hot loop
+    hpr = cfg["H"] // world
+    nch = prefill_chunks(hpr, world)
+    ranges = hd.head_chunks(cfg["H"], world, rank, nch)  # this rank's heads, chunk by chunk
+    hs = [h for r in ranges for h in r]
     Q, K, V = make_prefill_inputs(cfg, hs, args.seed, device)
     kw = dict(k_budget=cfg["k"], b_q=cfg["bq"], b_k=cfg["bk"], causal=True)
     O = torch.empty_like(Q)
@@ -188,22 +211,108 @@ def bench_prefill(cfg, args, rank, world, device, pg):
     idx = torch.empty(cfg["B"], len(hs), nqb, n, dtype=torch.int32, device=device)
     cnt = torch.empty(cfg["B"], len(hs), nqb, dtype=torch.int32, device=device)
     stream = torch.cuda.current_stream(device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    hc = hpr // nch
+    Ofull = torch.empty(cfg["B"], cfg["H"], cfg["T"], cfg["d"], dtype=Q.dtype, device=device) if world > 1 else None
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        HA.mask_estimate(Q, K, out=(idx, cnt), **kw)
-        if ev is not None:
-            ev[1].record(stream)
-        HA.sparse_attention_prefill(Q, K, V, idx, cnt, out=O, **kw)
+        if world == 1:
+            HA.mask_estimate(Q, K, out=(idx, cnt), **kw)
+            if ev is not None:
+                ev[1].record(stream)
+            HA.sparse_attention_prefill(Q, K, V, idx, cnt, out=O, **kw)
+        else:
+            # chunk c: mask + attention of this rank's heads [c h_c, (c+1) h_c), then its all-gather on
+            # a second stream while the next chunk computes (dist.ChunkGather)
+            gat = hd.ChunkGather(cfg["H"], out=Ofull)
+            for c in range(nch):
+                sl = slice(c * hc, (c + 1) * hc)
+                HA.mask_estimate(Q[:, sl], K[:, sl], out=(idx[:, sl], cnt[:, sl]), **kw)
+                if ev is not None and c == nch - 1:
+                    ev[1].record(stream)
+                HA.sparse_attention_prefill(Q[:, sl], K[:, sl], V[:, sl], idx[:, sl], cnt[:, sl], out=O[:, sl], **kw)
+                gat.push(c, O[:, sl])
+            gat.finish()
         if ev is not None:
             ev[2].record(stream)
-        if world > 1:
-            hd.gather_heads(O)  # the one collective: NCCL all-gather of the head shards over NVLink
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(device)
+
+    # K timed steps, each bracketed by CUDA events on the launching stream, with an untimed L2 flush
+    # before it; the step total is the sum of the per-step device times (max over ranks below)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    with ClockSampler(device.index) as clk:
+        for e in evs:
+            flush.fill_(1)
+            step(e)
+        torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(e[0].elapsed_time(e[2]) for e in evs)
+    if world == 1:
+        mask_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+        attn_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    else:  # per-kernel times of one chunked step (separate pass, events around each launch)
+        mask_ms = attn_ms = 0.0
+        for _ in range(2):
+            torch.cuda.synchronize(device)
+            t = [torch.cuda.Event(enable_timing=True) for _ in range(3 * nch)]
+            for c in range(nch):
+                sl = slice(c * hc, (c + 1) * hc)
+                t[3 * c].record(stream)
+                HA.mask_estimate(Q[:, sl], K[:, sl], out=(idx[:, sl], cnt[:, sl]), **kw)
+                t[3 * c + 1].record(stream)
+                HA.sparse_attention_prefill(Q[:, sl], K[:, sl], V[:, sl], idx[:, sl], cnt[:, sl], out=O[:, sl], **kw)
+                t[3 * c + 2].record(stream)
+            torch.cuda.synchronize(device)
+            mask_ms = sum(t[3 * c].elapsed_time(t[3 * c + 1]) for c in range(nch))
+            attn_ms = sum(t[3 * c + 1].elapsed_time(t[3 * c + 2]) for c in range(nch))
+
+    ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms, mask_ms, attn_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, mask_ms, attn_ms = t.tolist()
+        del Ofull
+
+    bytes_in = 3 * Q.numel() * Q.element_size()
+    bytes_out = O.numel() * O.element_size()
+    res = dict(ms=ms, mask_ms=mask_ms, attn_ms=attn_ms, e2e_ms=None, e2e_seq_ms=None, h2d=bytes_in * world,
+               d2h=bytes_out * world, clocks=clk.summary(), heads_per_rank=len(hs), chunks=nch,
+               tensors=(Q, K, V, O, idx, cnt))
+    if getattr(args, "no_e2e", False):
+        return res
+    # e2e through the public API with pinned host buffers
+    Qh = Q.cpu().pin_memory()
+    Kh = K.cpu().pin_memory()
+    Vh = V.cpu().pin_memory()
+    Oh = torch.empty(O.shape, dtype=O.dtype).pin_memory()
+    Qd, Kd, Vd = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
+    Og = torch.empty(cfg["B"], cfg["H"], cfg["T"], cfg["d"], dtype=Q.dtype).pin_memory() if world > 1 else None
+
+    def e2e_seq_step():
+        Qd.copy_(Qh, non_blocking=True)
+        Kd.copy_(Kh, non_blocking=True)
+        Vd.copy_(Vh, non_blocking=True)
+        o = HA.hip_attention(Qd, Kd, Vd, out=O, **kw)
+        if world > 1:  # the gathered layer output (chunk-major head order of this map) to the host
+            o = hd.gather_heads(o)
+            Og.copy_(o, non_blocking=True)
+        else:
+            Oh.copy_(o, non_blocking=True)
+
+    def e2e_pipe_step():
+        # the public host-memory entry point: heads streamed through the device in chunks, copies
+        # overlapping the kernels (hipattn.hip_attention_host)
+        done = HA.hip_attention_host(Qh, Kh, Vh, Oh, device=device, **kw)
+        stream.wait_event(done)
 
     def timed(fn_step, K_):
         if world > 1:
@@ -220,50 +329,6 @@ def bench_prefill(cfg, args, rank, world, device, pg):
             dist.barrier()
         return t0.elapsed_time(t1)
 
-    with ClockSampler(device.index) as clk:
-        total_ms = timed(step, args.steps)
-    # per-kernel durations (separate pass, events around each launch)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    torch.cuda.synchronize(device)
-    for e in evs:
-        step(e)
-    torch.cuda.synchronize(device)
-    mask_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    attn_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-
-    ms = total_ms / args.steps
-    if world > 1:
-        t = torch.tensor([ms, mask_ms, attn_ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, mask_ms, attn_ms = t.tolist()
-
-    bytes_in = 3 * Q.numel() * Q.element_size()
-    bytes_out = O.numel() * O.element_size()
-    if getattr(args, "no_e2e", False):
-        return dict(ms=ms, mask_ms=mask_ms, attn_ms=attn_ms, e2e_ms=None, h2d=bytes_in, d2h=bytes_out,
-                    clocks=clk.summary(), heads_per_rank=len(hs), tensors=(Q, K, V, O, idx, cnt))
-    # e2e through the public API with pinned host buffers
-    Qh = Q.cpu().pin_memory()
-    Kh = K.cpu().pin_memory()
-    Vh = V.cpu().pin_memory()
-    Oh = torch.empty(O.shape, dtype=O.dtype).pin_memory()
-    Qd, Kd, Vd = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
-
-    def e2e_seq_step():
-        Qd.copy_(Qh, non_blocking=True)
-        Kd.copy_(Kh, non_blocking=True)
-        Vd.copy_(Vh, non_blocking=True)
-        o = HA.hip_attention(Qd, Kd, Vd, out=O, **kw)
-        if world > 1:
-            hd.gather_heads(o)
-        Oh.copy_(o, non_blocking=True)
-
-    def e2e_pipe_step():
-        # the public host-memory entry point: heads streamed through the device in chunks, copies
-        # overlapping the kernels (hipattn.hip_attention_host)
-        done = HA.hip_attention_host(Qh, Kh, Vh, Oh, device=device, **kw)
-        stream.wait_event(done)
-
     e2e_step = e2e_pipe_step if world == 1 else e2e_seq_step
     e2e_step()
     torch.cuda.synchronize(device)
@@ -274,12 +339,10 @@ def bench_prefill(cfg, args, rank, world, device, pg):
         t = torch.tensor([e2e_ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = t.item()
-    bytes_in = 3 * Q.numel() * Q.element_size()
-    bytes_out = O.numel() * O.element_size()
+        res["d2h"] = Og.numel() * Og.element_size() * world
     del Qh, Kh, Vh, Qd, Kd, Vd
-    return dict(ms=ms, mask_ms=mask_ms, attn_ms=attn_ms, e2e_ms=e2e_ms, e2e_seq_ms=e2e_seq_ms, h2d=bytes_in,
-                d2h=bytes_out,
-                clocks=clk.summary(), heads_per_rank=len(hs), tensors=(Q, K, V, O, idx, cnt))
+    res.update(e2e_ms=e2e_ms, e2e_seq_ms=e2e_seq_ms)
+    return res
 
 
 def mask_quality(Q, K, idx, cnt, cfg, n_samples=64, seed=0):
@@ -400,21 +463,39 @@ def roofline_obj(cfg, heads, mask_ms, attn_ms, pk, traffic=None):
             "flops_per_launch": flops}
 
 
-def tensor_util(cfg, heads, mask_ms, attn_ms, pk):
+def latest_ncu_summary(cfg_name: str):
+    """The newest committed `ncu --set full` summary of this config (profiles/r02 before r01, highest
+    capture version first)."""
+    import glob
+    import re
+    best = None
+    for rnd in ("r02", "r01"):
+        for p in glob.glob(os.path.join(ROOT, "profiles", rnd, f"ncu_{cfg_name}_v*_summary.txt")):
+            m = re.search(r"_v(\d+)_summary", p)
+            v = int(m.group(1)) if m else 0
+            if best is None or (rnd, v) > best[:2]:
+                best = (rnd, v, p)
+        if best:
+            break
+    return best[2] if best else None
+
+
+def tensor_util(cfg, heads, mask_ms, attn_ms, pk, cfg_name):
     """Tensor-pipe utilisation of the prefill layer (north_star): useful MMA FLOPs of mask + attention
-    over the layer time and the bf16 peak, with ncu's tensor-pipe-active % of each kernel."""
+    over the layer time and the bf16 peak, with ncu's tensor-pipe-active % of each kernel from the
+    latest committed capture of this config."""
     w = work_model(cfg, heads)
     f = w["mask_flops"] + w["attn_flops"]
     t = (mask_ms + attn_ms) / 1e3
     res = {"layer_flops": f, "achieved_tflops": round(f / t / 1e12, 2), "peak_tflops": pk["bf16_tflops"],
            "frac": round(f / t / 1e12 / pk["bf16_tflops"], 4)}
-    p = os.path.join(ROOT, "profiles", "r01", "ncu_c2_v4_summary.txt")
-    if os.path.exists(p):
+    p = latest_ncu_summary(cfg_name)
+    if p:
         import re
         pct = re.findall(r"sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active\s+([0-9.]+)", open(p).read())
         if len(pct) >= 2:
             res["ncu_tensor_pipe_active_pct"] = {"mask": float(pct[0]), "attention": float(pct[1]),
-                                                 "source": "profiles/r01/ncu_c2_v4_summary.txt (C2)"}
+                                                 "source": os.path.relpath(p, ROOT)}
     return res
 
 
@@ -428,6 +509,90 @@ def ncu_traffic(kernel_key: str, config: str):
         return j.get(config, {}).get(kernel_key, {}).get("dram_bytes")
     except (ValueError, OSError):
         return None
+
+
+def time_hip_decoder(q, kp, vp, bt, c, device, steps=16):
+    """Alg. 2 measured: HipDecoder.step over `steps` consecutive decode steps, at r_m = 1
+    and the paper's default r_m = 8, with the paper's sink / window (32, 128).
+    Step t runs at sequence length T - steps + t + 1 (the cache holds T tokens), so an r_m = 8 run
+    refreshes the mask on every 8th step exactly as the loop would.  Per-step CUDA events on the
+    launching stream; the mean over the steps (one L2 flush before the run)."""
+    import torch
+    from paper_2406_09827_b200.decode import HipDecoder
+    st = torch.cuda.current_stream(device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    out = {}
+    T0 = c["T"] - steps
+    for r_m in (1, 8):
+        dec = HipDecoder(r_m=r_m, k_budget=c["k"], b_k=c["bk"], b_q=1)
+        lens = [T0 + 1 + t for t in range(steps)]
+        sls = [torch.full((c["B"],), L, dtype=torch.int32, device=device) for L in lens]
+        # warm-up on the first length (then reset so the timed run starts with a refresh)
+        dec.step(q, kp, vp, bt, sls[0], [lens[0]] * c["B"])
+        dec.idx = dec.cnt = None
+        dec.refreshes = 0
+        torch.cuda.synchronize(device)
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record(st)
+        for t in range(steps):
+            dec.step(q, kp, vp, bt, sls[t], [lens[t]] * c["B"])
+            ev[t + 1].record(st)
+        torch.cuda.synchronize(device)
+        per = [ev[t].elapsed_time(ev[t + 1]) * 1e3 for t in range(steps)]
+        out[f"r_m{r_m}"] = {"us_per_step": round(sum(per) / steps, 2), "refreshes": dec.refreshes, "steps": steps,
+                            "us_refresh_steps": round(statistics.mean(p for p, L in zip(per, lens) if L % r_m == 0 or r_m == 1), 2)
+                            if any(L % r_m == 0 for L in lens) else None,
+                            "us_cached_steps": round(statistics.mean(p for p, L in zip(per, lens) if L % r_m), 2)
+                            if r_m > 1 else None}
+    out["note"] = ("HipDecoder.step (decode.py): mask estimation when the length is divisible by r_m, then the "
+                   "paged sparse attention with sink 32 + window 128; seq lengths T-16+1..T")
+    return out
+
+
+def bench_decode_sharded(args, device, world, rank):
+    """N > 1: the C3 decode step sharded by batch (16 / N sequences per rank; dist.sharded_decode's
+    batch mode), each rank holding its sequences' paged cache, + the all-gather of O [16, 32, 1, 128].
+    Per-step CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_09827_b200 import dist as hd
+    from paper_2406_09827_b200 import hipattn as HA
+    from paper_2406_09827_b200 import synth
+    c = dict(DECODE)
+    br = hd.batch_range(c["B"], world, rank)
+    Bl = len(br)
+    q = synth.gen_decode_q(c["B"], c["Hq"], c["d"], seed=args.seed, device=device)[br.start:br.stop].contiguous()
+    kp, vp, bt, sl = synth.gen_paged_direct(Bl, c["Hkv"], [c["T"]] * Bl, c["d"], c["page"], seed=args.seed * 64 + rank,
+                                            device=device)
+    kw = dict(k_budget=c["k"], b_q=1, b_k=c["bk"], causal=True)
+    n = c["k"] // c["bk"]
+    idx = torch.empty(Bl, c["Hq"], 1, n, dtype=torch.int32, device=device)
+    cnt = torch.empty(Bl, c["Hq"], 1, dtype=torch.int32, device=device)
+    o = torch.empty_like(q)
+    st = torch.cuda.current_stream(device)
+
+    def step():
+        HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(idx, cnt), **kw)
+        HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], idx, cnt, out=o, **kw)
+        return hd.gather_batch(o)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize(device)
+    dist.barrier()
+    K_ = max(args.steps, 10)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(st)
+    for _ in range(K_):
+        step()
+    ev[1].record(st)
+    torch.cuda.synchronize(device)
+    dist.barrier()
+    t = torch.tensor([ev[0].elapsed_time(ev[1]) * 1e3 / K_], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"workload": c["workload"], "r_m": 1, "us_per_step": round(t.item(), 2),
+            "sharding": f"batch/{world} ({Bl} sequences per rank)", "gather": "NCCL all-gather of O along batch"}
 
 
 def bench_decode(args, device, T=None, options=True):
@@ -475,7 +640,6 @@ def bench_decode(args, device, T=None, options=True):
     res = {
         "workload": c["workload"], "r_m": 1,
         "us_per_step": round(mask_us + attn_us, 2), "mask_us": round(mask_us, 2), "attn_us": round(attn_us, 2),
-        "us_per_step_r_m8": round(attn_us + mask_us / 8, 2),
         "us_per_sequence": round((mask_us + attn_us) / c["B"], 3),
         "roofline": {"kernel": "mask_estimate (paged, b_q=1)", "bound": "hbm",
                      "achieved": round(mask_bytes / (mask_us * 1e-6) / 1e9, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -488,6 +652,7 @@ def bench_decode(args, device, T=None, options=True):
         "dense_decode_us": dense_decode_us(kp, vp, bt, q, c),
         "step_bytes": mask_bytes + attn_bytes,
     }
+    res["hip_decoder"] = time_hip_decoder(q, kp, vp, bt, c, device, steps=max(16, args.steps))
     # appendix / NEXT options of the same step (different masks, not Alg. 1's per-head mask):
     # GQA-shared masks (reading G25) alone and with the stridden partial top-k (S = 4, G21)
     variants = {}
@@ -563,14 +728,15 @@ def cpu_baseline_prefill(cfg, budget_s: float, seed: int):
                       f"{tot_t:.1f}s of CPU work, extrapolated to {units} query blocks ({cfg['H']} heads)"}
 
 
-def config_obj(cfg, world):
+def config_obj(cfg, world, chunks=1):
     """The `config` of the JSON line — identical for both arms."""
     return {"workload": cfg["workload"], "model": "attention layer only", "global_batch": cfg["B"],
             "seq_len": cfg["T"], "heads": cfg["H"], "head_dim": cfg["d"], "k": cfg["k"],
             "b_q": cfg["bq"], "b_k": cfg["bk"], "causal": True, "dist": cfg["dist"],
-            "parallelism": f"heads/{world}" if world > 1 else "single GPU",
-            "l2": "inputs larger than L2 (Q,K,V,O = %.2f GB)" % (4 * cfg["B"] * cfg["H"] * cfg["T"] * cfg["d"] *
-                                                                (4 if cfg["dtype"] == "f32" else 2) / 1e9)}
+            "parallelism": (f"heads/{world}, {chunks} head chunks per rank, all-gather per chunk overlapped"
+                            if world > 1 else "single GPU"),
+            "l2": "L2 flushed (256 MB write, untimed) before every timed step; inputs larger than L2 (Q,K,V,O = "
+                  "%.2f GB)" % (4 * cfg["B"] * cfg["H"] * cfg["T"] * cfg["d"] * (4 if cfg["dtype"] == "f32" else 2) / 1e9)}
 
 
 def reference_arm(args, cfg):
@@ -588,9 +754,31 @@ def reference_arm(args, cfg):
     return {"impl": "reference", "metric": "prefill_ms_per_layer", "value": round(v, 1), "unit": "ms",
             "higher_is_better": False, "n_gpus": args.gpus, "steps": K, "warmup": W,
             "ms_per_step": round(v, 1), "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
-            "data": "synthetic", "config": config_obj(cfg, args.gpus),
+            "data": "synthetic", "config": config_obj(cfg, args.gpus, prefill_chunks(cfg["H"] // args.gpus, args.gpus)),
             "cpu_baseline": base,
             "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def prefill_extra(cfg_name, args, device, pk):
+    """Another prefill config at N = 1 (the C2 32k layer beside the C4 headline): layer ms, kernels,
+    dense SDPA, speedup, mask quality, roofline with the committed ncu traffic."""
+    import torch
+    a2 = argparse.Namespace(**vars(args))
+    a2.no_e2e = True
+    a2.steps = max(3, min(args.steps, 10))
+    c = CONFIGS[cfg_name]
+    r = bench_prefill(c, a2, 0, 1, device, None)
+    Q, K, V = r["tensors"][:3]
+    qual = mask_quality(Q, K, r["tensors"][4], r["tensors"][5], c)
+    dn = dense_ms(Q, K, V, reps=3)
+    traffic = ncu_traffic("mask_estimate" if r["mask_ms"] >= r["attn_ms"] else "sparse_attention_prefill", cfg_name)
+    out = {"workload": c["workload"], "ms": round(r["ms"], 4), "mask_ms": round(r["mask_ms"], 4),
+           "attn_ms": round(r["attn_ms"], 4), "dense_sdpa_ms": round(dn, 3), "speedup_vs_dense": round(dn / r["ms"], 2),
+           "mask_quality": qual, "roofline": roofline_obj(c, c["H"], r["mask_ms"], r["attn_ms"], pk, traffic),
+           "tensor_util": tensor_util(c, c["H"], r["mask_ms"], r["attn_ms"], pk, cfg_name)}
+    del Q, K, V, r
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -601,7 +789,7 @@ def main():
     ap.add_argument("--impl", default="hip", choices=["hip", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--no-extras", action="store_true", help="skip the decode / 128k extras")
+    ap.add_argument("--no-extras", action="store_true", help="skip the decode / C2 extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--decode-only", action="store_true", help="only the C3 decode step (profiling aid)")
     ap.add_argument("--no-e2e", action="store_true",
@@ -612,7 +800,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg_name = args.config or "c2"
+    cfg_name = args.config or DEFAULT_CONFIG
     cfg = CONFIGS[cfg_name]
 
     if args.impl == "reference":
@@ -633,19 +821,20 @@ def main():
         print(json.dumps(bench_decode(args, device)), flush=True)
         return
     r = bench_prefill(cfg, args, rank, world, device, pg)
-    heads = r["heads_per_rank"] * world
     pk = peaks()
     traffic = ncu_traffic("mask_estimate" if r["mask_ms"] >= r["attn_ms"] else "sparse_attention_prefill", cfg_name)
-    roof = roofline_obj(cfg, heads, r["mask_ms"] * world / world, r["attn_ms"], pk, traffic)
-    if world > 1:  # per-rank kernels process heads/world heads
-        roof = roofline_obj(cfg, r["heads_per_rank"], r["mask_ms"], r["attn_ms"], pk, traffic)
+    # per-rank kernels process heads/world heads (world = 1: all heads)
+    roof = roofline_obj(cfg, r["heads_per_rank"], r["mask_ms"], r["attn_ms"], pk, traffic if world == 1 else None)
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
         Q, K, V = r["tensors"][:3]
         extras["mask_quality"] = mask_quality(Q, K, r["tensors"][4], r["tensors"][5], cfg)
-        extras["dense_sdpa_ms"] = round(dense_ms(Q, K, V), 3)
-        extras["speedup_vs_dense"] = round(extras["dense_sdpa_ms"] / r["ms"], 2)
+        del Q, K, V
+    dense = None
+    if rank == 0 and world == 1 and cfg_name != "c5":
+        Q, K, V = r["tensors"][:3]
+        dense = dense_ms(Q, K, V, reps=3)
         del Q, K, V
     r["tensors"] = None
     torch.cuda.empty_cache()
@@ -656,26 +845,19 @@ def main():
         except Exception as e:  # noqa: BLE001 - report, do not hide the headline
             extras["decode"] = {"error": repr(e)}
         torch.cuda.empty_cache()
-        if cfg_name != "c4":
-            try:
-                a2 = argparse.Namespace(**vars(args))
-                a2.no_e2e = True
-                a2.steps = 3
-                a2.warmup = 3
-                c4 = CONFIGS["c4"]
-                r4 = bench_prefill(c4, a2, 0, 1, device, None)
-                Q, K, V = r4["tensors"][:3]
-                q4 = mask_quality(Q, K, r4["tensors"][4], r4["tensors"][5], c4)
-                d4 = dense_ms(Q, K, V, reps=2)
-                extras["c4_128k"] = {"workload": c4["workload"], "ms": round(r4["ms"], 3),
-                                     "mask_ms": round(r4["mask_ms"], 3), "attn_ms": round(r4["attn_ms"], 3),
-                                     "dense_sdpa_ms": round(d4, 3), "speedup_vs_dense": round(d4 / r4["ms"], 2),
-                                     "mask_quality": q4,
-                                     "roofline": roofline_obj(c4, c4["H"], r4["mask_ms"], r4["attn_ms"], pk)}
-                del Q, K, V, r4
-            except Exception as e:  # noqa: BLE001
-                extras["c4_128k"] = {"error": repr(e)}
-            torch.cuda.empty_cache()
+        other = "c2" if cfg_name != "c2" else "c4"
+        try:
+            extras[{"c2": "c2_32k", "c4": "c4_128k"}[other]] = prefill_extra(other, args, device, pk)
+        except Exception as e:  # noqa: BLE001
+            extras[other] = {"error": repr(e)}
+        torch.cuda.empty_cache()
+    if world > 1 and not args.no_extras:
+        try:
+            dec = bench_decode_sharded(args, device, world, rank)
+        except Exception as e:  # noqa: BLE001
+            dec = {"error": repr(e)}
+        if rank == 0:
+            extras["decode"] = dec
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -687,16 +869,18 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"], 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic",
-            "config": config_obj(cfg, world),
+            "config": config_obj(cfg, world, r.get("chunks", 1)),
             "mask_ms": round(r["mask_ms"], 4), "attn_ms": round(r["attn_ms"], 4),
+            "dense_sdpa_ms": round(dense, 3) if dense else None,
+            "speedup_vs_dense": round(dense / r["ms"], 2) if dense else None,
             "e2e": ({"value": round(r["e2e_ms"], 3), "unit": "ms", "h2d_bytes_per_step": r["h2d"],
                      "d2h_bytes_per_step": r["d2h"],
                      "api": "hipattn.hip_attention_host (pinned host in/out, copies overlapped with the kernels)"
                      if world == 1 else "hipattn.hip_attention + NCCL gather (pinned host in/out)",
                      "sequential_ms": round(r["e2e_seq_ms"], 3)} if r["e2e_ms"] is not None else None),
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 2 * args.steps * r.get("chunks", 1),
             "roofline": roof,
-            "tensor_util": tensor_util(cfg, heads if world == 1 else r["heads_per_rank"], r["mask_ms"], r["attn_ms"], pk),
+            "tensor_util": tensor_util(cfg, r["heads_per_rank"], r["mask_ms"], r["attn_ms"], pk, cfg_name),
             "clocks": r["clocks"],
             "cpu_baseline": cpu,
         }

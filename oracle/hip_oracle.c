@@ -55,6 +55,7 @@
 #define ORC_EINVAL 1
 #define ORC_ENOMEM 2
 #define ORC_ERANGE 3
+#define ORC_EREPLAY 4 /* replay: the search asked for a block score that was not supplied */
 
 #define ORC_F32C 0
 #define ORC_F64 1
@@ -81,6 +82,7 @@ typedef struct {
     uint64_t key;    /* per-unit generator key (orc_unit_key) */
     int G;           /* query heads scored together (GQA-shared mask, G25); 1 = one head */
     int64_t hstride; /* floats between the Q rows of consecutive heads of the group */
+    int replay;      /* 1: scores come only from the caller-filled memo (oracle_mask_replay) */
 } orc_ext;
 
 /* splitmix64 output function (Steele, Lea & Flood 2014): the counter-based generator of the
@@ -327,6 +329,10 @@ static int search_range(const float *Qh, const float *Kh, int Tq, int Tk, int d,
         for (int c = 0; c < nc; ++c) {
             int64_t r = cand[c].f; /* representative = first block of the branch */
             if (isnan(memo[r])) {
+                if (ex->replay) { /* replay: every score must have been supplied */
+                    free(nodes); free(cand); free(firsts);
+                    return ORC_EREPLAY;
+                }
                 double e = 0.0;
                 memo[r] = block_score_c(Qh, Kh, t0, t1, r, bk, Tq, Tk, d, causal, mode, ex->comp, ex->ncomp, ex->G,
                                         ex->hstride, &e);
@@ -385,7 +391,7 @@ static int mask_unit_chunked(const float *Qh, const float *Kh, int Tq, int Tk, i
     double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
     if (!memo) return ORC_ENOMEM;
     int comp[1024];
-    orc_ext ex = {NULL, d, R > 0 ? R : 0, 0, G, (int64_t)Tq * d};
+    orc_ext ex = {NULL, d, R > 0 ? R : 0, 0, G, (int64_t)Tq * d, 0};
     if (top_r > 0 && top_r < d) { /* top-r approximation */
         if (d > 1024) { free(memo); return ORC_EINVAL; }
         top_r_components(Qh, t0, t1, G, (int64_t)Tq * d, d, top_r, comp);
@@ -413,6 +419,58 @@ static int mask_unit(const float *Qh, const float *Kh, int Tq, int Tk, int d, in
 {
     return mask_unit_chunked(Qh, Kh, Tq, Tk, d, q, n, bq, bk, causal, mode, 1, out_idx, out_cnt, diag,
                              trace_nodes, trace_scores, max_trace, 0, 0, 0, 0, 1);
+}
+
+/* Replay (test infrastructure): Alg. 1's split / rank / keep steps (search_range,
+ * unchanged) driven by SUPPLIED branch scores instead of computed ones — scores[u][j] is the score of
+ * key block j for the u-th listed query block q_of_unit[u] (NaN = not supplied; asking for one is
+ * ORC_EREPLAY).  Fed the GPU's own fp32 scores, it checks the GPU's splitting, inheritance, top-n and
+ * tie rule independently of how the scores were rounded.  Plain Alg. 1 only (no chunks / options).
+ * trace_nodes (optional, [nunits][max_trace + 1][n][2]) receives every unit's node ranges per
+ * iteration (row 0 = initial partition), as oracle_mask_trace does. */
+int oracle_mask_replay(int Tq, int Tk, int k, int bq, int bk, int causal, int64_t nunits, const int64_t *q_of_unit,
+                       const float *scores, int64_t nkb, int32_t *idx, int32_t *cnt, int32_t *trace_nodes,
+                       int max_trace)
+{
+    if (Tq < 1 || Tk < 1 || bq < 1 || bk < 1 || k < bk || k % bk || (causal && Tq > Tk)) return ORC_EINVAL;
+    int n = k / bk;
+    int64_t nqb = ((int64_t)Tq + bq - 1) / bq;
+    int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t u = 0; u < nunits; ++u) {
+        int64_t q = q_of_unit[u];
+        int r = ORC_OK;
+        if (q < 0 || q >= nqb) {
+            r = ORC_ERANGE;
+        } else {
+            int64_t Bq = visible_blocks(q, bq, bk, Tq, Tk, causal);
+            if (Bq > nkb) {
+                r = ORC_ERANGE;
+            } else if (Bq <= n) { /* exact case: no score involved */
+                for (int64_t j = 0; j < n; ++j) idx[u * n + j] = j < Bq ? (int32_t)j : -1;
+                cnt[u] = (int32_t)Bq;
+            } else {
+                double *memo = (double *)malloc(sizeof(double) * (size_t)Bq);
+                if (!memo) {
+                    r = ORC_ENOMEM;
+                } else {
+                    for (int64_t j = 0; j < Bq; ++j) memo[j] = (double)scores[u * nkb + j];
+                    orc_ext ex = {NULL, 0, 0, 0, 1, 0, 1};
+                    orc_diag dg = {INFINITY, 0.0, 0, 0};
+                    int32_t *tn = trace_nodes ? trace_nodes + (size_t)u * (size_t)(max_trace + 1) * 2 * n : NULL;
+                    r = search_range(NULL, NULL, Tq, Tk, 0, q * (int64_t)bq, imin64((q + 1) * (int64_t)bq, Tq), 0, Bq,
+                                     n, bk, causal, ORC_F32C, memo, idx + u * n, &dg, tn, NULL, max_trace, &ex);
+                    cnt[u] = (int32_t)n;
+                    free(memo);
+                }
+            }
+        }
+        if (r) {
+#pragma omp critical
+            err = r;
+        }
+    }
+    return err;
 }
 
 /* -------------------------------------------------------------------------------------------- */

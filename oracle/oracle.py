@@ -23,7 +23,7 @@ F32C = 0  # canonical fp32: acc = fmaf(q[c], k[c], acc), c = 0..d-1 (reading G9)
 F64 = 1   # fp64 dot products
 F32L = 2  # reading G9b: 16 sequential fmaf segments of d/16 terms + pairwise tree (o = 8, 4, 2, 1)
 
-_ERR = {1: "invalid value", 2: "out of memory", 3: "index out of range"}
+_ERR = {1: "invalid value", 2: "out of memory", 3: "index out of range", 4: "replay: a block score was not supplied"}
 
 
 def build(force: bool = False) -> str:
@@ -75,6 +75,8 @@ def lib():
         _lib.oracle_jitter.argtypes = [u64, i64, i32, i64, i32]
         _lib.oracle_jitter.restype = i64
         _lib.oracle_vote.argtypes = [i32, i64, i32, P, P, i32, i32, i32, P, P]
+        _lib.oracle_mask_replay.argtypes = [i32] * 6 + [i64, P, P, i64, P, P, P, i32]
+        _lib.oracle_mask_replay.restype = i32
         for name in ("oracle_mask_ext", "oracle_mask_trace_ext", "oracle_mask_paged_ext", "oracle_top_r_components",
                      "oracle_vote"):
             getattr(_lib, name).restype = i32
@@ -239,6 +241,27 @@ def dense_attention(Q, K, V, causal: bool, sm_scale: float = 0.0):
                                       float(sm_scale), _p(O), _p(lse))
     _check(rc, "oracle_dense_attention")
     return O, lse
+
+
+def mask_replay(Tq: int, Tk: int, k: int, bq: int, bk: int, causal: bool, q_of_unit, scores, trace: bool = False,
+                max_trace: int = 40):
+    """Alg. 1's split / rank / keep on SUPPLIED scores (C-2 replay parity): scores [u, nkb] fp32 holds
+    the score of every key block the u-th listed query block q_of_unit[u] needs (NaN elsewhere).
+    Returns (idx [u, n], cnt [u]) (+ per unit the list of [n, 2] node ranges after every iteration,
+    entry 0 = initial, if trace); raises if the search needs a score that was not supplied."""
+    qs = np.ascontiguousarray(np.asarray(q_of_unit, np.int64))
+    sc = np.ascontiguousarray(np.asarray(scores, np.float32))
+    n = k // bk
+    idx = np.empty((len(qs), n), np.int32)
+    cnt = np.empty(len(qs), np.int32)
+    tn = np.full((len(qs), max_trace + 1, n, 2), -7, np.int32) if trace else None
+    rc = lib().oracle_mask_replay(Tq, Tk, k, bq, bk, int(causal), len(qs), _p(qs), _p(sc), sc.shape[1], _p(idx),
+                                  _p(cnt), _p(tn), max_trace)
+    _check(rc, "oracle_mask_replay")
+    if not trace:
+        return idx, cnt
+    nodes = [[tn[u, i] for i in range(max_trace + 1) if tn[u, i, 0, 0] != -7] for u in range(len(qs))]
+    return idx, cnt, nodes
 
 
 def mask_paged(Q, Kpages, block_table, seq_lens, k: int, bq: int, bk: int, causal: bool, mode: int = F32C,

@@ -9,6 +9,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libhipattn.so")
+# Debug variant (test infrastructure, SURVEY 8(c) C-2 replay parity): the product objects with
+# mask_tc.cu rebuilt under -DHIPATTN_DEBUG_SCORES (the tcgen05 mask kernel dumps its branch scores).
+DEBUG_LIB = os.path.join(PKG, "libhipattn_debug.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -54,6 +57,25 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
                            "-o", LIB + ".tmp", *objs])
     os.replace(LIB + ".tmp", LIB)
     return LIB
+
+
+def build_debug(force: bool = False) -> str:
+    """libhipattn_debug.so: build() first, then mask_tc.cu again with -DHIPATTN_DEBUG_SCORES, linked
+    with the other product objects."""
+    build(force=False)
+    if not force and os.path.exists(DEBUG_LIB) and os.path.getmtime(DEBUG_LIB) >= max(os.path.getmtime(f) for f in deps()):
+        return DEBUG_LIB
+    objdir = os.path.join(ROOT, "build", "obj")
+    dbg_obj = os.path.join(ROOT, "build", "mask_tc_debug.o")
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+                           "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
+                           "-DHIPATTN_DEBUG_SCORES", "-c", os.path.join(PKG, "csrc", "mask_tc.cu"), "-o", dbg_obj])
+    objs = [os.path.join(objdir, os.path.basename(src) + ".o") for src in sources()
+            if os.path.basename(src) != "mask_tc.cu"] + [dbg_obj]
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                           "-o", DEBUG_LIB + ".tmp", *objs])
+    os.replace(DEBUG_LIB + ".tmp", DEBUG_LIB)
+    return DEBUG_LIB
 
 
 if __name__ == "__main__":

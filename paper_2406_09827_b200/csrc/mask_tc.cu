@@ -38,6 +38,20 @@ constexpr uint32_t kQTileBytes = 2 * 32 * 128;   // two 64-column regions x 32 r
 constexpr uint32_t kMTSlot = 128 * 128;          // one item: 128 rows x 64 bf16
 constexpr uint32_t kIdescS = idesc_bf16(128, 32, 0, 0);
 
+#ifdef HIPATTN_DEBUG_SCORES
+// Debug builds only (libhipattn_debug.so; SURVEY 8(c) C-2 replay parity): every representative score
+// of the units whose mask row `lin` has g_dbg_slot[lin] >= 0 is written to g_dbg_dump[slot * stride +
+// block], so a test can feed the GPU's own scores to the oracle's selection steps.
+__device__ const int32_t* g_dbg_slot = nullptr;
+__device__ float* g_dbg_dump = nullptr;
+__device__ int64_t g_dbg_stride = 0;
+#define HIP_DBG_MEMBER float* dbg = nullptr;
+#define HIP_DBG_STORE(blk, v) do { if (dbg) dbg[blk] = (v); } while (0)
+#else
+#define HIP_DBG_MEMBER
+#define HIP_DBG_STORE(blk, v) do { } while (0)
+#endif
+
 template <int SLOTS, bool PAGED = false>
 struct MaskTCSmemLayout {
   static constexpr uint32_t k0 = 0;                                        // ring (1024-aligned)
@@ -74,6 +88,7 @@ struct TCScorer {
   uint32_t ckeep = 3u;   // top-r: bit h = this thread's chunk of d-half h has a kept component
                          // (else the chunk is zero-filled without a global read, topr.cuh)
   HIP_PT_MEMBER
+  HIP_DBG_MEMBER
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
   __device__ __forceinline__ const char* row(int s) const { return kh + (uint64_t)(uint32_t)s * row_bytes; }
@@ -170,7 +185,10 @@ struct TCScorer {
           if (s < Tk && (!causal || s <= tpos0)) best = v0;
         }
         for (int off = 1; off <= bm; off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-        if (lb < nblk && (r & bm) == 0) out[blk0 + lb] = best;
+        if (lb < nblk && (r & bm) == 0) {
+          HIP_DBG_STORE(rep[blk0 + lb], best);
+          out[blk0 + lb] = best;
+        }
         continue;
       }
       float v[32];
@@ -197,7 +215,10 @@ struct TCScorer {
         }
       }
       for (int off = 1; off <= bm; off <<= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-      if (lb < nblk && (r & bm) == 0) out[blk0 + lb] = best;
+      if (lb < nblk && (r & bm) == 0) {
+        HIP_DBG_STORE(rep[blk0 + lb], best);
+        out[blk0 + lb] = best;
+      }
     }
   }
 
@@ -397,6 +418,9 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
         sc.bt16 = tb;  // visible to the CTA after tree_search's first barrier
       }
     }
+#ifdef HIPATTN_DEBUG_SCORES
+    if (g_dbg_slot && g_dbg_slot[lin] >= 0) sc.dbg = g_dbg_dump + (int64_t)g_dbg_slot[lin] * g_dbg_stride;
+#endif
 #ifdef HIPATTN_PHASES
     sc.pt = &ptimer;
     ptimer.mark(7);  // unit setup / Q load / exact units
@@ -459,6 +483,16 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
     default: return launch_v<2, 4, 4, 7>(sh, qs, ks, idx, cnt, stream, num_sms);
   }
 }
+
+#ifdef HIPATTN_DEBUG_SCORES
+// Debug builds only: slot_of_unit [units] (device, -1 = not dumped) and dump [slots, stride] (device);
+// NULL slot_of_unit switches the dump off.
+extern "C" int hip_debug_score_dump(const int32_t* slot_of_unit, float* dump, int64_t stride) {
+  if (cudaMemcpyToSymbol(hip::g_dbg_slot, &slot_of_unit, sizeof(slot_of_unit)) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(hip::g_dbg_dump, &dump, sizeof(dump)) != cudaSuccess) return 2;
+  return cudaMemcpyToSymbol(hip::g_dbg_stride, &stride, sizeof(stride)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 #ifdef HIPATTN_PHASES
 // Profiling builds only (profiles/phase_timers.py): read and clear this translation unit's

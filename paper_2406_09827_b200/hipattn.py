@@ -9,6 +9,7 @@ key block sizes, n = k / b_k selected key blocks per query block (re
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -53,13 +54,23 @@ class PagedKV(ctypes.Structure):
 
 
 _lib = None
+_libs: dict = {}
 
 
 def load(path: str = LIB_PATH):
     """Load libhipattn.so (ctypes).  Raises if it has not been built: there is no fallback."""
     global _lib
-    if _lib is not None:
+    if _lib is not None and path == LIB_PATH:
         return _lib
+    lib = _open(path)
+    if path == LIB_PATH:
+        _lib = lib
+    return lib
+
+
+def _open(path: str):
+    if path in _libs:
+        return _libs[path]
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
@@ -81,8 +92,38 @@ def load(path: str = LIB_PATH):
     lib.hip_sparse_attention_decode.restype = ctypes.c_int
     lib.hip_sparse_attention_decode.argtypes = ([ctypes.c_int] + [i32] * 5 + [TensorDesc, ctypes.POINTER(PagedKV),
                                                 ctypes.POINTER(Params), P, P, TensorDesc, P, P, sz, P])
-    _lib = lib
+    _libs[path] = lib
     return lib
+
+
+DEBUG_LIB_PATH = os.path.join(_PKG, "libhipattn_debug.so")
+
+
+@contextlib.contextmanager
+def debug_score_dump(slot_of_unit: torch.Tensor, dump: torch.Tensor):
+    """TEST INFRASTRUCTURE (SURVEY 8(c) C-2 replay parity): inside the block, the mask calls of this
+    module go through libhipattn_debug.so, whose tcgen05 mask kernel writes the score of every
+    representative block of unit row `lin` (b * H_m + h) * N_qb + q with slot_of_unit[lin] = s >= 0 to
+    dump[s, block].  slot_of_unit: int32 [units] on the device; dump: fp32 [slots, N_kb] on the device."""
+    global _lib
+    if slot_of_unit.dtype != torch.int32 or dump.dtype != torch.float32 or dump.dim() != 2:
+        raise TypeError("slot_of_unit int32 [units], dump float32 [slots, N_kb]")
+    if not (slot_of_unit.is_contiguous() and dump.is_contiguous()):
+        raise ValueError("contiguous buffers")
+    dbg = _open(DEBUG_LIB_PATH)
+    dbg.hip_debug_score_dump.restype = ctypes.c_int
+    dbg.hip_debug_score_dump.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+    with torch.cuda.device(dump.device):
+        if dbg.hip_debug_score_dump(slot_of_unit.data_ptr(), dump.data_ptr(), dump.shape[1]) != 0:
+            raise RuntimeError("hip_debug_score_dump failed")
+        saved = load()
+        _lib = dbg
+        try:
+            yield
+        finally:
+            torch.cuda.synchronize(dump.device)
+            dbg.hip_debug_score_dump(None, None, 0)
+            _lib = saved
 
 
 def _check(status: int):

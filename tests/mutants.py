@@ -49,6 +49,11 @@ MUTANTS = {
                                                  "for (int64_t gt = 0; gt < (int64_t)1 * (t1 - t0); ++gt) {"),
     "GQA-shared rows taken from consecutive heads' wrong rows": ("const float *q = Qh + (gt / (t1 - t0)) * hstride + t * d;",
                                                                   "const float *q = Qh + (gt / (t1 - t0)) * d + t * d;"),
+    "F32L tree reversed (o = 1, 2, 4, 8)": ("for (int o = 8; o >= 1; o >>= 1) {", "for (int o = 1; o <= 8; o <<= 1) {"),
+    "F32L strided segments instead of contiguous": ("seg[c / w] = fmaf(q[c], kk[c], seg[c / w]);",
+                                                    "seg[c % 16] = fmaf(q[c], kk[c], seg[c % 16]);"),
+    "F32C accumulates in reverse order": ("for (int i = 0; i < ncomp; ++i) {\n                    int c = comp ? comp[i] : i;\n                    acc = fmaf(",
+                                          "for (int i = ncomp - 1; i >= 0; --i) {\n                    int c = comp ? comp[i] : i;\n                    acc = fmaf("),
     "union keeps duplicates": ("if (w == 0 || tok[i] != tok[w - 1]) tok[w++] = tok[i];", "tok[w++] = tok[i];"),
 }
 

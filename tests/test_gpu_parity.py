@@ -23,9 +23,6 @@ from paper_2406_09827_b200 import synth
 pytestmark = pytest.mark.gpu
 
 TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
-# rigorous bound for any fp32 evaluation order of a d-term dot product (tensor-core accumulation
-# included): |err| <= TAU * sum_c |q_c k_c|, TAU = d * 2^-22 (4x the round-to-nearest bound d*u)
-TAU_UNIT = 2.0 ** -22
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -101,28 +98,34 @@ def test_mask_tcgen05_integer_bitexact(orc, Tq, Tk, Hq, Hkv, bk, k, causal):
     _assert_mask_equal(gi, gc, oi, oc)
 
 
-def _certify(orc, Q, K, k, bq, bk, causal, gi, gc):
-    """Mismatch fraction of the tcgen05 mask vs the F64 oracle, and whether every mismatching query
-    block is a certified near-tie: some selection gap of the exact (fp64) run <= 2 * eps where
-    eps = TAU * max over scored pairs of sum |q_c k_c| bounds every fp32 score error."""
-    oi, oc, dg = orc.mask(Q, K, k, bq, bk, causal, mode=orc.F64, diag=True)
-    assert np.array_equal(gc, oc)
-    d = Q.shape[-1]
-    bad = (gi != oi).any(-1)
-    eps = TAU_UNIT * d * dg["emax"]
-    explained = dg["margin_min"] <= 2 * eps
-    return bad.mean(), int(bad.sum()), int((bad & ~explained).sum())
+def _slot_map(lins, units):
+    slot = torch.full((units,), -1, dtype=torch.int32, device="cuda")
+    slot[torch.as_tensor(lins, dtype=torch.long, device="cuda")] = torch.arange(len(lins), dtype=torch.int32,
+                                                                                 device="cuda")
+    return slot
 
 
 @pytest.mark.parametrize("dist", ["iid", "llm"])
 def test_mask_tcgen05_gaussian_certified(orc, dist):
-    Q, K, _ = synth.gen_qkv(1, 4, 2, 4096, 4096, 128, dist, seed=3, dtype=torch.bfloat16, make_v=False)
-    gi, gc = _gpu_mask(Q, K, 512, 32, 2, True)
-    frac, nbad, unexplained = _certify(orc, Q, K, 512, 32, 2, True, gi, gc)
-    print(f"\n[parity] tcgen05 mask vs F64 oracle ({dist}): {nbad} of {gi.shape[1] * gi.shape[2]} query blocks "
-          f"differ ({100 * frac:.2f}%), unexplained {unexplained}")
-    assert unexplained == 0
-    assert frac <= 0.10
+    """tcgen05 masks on Gaussian inputs: every unit's scores within the fp32 bound, the GPU's selection
+    replayed bit-exactly from its own scores, and every mismatch vs F64 certified at its first
+    divergent iteration (tests/test_gpu_replay.py check_unit)."""
+    from test_gpu_replay import check_unit
+    Hq, Hkv, T, d = 4, 2, 4096, 128
+    Q, K, _ = synth.gen_qkv(1, Hq, Hkv, T, T, d, dist, seed=3, dtype=torch.bfloat16, make_v=False)
+    nqb, nkb = T // 32, T // 2
+    dump = torch.full((Hq * nqb, nkb), float("nan"), dtype=torch.float32, device="cuda")
+    with H.debug_score_dump(_slot_map(list(range(Hq * nqb)), Hq * nqb), dump):
+        idx, cnt = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=512, b_q=32, b_k=2)
+    gi, gs = idx.cpu().numpy(), dump.cpu().numpy()
+    st = dict(units=0, scores=0, replayed=0, mismatch=0, certified=0, unexplained=0)
+    for h in range(Hq):
+        for q in range(nqb):
+            check_unit(orc, Q[:, h:h + 1], K[:, h // 2:h // 2 + 1], 512, 32, 2, True, q, gi[0, h, q],
+                       gs[h * nqb + q], d, st)
+    print(f"\n[parity] tcgen05 mask vs F64 oracle ({dist}): {st}")
+    assert st["unexplained"] == 0
+    assert st["mismatch"] <= 0.10 * st["units"]
 
 
 # ------------------------------------------------------------------------------------------------
@@ -201,26 +204,31 @@ def test_decode_paged_parity(orc, dt, dist, ps):
     Q = synth.gen_decode_q(B, Hq, d, seed=7, dtype=dt, dist=dist)
     kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=7, dtype=dt, dist=dist)
     T = max(seq)
-    idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk,
-                                     causal=True)
+    dump = torch.full((B * Hq, -(-T // bk)), float("nan"), dtype=torch.float32, device="cuda")
+    with H.debug_score_dump(_slot_map(list(range(B * Hq)), B * Hq), dump):
+        idx, cnt = H.mask_estimate_paged(Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=1, b_k=bk,
+                                         causal=True)
     torch.cuda.synchronize()
-    gi, gc = idx.cpu().numpy(), cnt.cpu().numpy()
+    gi, gc, gs = idx.cpu().numpy(), cnt.cpu().numpy(), dump.cpu().numpy()
     if dt == torch.float32:  # decode GEMV kernel: oracle F32L order (G9b), bit-exact
         oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F32L)
         _assert_mask_equal(gi, gc, oi, oc)
     elif dist == "int":  # tcgen05 scoring on integer inputs: every sum exact
         oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F32C)
         _assert_mask_equal(gi, gc, oi, oc)
-    else:  # tcgen05 scoring on Gaussian inputs: mismatches must be certified near-ties
+    else:  # tcgen05 scoring on Gaussian inputs: scores bounded, replay exact, mismatches certified
+        from test_gpu_replay import check_unit
         oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True, mode=orc.F64)
-        nbad = unexplained = 0
+        assert np.array_equal(gc, oc)
+        st = dict(units=0, scores=0, replayed=0, mismatch=0, certified=0, unexplained=0)
         for b in range(B):
             Kb = _paged_to_contiguous(kp, bt, sl, b)
-            frac, nb, un = _certify(orc, Q[b:b + 1], Kb, k, 1, bk, True, gi[b:b + 1], gc[b:b + 1])
-            nbad += nb
-            unexplained += un
-        print(f"\n[parity] tcgen05 decode mask vs F64 oracle: {nbad} of {B * Hq} units differ, unexplained {unexplained}")
-        assert unexplained == 0
+            for h in range(Hq):
+                hk = h // (Hq // Hkv)
+                check_unit(orc, Q[b:b + 1, h:h + 1], Kb[:, hk:hk + 1], k, 1, bk, True, 0, gi[b, h, 0],
+                           gs[b * Hq + h], d, st)
+        print(f"\n[parity] tcgen05 decode mask vs F64 oracle: {st}")
+        assert st["unexplained"] == 0
     # attention on the ORACLE's selection (never feed GPU output to the oracle)
     o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T,
                                        torch.from_numpy(oi).cuda(), torch.from_numpy(oc).cuda(), k_budget=k,
@@ -306,31 +314,31 @@ def test_full_size_sampled(orc, cfg):
     bottom-right alignment makes it exact)."""
     Hq, T, n_heads, per_head = {"c2": (32, 32768, 48, 7), "c4": (40, 131072, 8, 7), "c5": (32, 1048576, 3, 7)}[cfg]
     B, d, k, bq, bk = 1, 128, 512, 32, 2
+    from test_gpu_replay import check_unit
     Q, K, V = synth.gen_qkv(B, Hq, Hq, T, T, d, "llm", seed=0, dtype=torch.bfloat16, device="cuda")
-    idx, cnt = H.mask_estimate(Q, K, k_budget=k, b_q=bq, b_k=bk)
-    o = H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=k, b_q=bq, b_k=bk)
-    torch.cuda.synchronize()
     nqb = T // bq
     rng = np.random.default_rng(0)
     units = [(int(h), q) for h in rng.integers(0, Hq, n_heads) for q in
              [0, 15, 16, 31, 32, nqb - 1, int(rng.integers(33, nqb - 1))][:per_head]]
-    n_bad = n_unexpl = 0
-    for h, q in units:
+    units = sorted(set(units))
+    dump = torch.full((len(units), T // bk), float("nan"), dtype=torch.float32, device="cuda")
+    with H.debug_score_dump(_slot_map([h * nqb + q for h, q in units], Hq * nqb), dump):
+        idx, cnt = H.mask_estimate(Q, K, k_budget=k, b_q=bq, b_k=bk)
+    o = H.sparse_attention_prefill(Q, K, V, idx, cnt, k_budget=k, b_q=bq, b_k=bk)
+    torch.cuda.synchronize()
+    st = dict(units=0, scores=0, replayed=0, mismatch=0, certified=0, unexplained=0)
+    for u, (h, q) in enumerate(units):
         t1 = (q + 1) * bq
         Qs = Q[:, h:h + 1, q * bq:t1].cpu()
         Ks, Vs = K[:, h:h + 1, :t1].cpu(), V[:, h:h + 1, :t1].cpu()
-        oi, oc, dg = orc.mask(Qs, Ks, k, bq, bk, True, mode=orc.F64, diag=True)
         gi = idx[0, h, q].cpu().numpy()
-        assert int(cnt[0, h, q]) == oc[0, 0, 0]
-        if not np.array_equal(gi, oi[0, 0, 0]):
-            n_bad += 1
-            eps = TAU_UNIT * d * dg["emax"][0, 0, 0]
-            n_unexpl += int(dg["margin_min"][0, 0, 0] > 2 * eps)
-            continue
-        Oo, _ = orc.sparse_attention(Qs, Ks, Vs, k, bq, bk, True, oi, oc)
+        assert int(cnt[0, h, q]) == min(k // bk, t1 // bk)
+        check_unit(orc, Qs, Ks, k, bq, bk, True, 0, gi, dump[u, :t1 // bk].cpu().numpy(), d, st)
+        # C-3: attention on the GPU's own selection
+        Oo, _ = orc.sparse_attention(Qs, Ks, Vs, k, bq, bk, True, gi[None, None, None], cnt[0, h, q].view(1, 1, 1).cpu())
         assert np.abs(o[0, h, q * bq:t1].float().cpu().numpy() - Oo[0, 0]).max() <= 2e-2
-    print(f"\n[parity] {cfg} sampled: {n_bad}/{len(units)} query blocks differ, unexplained {n_unexpl}")
-    assert n_unexpl == 0
+    print(f"\n[parity] {cfg} sampled: {st}")
+    assert st["unexplained"] == 0
     del Q, K, V, o, idx, cnt
     torch.cuda.empty_cache()
 
@@ -444,6 +452,35 @@ def test_decoder_rm_cache_schedule(orc, shared, chunks):
         Oo, _ = orc.sparse_attention_paged(q, kp, vp, bt, sl, k, 1, bk, True, ei, ec, sink=4, window=16)
         assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
     assert 1 < dec.refreshes < 8
+
+
+def test_decoder_non_refresh_step_attends_current_token(orc):
+    """with a cached mask (r_m = 8, the paper's default) a step between refreshes must still
+    attend the token just generated — the default sliding window (128) covers it.  Changing
+    that token's V row changes the output, and the output matches the oracle's union mask."""
+    from paper_2406_09827_b200.decode import HipDecoder
+    B, Hq, Hkv, d, ps = 1, 2, 1, 128, 16
+    L0 = 4000                              # divisible by 8: refresh step
+    kp, vp, bt, _ = synth.gen_paged_direct(B, Hkv, [L0 + 16], d, ps, seed=90, dtype=torch.bfloat16)
+    kp, vp, bt = kp.cuda(), vp.cuda(), bt.cuda()
+    dec = HipDecoder(k_budget=256, b_k=2, b_q=1)
+    q0 = synth.gen_decode_q(B, Hq, d, seed=91).cuda()
+    dec.step(q0, kp, vp, bt, torch.tensor([L0], dtype=torch.int32, device="cuda"), [L0])
+    assert dec.refreshes == 1
+    L = L0 + 3                             # not divisible by 8: the cached mask is reused
+    q = synth.gen_decode_q(B, Hq, d, seed=92).cuda()
+    sl = torch.tensor([L], dtype=torch.int32, device="cuda")
+    o1 = dec.step(q, kp, vp, bt, sl, [L]).float()
+    assert dec.refreshes == 1
+    page, slot = int(bt[0, (L - 1) // ps]), (L - 1) % ps
+    vp[page, :, slot] = 512.0              # the current token's value row (weight ~1/700 -> ~0.7 change)
+    o2 = dec.step(q, kp, vp, bt, sl, [L]).float()
+    torch.cuda.synchronize()
+    assert dec.refreshes == 1
+    assert (o2 - o1).abs().min() > 0.1, "the current token is not attended"
+    Oo, _ = orc.sparse_attention_paged(q.cpu(), kp.cpu(), vp.cpu(), bt.cpu(), sl.cpu(), 256, 1, 2, True,
+                                       dec.idx.cpu().numpy(), dec.cnt.cpu().numpy(), sink=32, window=128)
+    assert np.abs(o2.cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
 
 
 # ------------------------------------------------------------------------------------------------

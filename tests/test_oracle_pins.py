@@ -462,6 +462,137 @@ def test_f32l_mode_pins(orc):
 
 
 # --------------------------------------------------------------------------------------------
+# Replay entry (C-2): the split / rank / keep steps on supplied scores.  Supplied the exact block
+# maxima (computed here by brute force, independently of the oracle), it must give the oracle's own
+# F64 mask; a missing score is an error; and in the one-level regime it is the exact top-n of the
+# supplied scores (PIN-2 again, now for the replay path).
+# --------------------------------------------------------------------------------------------
+def _brute_block_max(Q, K, bq, bk, q):
+    Qn, Kn = Q[0, 0].double().numpy(), K[0, 0].double().numpy()
+    Tq, Tk = Qn.shape[0], Kn.shape[0]
+    t0, t1 = q * bq, min((q + 1) * bq, Tq)
+    S = Qn[t0:t1] @ Kn.T
+    S[np.arange(t0, t1)[:, None] + (Tk - Tq) < np.arange(Tk)[None, :]] = -np.inf
+    nkb = -(-Tk // bk)
+    Sp = np.full((t1 - t0, nkb * bk), -np.inf)
+    Sp[:, :Tk] = S
+    return Sp.reshape(t1 - t0, nkb, bk).max(axis=(0, 2)).astype(np.float32)
+
+
+def test_replay_reproduces_mask_from_supplied_scores(orc):
+    Tq, Tk, d, k, bq, bk = 1000, 1200, 32, 64, 16, 2
+    Q, K, _ = synth.gen_qkv(1, 1, 1, Tq, Tk, d, "int", seed=21, dtype=torch.float32, make_v=False)
+    qs = [0, 3, 10, 30, 45, 50, 62]
+    nkb = -(-Tk // bk)
+    sc = np.stack([_brute_block_max(Q, K, bq, bk, q) for q in qs])  # integer inputs: exact in fp32
+    ri, rc, tr = orc.mask_replay(Tq, Tk, k, bq, bk, True, qs, sc, trace=True)
+    oi, oc = orc.mask(Q, K, k, bq, bk, True, mode=orc.F64)
+    assert np.array_equal(ri, oi[0, 0, qs]) and np.array_equal(rc, oc[0, 0, qs])
+    for u, q in enumerate(qs):  # the replay's per-iteration node sets are the oracle's own trace
+        t = orc.mask_trace(Q, K, k, bq, bk, True, 0, 0, q, mode=orc.F64)
+        assert len(tr[u]) == len(t["nodes"]) and all(np.array_equal(a, b) for a, b in zip(tr[u], t["nodes"]))
+    # a score the search needs but nobody supplied: an error, not a silent choice
+    holey = sc.copy()
+    holey[-1, 0] = np.nan  # block 0 is always a first-iteration representative (f_0 = 0)
+    with pytest.raises(ValueError):
+        orc.mask_replay(Tq, Tk, k, bq, bk, True, qs, holey)
+    # one-level regime (n < B_q <= 2n): the replayed mask is the exact top-n of the supplied scores
+    n = k // bk
+    rng = np.random.default_rng(2)
+    for q in range(Tq // bq):
+        Bq = min(((q + 1) * bq - 1 + Tk - Tq) // bk + 1, nkb)
+        if not n < Bq <= 2 * n:
+            continue
+        s = rng.integers(-3, 4, size=(1, nkb)).astype(np.float32)  # many ties: tie rule matters
+        ri, _ = orc.mask_replay(Tq, Tk, k, bq, bk, True, [q], s)
+        order = np.lexsort((np.arange(Bq), -s[0, :Bq]))[:n]
+        assert np.array_equal(ri[0], np.sort(order))
+
+
+# --------------------------------------------------------------------------------------------
+# F32C / F32L pinned by exact rational arithmetic: the two fp32 orders of
+# readings G9 / G9b restated from their DEFINITIONS with fractions.Fraction — fmaf(a, b, c) is ONE
+# rounding of the exact a*b + c to binary32 (round to nearest, ties to even), an fp32 add one
+# rounding of the exact sum — and compared bit-for-bit with the oracle's C arithmetic on iid inputs
+# (where every partial sum rounds).  A reversed tree or strided segments fail here.
+# --------------------------------------------------------------------------------------------
+from fractions import Fraction
+
+
+def _round_f32(x: Fraction) -> Fraction:
+    """Exact value of binary32 round-to-nearest-even of the rational x (normal and subnormal)."""
+    if x == 0:
+        return Fraction(0)
+    sgn, a = (1, x) if x > 0 else (-1, -x)
+    e = a.numerator.bit_length() - a.denominator.bit_length()  # 2^e <= a < 2^(e+2)
+    if Fraction(2) ** e > a:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= a:
+        e += 1
+    q = Fraction(2) ** (max(e, -126) - 23)  # spacing of binary32 around a
+    m = a / q
+    fl = m.numerator // m.denominator
+    rem = m - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    assert fl * q < Fraction(2) ** 128, "overflow"
+    return sgn * fl * q
+
+
+def _fmaf(a, b, c):
+    return _round_f32(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def _f32c_dot(q, k):
+    acc = Fraction(0)
+    for c in range(len(q)):
+        acc = _fmaf(float(q[c]), float(k[c]), acc)
+    return acc
+
+
+def _f32l_dot(q, k):
+    """G9b: 16 segments of d/16 consecutive components, each a sequential fmaf chain, then the
+    pairwise tree v[l] <- v[l] + v[l xor o] for o = 8, 4, 2, 1 (all l at once), result v[0]."""
+    d = len(q)
+    w = d // 16
+    seg = []
+    for l in range(16):
+        acc = Fraction(0)
+        for c in range(l * w, (l + 1) * w):
+            acc = _fmaf(float(q[c]), float(k[c]), acc)
+        seg.append(acc)
+    for o in (8, 4, 2, 1):
+        seg = [_round_f32(seg[l] + seg[l ^ o]) for l in range(16)]
+    return seg[0]
+
+
+@pytest.mark.parametrize("mode_name", ["F32C", "F32L"])
+def test_fp32_orders_pinned_by_exact_rationals(orc, mode_name):
+    d, T = 128, 48
+    Q, K, _ = synth.gen_qkv(1, 1, 1, T, T, d, "iid", seed=77, dtype=torch.float32, make_v=False)
+    Q = Q * 3.0  # larger partial sums: more of them round
+    qn, kn = Q[0, 0].numpy(), K[0, 0].numpy()
+    mode = getattr(orc, mode_name)
+    ref = _f32c_dot if mode_name == "F32C" else _f32l_dot
+    # b_q = 1, b_k = 1: a tile is one (row, key) pair, so the oracle's block score IS one dot product
+    tup = [(0, 0, t, s) for t in range(T) for s in range(0, t + 1, 5)]
+    got, _ = orc.block_scores(Q, K, 1, 1, True, tup, mode=mode)
+    want = np.array([float(ref(qn[t], kn[s])) for _, _, t, s in tup])
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+    # the two orders really differ on these inputs (the test can tell them apart)
+    other = _f32l_dot if mode_name == "F32C" else _f32c_dot
+    assert any(float(other(qn[t], kn[s])) != g for (_, _, t, s), g in zip(tup, got))
+
+
+def test_round_f32_matches_numpy():
+    rng = np.random.default_rng(5)
+    for x in rng.standard_normal(2000) * 10.0 ** rng.integers(-40, 38, 2000):
+        assert float(_round_f32(Fraction(float(x)))) == float(np.float32(x))
+    for x in (1 + 2 ** -24, 1 + 3 * 2 ** -24, 2 ** -149 * 0.5, 2 ** -149 * 1.5, -(2 ** -126) * (1 - 2 ** -24)):
+        assert float(_round_f32(Fraction(x))) == float(np.float32(x))
+
+
+# --------------------------------------------------------------------------------------------
 # Sink + sliding window (f1; P:641-645 "local sliding window and global sink attention are also
 # added", sizes (128, 32); the EffectiveMask of S:285-301: per row the union of the selected block
 # tokens, [0, sink) and (p - window, p], intersected with the causal bound, each token once).
