@@ -40,8 +40,9 @@
 extern "C" {
 #endif
 
-#define HIP_ATTN_VERSION 120 /* 1.2.0: + HIP_FLAG_GQA_SHARED_MASK (1.1.0: top_r, split_jitter, sample_seed,
-                                 hip_mask_vote) */
+#define HIP_ATTN_VERSION 200 /* 2.0.0: every compute call takes a workspace (prefill gained the two
+                                 arguments); 1.2.0: + HIP_FLAG_GQA_SHARED_MASK (1.1.0: top_r,
+                                 split_jitter, sample_seed, hip_mask_vote) */
 
 typedef enum {
     HIP_SUCCESS = 0,
@@ -132,9 +133,20 @@ const char* hip_last_error(void);
 /* Number of key blocks kept per query block, n = k / b_k (0 if the params are invalid). */
 int32_t hip_num_blocks(const hip_params_t* params);
 
-/* Device workspace (bytes) a call needs; 0 means none (pass NULL).  Currently every op needs 0;
- * callers should still query it so a later split-K decode can ask for scratch without an ABI
- * change. */
+/* Device workspace (bytes) a call with these arguments needs: scratch owned by the caller, at
+ * least 16-byte aligned, passed as (workspace, workspace_bytes).  A call returns
+ * HIP_ERROR_WORKSPACE (before any launch) if it is NULL or smaller.  Contents need no
+ * initialisation and are meaningless after the call; the library (re)initialises what it uses on
+ * `stream` (cudaMemsetAsync) before each launch.  One workspace must not serve two calls that may
+ * run concurrently (different streams without ordering), exactly like the outputs.
+ *   - every op: 256 bytes for the launch's job counter (persistent CTAs claim (b, h, query block)
+ *     jobs in order, which balances uneven query blocks and keeps the running jobs within one or
+ *     two heads, so that head's K stays L2-resident);
+ *   - HIP_OP_PREFILL / HIP_OP_DECODE with single-row units (min(b_q, T_q) = 1), d = 128 and at most
+ *     4096 units (B * H_q * T_q): + the split-K region, units * (4 + 8 * 132 * 4) bytes rounded up
+ *     (per-unit arrival counters and up to 8 partial softmax states of d + 4 floats), used when the
+ *     units do not fill the GPU (decode).
+ * Returns 0 for invalid arguments. */
 size_t hip_workspace_bytes(hip_op_t op, hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,
                            int32_t T_k, int32_t d, const hip_params_t* params);
 
@@ -149,6 +161,7 @@ size_t hip_workspace_bytes(hip_op_t op, hip_dtype_t dtype, int32_t B, int32_t H_
  *                blocks of every query block in ascending order, -1 after the first block_cnt
  *   block_cnt    OUT int32 [B, H_q, N_qb]: min(n, B_q) where B_q is the number of visible key blocks
  *                (all of them if causal == 0)
+ *   workspace    device scratch of at least hip_workspace_bytes(HIP_OP_MASK, ...) bytes (see there)
  *   Semantics per query block (G1-G10): if B_q <= n all visible blocks are selected; else n initial
  *   nodes f_j = floor((2 j B_q + n) / 2n), split at m = floor((f + l + 1) / 2), branch score = max of
  *   q_t . k_s over the tile of the branch's first block (causal pairs only), keep the n best by
@@ -162,7 +175,8 @@ size_t hip_workspace_bytes(hip_op_t op, hip_dtype_t dtype, int32_t B, int32_t H_
  *     - otherwise, and always with HIP_FLAG_EXACT_SCORES: the sequential chain c = 0..d-1 ("F32C").
  *   Errors: INVALID_VALUE for NULL pointers, dims < 1, T_k = 0 ("empty K"), k < b_k or
  *   k % b_k != 0, H_q % H_kv != 0, causal with T_q > T_k, page_size % b_k != 0, n > 1024,
- *   misaligned rows; NOT_SUPPORTED for d not in {64, 128} or a device that is not sm_100.
+ *   misaligned rows; WORKSPACE for a NULL, short or misaligned workspace; NOT_SUPPORTED for d not in
+ *   {64, 128} or a device that is not sm_100.
  *   b_q > T_q or b_k > T_k is NOT an error (one ragged block).
  */
 hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q, int32_t T_k,
@@ -185,14 +199,19 @@ hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_
  *   lse          OUT optional fp32 [B, H_q, T_q] contiguous (natural log-sum-exp of the scaled
  *                scores), NULL to skip.  A row with no visible token gets o = 0 and
  *                lse = -inf (G13).
+ *   workspace    device scratch of at least hip_workspace_bytes(HIP_OP_PREFILL, ...) bytes
  *   Arithmetic: fp32 scores and softmax; bf16 probabilities into the PV contraction (bf16 path).
+ *   Single-row units that do not fill the GPU are split over the keys (split-K) and merged in the
+ *   kernel by rescaling each split's partial softmax state to the common max (same result up to
+ *   fp32 rounding).
  *   Errors: as hip_mask_estimate; block indices are NOT range-checked on the device (garbage in,
  *   garbage out, never an out-of-bounds read: indices are clamped to [0, ceil(T_k/b_k)) ).
  */
 hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,
                                           int32_t T_k, int32_t d, hip_tensor_t q, hip_tensor_t k, hip_tensor_t v,
                                           const hip_params_t* params, const int32_t* block_idx,
-                                          const int32_t* block_cnt, hip_tensor_t o, float* lse, void* stream);
+                                          const int32_t* block_cnt, hip_tensor_t o, float* lse, void* workspace,
+                                          size_t workspace_bytes, void* stream);
 
 /*
  * hip_sparse_attention_decode — Eq. 2-3 for T_q query rows per sequence (T_q = 1 for plain decode)
@@ -201,6 +220,7 @@ hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t 
  *   q            [B, H_q, T_q, d]; the rows sit at positions seq_lens[b] - T_q + t
  *   paged        the cache (k_pages and v_pages required)
  *   block_idx / block_cnt / o / lse as for prefill, with N_qb = ceil(T_q / b_q)
+ *   workspace    device scratch of at least hip_workspace_bytes(HIP_OP_DECODE, ...) bytes (split-K)
  *   Errors: as hip_mask_estimate.
  */
 hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,

@@ -122,9 +122,53 @@ hip_status_t check_paged(const hip_paged_kv_t* pg, int esz, bool need_v, int bk)
   return HIP_SUCCESS;
 }
 
+// Workspace layout (bytes): [0, 256) the JobQueue counter of the launch; attention launches of
+// single-row units (T_q = 1 or b_q = 1, at most kSplitMaxUnits units) add the split-K region:
+// arrivals [units] uint32 (256-aligned), then partials [units][kSplitMax][kSplitStride] fp32.
+constexpr size_t kWsQueue = 256;
+
+size_t split_region_bytes(int64_t units) {
+  return hip::align_up((size_t)units * 4, 256) + (size_t)units * hip::kSplitMax * hip::kSplitStride * 4;
+}
+
+int64_t attn_units(int32_t B, int32_t Hq, int32_t Tq, const hip_params_t* p) {
+  const int32_t bq = std::min(p->b_q, Tq);
+  return (int64_t)B * Hq * ((Tq + bq - 1) / bq);
+}
+
+bool split_eligible(int32_t B, int32_t Hq, int32_t Tq, int32_t d, const hip_params_t* p) {
+  return d == 128 && std::min(p->b_q, Tq) == 1 && attn_units(B, Hq, Tq, p) <= hip::kSplitMaxUnits;
+}
+
+size_t workspace_bytes_for(hip_op_t op, int32_t B, int32_t Hq, int32_t Tq, int32_t d, const hip_params_t* p) {
+  if (op == HIP_OP_MASK) return kWsQueue;
+  if (split_eligible(B, Hq, Tq, d, p)) return kWsQueue + split_region_bytes(attn_units(B, Hq, Tq, p));
+  return kWsQueue;
+}
+
+hip_status_t check_workspace(void* ws, size_t have, size_t need) {
+  if (need == 0) return HIP_SUCCESS;
+  if (!ws) return fail(HIP_ERROR_WORKSPACE, "workspace is NULL; hip_workspace_bytes() = %zu", need);
+  if (have < need) return fail(HIP_ERROR_WORKSPACE, "workspace of %zu bytes < hip_workspace_bytes() = %zu", have, need);
+  if (!aligned16(ws)) return fail(HIP_ERROR_WORKSPACE, "workspace not 16-byte aligned");
+  return HIP_SUCCESS;
+}
+
+// Point the launch's scheduling / split-K state at the caller's workspace.
+void bind_workspace(hip::Shape& sh, void* ws, bool attn, int32_t B, int32_t Hq, int32_t Tq, int32_t d,
+                    const hip_params_t* p) {
+  char* w = static_cast<char*>(ws);
+  sh.sched = reinterpret_cast<unsigned int*>(w);
+  if (attn && split_eligible(B, Hq, Tq, d, p)) {
+    const int64_t units = attn_units(B, Hq, Tq, p);
+    sh.arrive = reinterpret_cast<unsigned int*>(w + kWsQueue);
+    sh.part = reinterpret_cast<float*>(w + kWsQueue + hip::align_up((size_t)units * 4, 256));
+  }
+}
+
 hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk, int32_t d, const hip_params_t* p,
                       const int32_t* seq_lens) {
-  hip::Shape s;
+  hip::Shape s{};
   s.B = B; s.Hq = Hq; s.Hkv = Hkv; s.Tq = Tq; s.Tk = Tk; s.d = d;
   s.n = p->k / p->b_k; s.bq = std::min(p->b_q, Tq); s.bk = p->b_k; s.causal = p->causal;
   s.nqb = (Tq + s.bq - 1) / s.bq;
@@ -135,6 +179,10 @@ hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk
   s.group = (p->flags & HIP_FLAG_GQA_SHARED_MASK) ? Hq / Hkv : 1;
   s.seed = p->sample_seed;
   s.seq_lens = seq_lens;
+  s.sched = nullptr;
+  s.splits = 1;
+  s.part = nullptr;
+  s.arrive = nullptr;
   return s;
 }
 
@@ -180,15 +228,16 @@ int32_t hip_num_blocks(const hip_params_t* p) {
 
 size_t hip_workspace_bytes(hip_op_t op, hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,
                            int32_t T_k, int32_t d, const hip_params_t* params) {
-  (void)op; (void)dtype; (void)B; (void)H_q; (void)H_kv; (void)T_q; (void)T_k; (void)d; (void)params;
-  return 0;
+  (void)dtype; (void)H_kv; (void)T_k;
+  if (!params || B < 1 || H_q < 1 || T_q < 1 || params->b_q < 1) return 0;
+  if (op != HIP_OP_MASK && op != HIP_OP_PREFILL && op != HIP_OP_DECODE) return 0;
+  return workspace_bytes_for(op, B, H_q, T_q, d, params);
 }
 
 hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q, int32_t T_k,
                                int32_t d, hip_tensor_t q, hip_tensor_t k, const hip_paged_kv_t* paged,
                                const hip_params_t* params, int32_t* block_idx, int32_t* block_cnt, void* workspace,
                                size_t workspace_bytes, void* stream) {
-  (void)workspace; (void)workspace_bytes;
   hip_status_t s = check_common(dtype, B, H_q, H_kv, T_q, T_k, d, params);
   if (s) return s;
   const int esz = esize_of(dtype);
@@ -201,9 +250,12 @@ hip_status_t hip_mask_estimate(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_
   } else if ((s = check_tensor("k", k, esz))) {
     return s;
   }
+  if ((s = check_workspace(workspace, workspace_bytes, workspace_bytes_for(HIP_OP_MASK, B, H_q, T_q, d, params))))
+    return s;
   int sms = 0;
   if ((s = device_info(&sms))) return s;
   hip::Shape sh = make_shape(B, H_q, H_kv, T_q, T_k, d, params, paged ? paged->seq_lens : nullptr);
+  bind_workspace(sh, workspace, false, B, H_q, T_q, d, params);
   hip::QSrc qs = make_q(q, esz);
   hip::RowSrc ks = paged ? make_paged(*paged, paged->k_pages, esz) : make_rows(k, esz);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -244,7 +296,8 @@ hip_status_t hip_mask_vote(int32_t n_e, int64_t units, int32_t n_in, const int32
 hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,
                                           int32_t T_k, int32_t d, hip_tensor_t q, hip_tensor_t k, hip_tensor_t v,
                                           const hip_params_t* params, const int32_t* block_idx,
-                                          const int32_t* block_cnt, hip_tensor_t o, float* lse, void* stream) {
+                                          const int32_t* block_cnt, hip_tensor_t o, float* lse, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
   hip_status_t s = check_common(dtype, B, H_q, H_kv, T_q, T_k, d, params);
   if (s) return s;
   const int esz = esize_of(dtype);
@@ -252,9 +305,12 @@ hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t 
       (s = check_tensor("o", o, esz)))
     return s;
   if (!block_idx || !block_cnt) return fail(HIP_ERROR_INVALID_VALUE, "block_idx / block_cnt is NULL");
+  if ((s = check_workspace(workspace, workspace_bytes, workspace_bytes_for(HIP_OP_PREFILL, B, H_q, T_q, d, params))))
+    return s;
   int sms = 0;
   if ((s = device_info(&sms))) return s;
   hip::Shape sh = make_shape(B, H_q, H_kv, T_q, T_k, d, params, nullptr);
+  bind_workspace(sh, workspace, true, B, H_q, T_q, d, params);
   const float scale = params->sm_scale > 0.f ? params->sm_scale : 1.0f / sqrtf((float)d);
   hip::QSrc qs = make_q(q, esz);
   hip::RowSrc ks = make_rows(k, esz), vs = make_rows(v, esz);
@@ -279,7 +335,6 @@ hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H
                                          const hip_params_t* params, const int32_t* block_idx,
                                          const int32_t* block_cnt, hip_tensor_t o, float* lse, void* workspace,
                                          size_t workspace_bytes, void* stream) {
-  (void)workspace; (void)workspace_bytes;
   if (!paged) return fail(HIP_ERROR_INVALID_VALUE, "paged is NULL");
   hip_status_t s = check_common(dtype, B, H_q, H_kv, T_q, paged->max_seq_len, d, params);
   if (s) return s;
@@ -287,9 +342,12 @@ hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H
   if ((s = check_tensor("q", q, esz)) || (s = check_tensor("o", o, esz))) return s;
   if ((s = check_paged(paged, esz, true, params->b_k))) return s;
   if (!block_idx || !block_cnt) return fail(HIP_ERROR_INVALID_VALUE, "block_idx / block_cnt is NULL");
+  if ((s = check_workspace(workspace, workspace_bytes, workspace_bytes_for(HIP_OP_DECODE, B, H_q, T_q, d, params))))
+    return s;
   int sms = 0;
   if ((s = device_info(&sms))) return s;
   hip::Shape sh = make_shape(B, H_q, H_kv, T_q, paged->max_seq_len, d, params, paged->seq_lens);
+  bind_workspace(sh, workspace, true, B, H_q, T_q, d, params);
   const float scale = params->sm_scale > 0.f ? params->sm_scale : 1.0f / sqrtf((float)d);
   hip::QSrc qs = make_q(q, esz);
   hip::RowSrc ks = make_paged(*paged, paged->k_pages, esz), vs = make_paged(*paged, paged->v_pages, esz);

@@ -48,6 +48,20 @@ inline cudaError_t persistent_ctas(K kernel, int threads, size_t smem, int tmem_
   return cudaSuccess;
 }
 
+// Split-K of single-row attention units (attn_tc): at most kSplitMax splits, only for launches of at
+// most kSplitMaxUnits units; partial stride kSplitStride floats (O[128], max, sum, unrounded sum, pad).
+constexpr int kSplitMax = 8, kSplitMaxUnits = 4096, kSplitStride = 132;
+
+// Dynamic job claiming (common.cuh JobQueue) only pays when there are more jobs than resident
+// CTAs; then the launch's counter (sh.sched, caller workspace) is zeroed on the launch stream.
+inline cudaError_t setup_queue(Shape& sh, int64_t jobs, int64_t grid, cudaStream_t stream) {
+  if (!sh.sched || jobs <= grid) {
+    sh.sched = nullptr;
+    return cudaSuccess;
+  }
+  return cudaMemsetAsync(sh.sched, 0, sizeof(unsigned int), stream);
+}
+
 // CUDA-core mask estimation (exact sequential fp32 scores), contiguous or paged keys.
 cudaError_t launch_mask_cc(const Shape& sh, const QSrc& qs, const RowSrc& ks, bool bf16, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms);

@@ -60,7 +60,8 @@ struct MaskTCSmemLayout {
   static constexpr uint32_t bt = sel + (uint32_t)align_up(sizeof(SelState<kMTNmax, 4>), 128);
   static constexpr uint32_t bt_bytes = PAGED ? (uint32_t)align_up(kBt16Max * 2, 128) : 0u;  // uint16 row
   static constexpr uint32_t misc = bt + bt_bytes;                          // mbarriers, TMEM address
-  static constexpr uint32_t total = misc + 64;
+  static constexpr uint32_t jq = misc + (uint32_t)align_up(8 * SLOTS + 4, 16); // JobQueue slots (2 x int64)
+  static constexpr uint32_t total = jq + 16;
 };
 
 template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kGrp = false, bool kRow1 = false, bool kBk2 = false>
@@ -125,7 +126,7 @@ struct TCScorer {
     const uint32_t dst = k_s0 + (i % SLOTS) * kMTSlot + sw128_off(r0, c8);
 #pragma unroll
     for (int j = 0; j < RJ; ++j)  // rows r0 + RPP j share r0's swizzle phase (RPP % 8 == 0)
-      cp_async16(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
+      cp_async16_pf256(dst + j * (RPP / 8) * 1024, rp[j] + h * 128, ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
     }
   }
 
@@ -158,8 +159,8 @@ struct TCScorer {
     const uint32_t x = (uint32_t)c8;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      cp_async16(dst + j * 128 + ((x ^ j) << 4), rp[j >> 1] + ((j & 1) ? row_bytes : 0u) + h * 128,
-                 ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
+      cp_async16_pf256(dst + j * 128 + ((x ^ j) << 4), rp[j >> 1] + ((j & 1) ? row_bytes : 0u) + h * 128,
+                  ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
   }
 
   __device__ __forceinline__ void wait_slot(int slot) {
@@ -328,7 +329,9 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
 
   const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int S = max(sh.chunks, 1);
-  for (int64_t jb = blockIdx.x; jb < units * S; jb += gridDim.x) {
+  JobQueue jq(sh.sched, base + L::jq);
+  for (int64_t jb = blockIdx.x; jb < units * S; jb = jq.next(jb)) {
+    jq.claim();
     const int64_t u = jb / S;
     const int cs = (int)(jb - u * S);
     int b, h, q;  // h: mask head (the kv head when GQA-shared, G25)
@@ -458,8 +461,10 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int64_t jobs = units * std::max(sh.chunks, 1);
-  int64_t grid = std::min<int64_t>(jobs, (int64_t)num_sms * per_sm);
-  kern<<<(unsigned)grid, 128, smem, stream>>>(sh, qs, ks, idx, cnt);
+  const int64_t grid = std::min<int64_t>(jobs, (int64_t)num_sms * per_sm);
+  Shape s2 = sh;
+  if ((e = setup_queue(s2, jobs, grid, stream)) != cudaSuccess) return e;
+  kern<<<(unsigned)grid, 128, smem, stream>>>(s2, qs, ks, idx, cnt);
   return cudaGetLastError();
 }
 

@@ -86,7 +86,7 @@ def _open(path: str):
                                       ctypes.POINTER(Params), P, P, P, sz, P])
     lib.hip_sparse_attention_prefill.restype = ctypes.c_int
     lib.hip_sparse_attention_prefill.argtypes = ([ctypes.c_int] + [i32] * 6 + [TensorDesc] * 3 +
-                                                 [ctypes.POINTER(Params), P, P, TensorDesc, P, P])
+                                                 [ctypes.POINTER(Params), P, P, TensorDesc, P, P, sz, P])
     lib.hip_mask_vote.restype = ctypes.c_int
     lib.hip_mask_vote.argtypes = [i32, ctypes.c_int64, i32, P, P, i32, i32, i32, P, P, P]
     lib.hip_sparse_attention_decode.restype = ctypes.c_int
@@ -151,6 +151,27 @@ def _stream(t: torch.Tensor, stream=None) -> int:
     if stream is not None:
         return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _workspace(op: int, dtype: int, B, Hq, Hkv, Tq, Tk, d, p: Params, device, stream=None):
+    """Device scratch of hip_workspace_bytes(...) bytes (the launch's job counter; split-K partials
+    for single-row attention), allocated per call from torch's caching allocator.  If the call runs
+    on a stream other than the current one, the block is recorded on it so the allocator does not
+    hand it out again before the kernel is done."""
+    n = int(load().hip_workspace_bytes(op, dtype, B, Hq, Hkv, Tq, Tk, d, ctypes.byref(p)))
+    if n == 0:
+        return None
+    ws = torch.empty(n, dtype=torch.uint8, device=device)
+    if stream is not None:
+        st = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(int(
+            stream.cuda_stream if hasattr(stream, "cuda_stream") else stream), device=device)
+        if st.cuda_stream != torch.cuda.current_stream(device).cuda_stream:
+            ws.record_stream(st)
+    return ws
+
+
+def _ws_args(ws):
+    return (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
 
 
 def _params(k: int, b_q: int, b_k: int, causal: bool, sm_scale=None, exact: bool = False, sink: int = 0,
@@ -226,8 +247,9 @@ def mask_estimate(q: torch.Tensor, k: torch.Tensor, *, k_budget: int = 512, b_q:
         _int32_buffer("out idx", idx, ishape, q.device)
         _int32_buffer("out cnt", cnt, cshape, q.device)
     with torch.cuda.device(q.device):
+        ws = _workspace(HIP_OP_MASK, _dtype_code(q), B, Hq, Hkv, Tq, Tk, d, p, q.device, stream)
         _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, Tk, d, _desc(q), _desc(k), None,
-                                     ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), None, 0, _stream(q, stream)))
+                                     ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), *_ws_args(ws), _stream(q, stream)))
     return idx, cnt
 
 
@@ -305,9 +327,10 @@ def mask_estimate_paged(q, k_pages, block_table, seq_lens, max_seq_len: int, *, 
         _int32_buffer("out idx", idx, ishape, q.device)
         _int32_buffer("out cnt", cnt, cshape, q.device)
     with torch.cuda.device(q.device):
+        ws = _workspace(HIP_OP_MASK, _dtype_code(q), B, Hq, Hkv, Tq, int(max_seq_len), d, p, q.device, stream)
         _check(lib.hip_mask_estimate(_dtype_code(q), B, Hq, Hkv, Tq, int(max_seq_len), d, _desc(q),
                                      TensorDesc(None, 0, 0, 0), ctypes.byref(pg), ctypes.byref(p), idx.data_ptr(),
-                                     cnt.data_ptr(), None, 0, _stream(q, stream)))
+                                     cnt.data_ptr(), *_ws_args(ws), _stream(q, stream)))
     return idx, cnt
 
 
@@ -328,9 +351,11 @@ def sparse_attention_prefill(q, k, v, idx, cnt, *, k_budget: int = 512, b_q: int
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
     with torch.cuda.device(q.device):
+        ws = _workspace(HIP_OP_PREFILL, _dtype_code(q), B, Hq, Hkv, Tq, Tk, d, p, q.device, stream)
         _check(lib.hip_sparse_attention_prefill(_dtype_code(q), B, Hq, Hkv, Tq, Tk, d, _desc(q), _desc(k), _desc(v),
                                                 ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), _desc(o),
-                                                lse.data_ptr() if lse is not None else None, _stream(q, stream)))
+                                                lse.data_ptr() if lse is not None else None, *_ws_args(ws),
+                                                _stream(q, stream)))
     return (o, lse) if return_lse else o
 
 
@@ -353,9 +378,10 @@ def sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, max_seq_
     o = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, Hq, Tq), dtype=torch.float32, device=q.device) if return_lse else None
     with torch.cuda.device(q.device):
+        ws = _workspace(HIP_OP_DECODE, _dtype_code(q), B, Hq, Hkv, Tq, int(max_seq_len), d, p, q.device, stream)
         _check(lib.hip_sparse_attention_decode(_dtype_code(q), B, Hq, Hkv, Tq, d, _desc(q), ctypes.byref(pg),
                                                ctypes.byref(p), idx.data_ptr(), cnt.data_ptr(), _desc(o),
-                                               lse.data_ptr() if lse is not None else None, None, 0,
+                                               lse.data_ptr() if lse is not None else None, *_ws_args(ws),
                                                _stream(q, stream)))
     return (o, lse) if return_lse else o
 

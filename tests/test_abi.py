@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     lib = H.load()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.hip_version() == 120
+    assert lib.hip_version() == 200
 
 
 def test_nm_dynamic_symbols():
@@ -54,17 +54,28 @@ def test_num_blocks_and_workspace():
     assert H.num_blocks(512, 2) == 256
     assert H.num_blocks(512, 3) == 0  # k % b_k != 0 (G12)
     p = H._params(512, 32, 2, True)
-    assert lib.hip_workspace_bytes(H.HIP_OP_DECODE, H.HIP_DTYPE_BF16, 16, 32, 8, 1, 131072, 128, ctypes.byref(p)) == 0
+    ws = lambda op, B, Hq, Tq, pp=p, d=128: lib.hip_workspace_bytes(op, H.HIP_DTYPE_BF16, B, Hq, 8, Tq, 131072, d,  # noqa: E731
+                                                                ctypes.byref(pp))
+    # every op: the launch's 256-byte job counter
+    assert ws(H.HIP_OP_MASK, 1, 32, 32768) == 256
+    assert ws(H.HIP_OP_PREFILL, 1, 32, 32768) == 256
+    # single-row attention units (C3: 16 x 32 heads): + arrivals (256-aligned) + 8 partials of 132 floats
+    assert ws(H.HIP_OP_DECODE, 16, 32, 1) == 256 + 2048 + 512 * 8 * 132 * 4
+    p1 = H._params(512, 1, 2, True)
+    assert ws(H.HIP_OP_PREFILL, 2, 4, 3, pp=p1) == 256 + 256 + 24 * 8 * 132 * 4
+    assert ws(H.HIP_OP_DECODE, 16, 32, 1, d=64) == 256            # d = 64 decode: no tcgen05 split-K
+    assert ws(H.HIP_OP_DECODE, 64, 128, 1) == 256                 # > 4096 units: no split-K region
+    assert lib.hip_workspace_bytes(H.HIP_OP_DECODE, H.HIP_DTYPE_BF16, 0, 32, 8, 1, 10, 128, ctypes.byref(p)) == 0
 
 
 def _call_mask(dtype=H.HIP_DTYPE_BF16, B=1, Hq=2, Hkv=1, Tq=64, Tk=64, d=128, params=None, qptr=0x1000, kptr=0x2000,
-               st=(8192, 8192, 128), idx=0x3000, cnt=0x4000):
+               st=(8192, 8192, 128), idx=0x3000, cnt=0x4000, ws=0x8000, ws_bytes=256):
     lib = H.load()
     p = params if params is not None else H._params(512, 32, 2, True)
     q = H.TensorDesc(qptr, *st)
     k = H.TensorDesc(kptr, *st)
     return lib.hip_mask_estimate(dtype, B, Hq, Hkv, Tq, Tk, d, q, k, None, ctypes.byref(p) if p else None, idx, cnt,
-                                 None, 0, None)
+                                 ws, ws_bytes, None)
 
 
 @pytest.mark.parametrize("kw,status", [
@@ -83,6 +94,9 @@ def _call_mask(dtype=H.HIP_DTYPE_BF16, B=1, Hq=2, Hkv=1, Tq=64, Tk=64, d=128, pa
     (dict(qptr=0x1008), H.HIP_ERROR_INVALID_VALUE),               # misaligned
     (dict(st=(8192, 8192, 100)), H.HIP_ERROR_INVALID_VALUE),      # row stride not 16-byte multiple
     (dict(idx=0), H.HIP_ERROR_INVALID_VALUE),
+    (dict(ws=None, ws_bytes=0), H.HIP_ERROR_WORKSPACE),           # workspace required (job counter)
+    (dict(ws_bytes=255), H.HIP_ERROR_WORKSPACE),                  # shorter than hip_workspace_bytes
+    (dict(ws=0x8008), H.HIP_ERROR_WORKSPACE),                     # misaligned
 ])
 def test_validation_before_launch(kw, status):
     if kw.get("params") is False:

@@ -733,3 +733,78 @@ def test_vote_max_size(orc):
         oi, oc = orc.vote(I, C, theta, tau)
         torch.cuda.synchronize()
         assert np.array_equal(gi.cpu().numpy(), oi) and np.array_equal(gc.cpu().numpy(), oc)
+
+
+# ------------------------------------------------------------------------------------------------
+# Split-K single-row attention (decode) and the dynamic job queue
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("B,Hq,Hkv,sw", [
+    (2, 4, 1, False),    # 8 units: S = 8, most splits empty (<= 4 chunks)
+    (16, 32, 8, True),   # 512 units (the C3 shape): S = 3, sink + window extras
+    (20, 32, 8, False),  # 640 units >= the GPU's 592 slots: no split, dynamic queue
+])
+def test_decode_split_k_parity(orc, B, Hq, Hkv, sw):
+    """Split-K partials merged in the kernel (max-rescaled softmax states) == the fp64 oracle on the
+    oracle's own selection, for split counts 8 / 3 / 1 (units below / near / above the CTA slots),
+    ragged sequence lengths (some shorter than one chunk, so whole splits are empty), bf16 2e-2,
+    lse 1e-3."""
+    d, k, bk, ps = 128, 512, 2, 16
+    rng = np.random.default_rng(B)
+    seq = [int(x) for x in rng.integers(1, 3000, size=B)]
+    seq[0] = 1
+    T = max(seq)
+    Q = synth.gen_decode_q(B, Hq, d, seed=31 + B, dtype=torch.bfloat16)
+    kp, vp, bt, sl = synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=31 + B, dtype=torch.bfloat16)
+    oi, oc = orc.mask_paged(Q, kp, bt, sl, k, 1, bk, True)
+    kw = dict(sink=32, window=128) if sw else {}
+    o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T,
+                                       torch.from_numpy(oi).cuda(), torch.from_numpy(oc).cuda(), k_budget=k, b_q=1,
+                                       b_k=bk, causal=True, return_lse=True, **kw)
+    torch.cuda.synchronize()
+    Oo, lo = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, 1, bk, True, oi, oc, **kw)
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
+    assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
+
+
+def test_single_row_prefill_split_k_parity(orc):
+    """T_q = 1 through the contiguous prefill entry also takes the split-K path (same kernel)."""
+    B, Hq, Hkv, Tk, d, k, bk = 3, 4, 2, 2500, 128, 256, 2
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, 1, Tk, d, "iid", seed=41, dtype=torch.bfloat16)
+    idx, cnt = synth.gen_block_indices(B, Hq, 1, k // bk, torch.full((B, Hq, 1), -(-Tk // bk)), seed=41)
+    o, lse = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx.cuda(), cnt.cuda(), k_budget=k, b_q=1,
+                                        b_k=bk, causal=True, return_lse=True)
+    torch.cuda.synchronize()
+    Oo, lo = orc.sparse_attention(Q, K, V, k, 1, bk, True, idx.numpy(), cnt.numpy())
+    assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
+    fin = np.isfinite(lo)
+    assert np.array_equal(fin, np.isfinite(lse.cpu().numpy()))
+    assert np.abs(lse.cpu().numpy()[fin] - lo[fin]).max() <= 1e-3
+
+
+def test_concurrent_streams_own_workspaces():
+    """Each call gets its own workspace (job counter, split-K partials), so the same launches
+    issued concurrently on two streams give the bits of the sequential run."""
+    B, Hq, Hkv, d, k, bk, ps = 16, 32, 8, 128, 512, 2, 64
+    seq = [4096] * B
+    q = synth.gen_decode_q(B, Hq, d, seed=51).cuda()
+    kp, vp, bt, sl = (x.cuda() for x in synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=51))
+    Q, K, V = (x.cuda() for x in synth.gen_qkv(1, 8, 8, 8192, 8192, d, "llm", seed=52))
+    kw = dict(k_budget=k, b_q=1, b_k=bk, causal=True)
+    ref_i, ref_c = H.mask_estimate_paged(q, kp, bt, sl, 4096, **kw)
+    ref_o = H.sparse_attention_decode(q, kp, vp, bt, sl, 4096, ref_i, ref_c, **kw)
+    ref_pi, ref_pc = H.mask_estimate(Q, K)
+    ref_po = H.sparse_attention_prefill(Q, K, V, ref_pi, ref_pc)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        s1.wait_stream(torch.cuda.current_stream())
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s1):
+            i1, c1 = H.mask_estimate_paged(q, kp, bt, sl, 4096, **kw)
+            o1 = H.sparse_attention_decode(q, kp, vp, bt, sl, 4096, i1, c1, **kw)
+        with torch.cuda.stream(s2):
+            pi, pc = H.mask_estimate(Q, K)
+            po = H.sparse_attention_prefill(Q, K, V, pi, pc)
+        torch.cuda.synchronize()
+        assert torch.equal(i1, ref_i) and torch.equal(o1, ref_o)
+        assert torch.equal(pi, ref_pi) and torch.equal(po, ref_po)
