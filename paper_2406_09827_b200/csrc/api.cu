@@ -317,7 +317,10 @@ hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* op = static_cast<char*>(const_cast<void*>(o.ptr));
   cudaError_t e;
-  if (dtype == HIP_DTYPE_BF16 && hip::attn_tc_supported(sh))
+  if (dtype == HIP_DTYPE_BF16 && hip::attn_row1_supported(sh))
+    e = hip::launch_attn_row1(sh, qs, ks, vs, block_idx, block_cnt, scale, op, o.stride_b, o.stride_h, o.stride_t, lse,
+                              st, sms);
+  else if (dtype == HIP_DTYPE_BF16 && hip::attn_tc_supported(sh))
     e = hip::launch_attn_tc(sh, qs, ks, vs, block_idx, block_cnt, scale, op, o.stride_b, o.stride_h, o.stride_t, lse,
                             st, sms);
   else if (hip::attn_decode_supported(sh))
@@ -357,7 +360,10 @@ hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H
   // tcgen05 path: physical row index page * (page stride in rows) + offset must fit in int32
   const bool tc_rows = ks.sp_rows > 0 && paged->num_pages > 0 &&
                        (int64_t)paged->num_pages * ks.sp_rows < ((int64_t)1 << 31);
-  if (dtype == HIP_DTYPE_BF16 && tc_rows && hip::attn_tc_supported(sh))
+  if (dtype == HIP_DTYPE_BF16 && tc_rows && hip::attn_row1_supported(sh))
+    e = hip::launch_attn_row1(sh, qs, ks, vs, block_idx, block_cnt, scale, op, o.stride_b, o.stride_h, o.stride_t, lse,
+                              st, sms);
+  else if (dtype == HIP_DTYPE_BF16 && tc_rows && hip::attn_tc_supported(sh))
     e = hip::launch_attn_tc(sh, qs, ks, vs, block_idx, block_cnt, scale, op, o.stride_b, o.stride_h, o.stride_t, lse,
                             st, sms);
   else if (hip::attn_decode_supported(sh))

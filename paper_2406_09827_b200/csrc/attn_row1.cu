@@ -1,0 +1,370 @@
+// attn_row1.cu — block-sparse attention for single-row query blocks (decode: T_q = 1, or b_q = 1),
+// bf16, d = 128, contiguous or paged K/V (Eq. 2-3; paged decode P:451, Alg. 2 line
+// "fused sparse attention" P:612).
+//
+// One query row against <= k selected keys is a vector-matrix product: "tensor units cannot help"
+// (P:1053-1054), the kernel is HBM-bound, and what sets its speed is how many bytes each unit keeps
+// in flight and how little else sits on its serial path.  So, unlike the prefill kernel (attn_tc,
+// tcgen05), the math here runs on the CUDA cores straight from shared memory:
+//   * items of 32 keys = 32 K rows + 32 V rows (16 KB) stream through a 3-slot ring of cp.async
+//     gathers (16 lanes per 256-byte row: whole sectors, no L1); completion is tracked on mbarriers
+//     (cp.async.mbarrier.arrive.noinc -> "full", one arrival per warp -> "empty"), so no CTA-wide
+//     barrier sits between items and a slot is refilled as soon as the four warps have read it;
+//   * warp w owns keys 8w..8w+7 of every item: 4 lanes per key each dot a quarter of d (q in
+//     registers), two shuffles complete q.k; the warp keeps its own online softmax state (max, sum,
+//     O[4 columns per lane]), so the per-item softmax needs shuffles only; PV reads V rows with
+//     conflict-free 8-byte lanes; the four warp states are merged once per unit;
+//   * probabilities stay fp32 (no bf16 rounding of P as in the tensor-core kernel).
+// Rows are staged in shared memory with the 16-byte chunk index XOR 4 * (key & 1), which makes the
+// QK reads (lanes of two keys x four quarters) bank-conflict-free per quarter warp.
+// Split-K (jobs = units x S when the units leave CTA slots idle): job (u, sp) takes items
+// [sp n / S, (sp + 1) n / S) of its unit and leaves an unnormalised partial state in the workspace;
+// the last split to arrive merges them (max-rescaled, like the warp states).
+#include "kernels.h"
+#include "sinkwin.cuh"
+
+namespace hip {
+
+constexpr int kR1Threads = 128;
+constexpr int kR1Slots = 3;
+constexpr uint32_t kR1Item = 16384;            // 32 K rows + 32 V rows of 256 bytes
+constexpr int kR1Tok = 768;                    // <= 512 selected keys + <= 256 sink / window tokens
+constexpr int kR1MaxN = 512;                   // n = k / b_k <= kR1MaxN (the index row staged in the prologue)
+constexpr int kR1BtStage = (int)(kR1Item / 4) - kR1MaxN;  // block-table entries staged with it (3584)
+constexpr float kR1Log2e = 1.4426950408889634f;
+constexpr float kR1Ln2 = 0.6931471805599453f;
+
+struct Row1Smem {
+  static constexpr uint32_t ring = 0;
+  static constexpr uint32_t tok = ring + kR1Slots * kR1Item;      // [kR1Tok] row of each key slot (-1: none)
+  static constexpr uint32_t xlist = tok + kR1Tok * 4;              // [kMaxExtra] sink / window tokens
+  static constexpr uint32_t merge = xlist + kMaxExtra * 4;         // [4][128] O + [4] max + [4] sum, scan scratch
+  static constexpr uint32_t bar = merge + (4 * 128 + 8 + 8) * 4;   // full[3], empty[3]
+  static constexpr uint32_t jq = bar + 2 * kR1Slots * 8;           // JobQueue slots
+  static constexpr uint32_t flag = jq + 16;
+  static constexpr uint32_t total = flag + 16;
+};
+
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar) : "memory");
+}
+
+template <bool kPaged, bool kSW, bool kSplit>
+__global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
+                                                                   const int32_t* __restrict__ idx,
+                                                                   const int32_t* __restrict__ cnt, float scale_log2,
+                                                                   char* __restrict__ o, int64_t osb, int64_t osh,
+                                                                   int64_t ost, float* __restrict__ lse) {
+  extern __shared__ __align__(16) char smem[];
+  using L = Row1Smem;
+  const uint32_t sb = smem_u32(smem);
+  int* tok = reinterpret_cast<int*>(smem + L::tok);
+  int* xlist = reinterpret_cast<int*>(smem + L::xlist);
+  float* mo = reinterpret_cast<float*>(smem + L::merge);          // [4][128]
+  float* mm = mo + 4 * 128;                                        // [4] warp maxima
+  float* ml = mm + 4;                                              // [4] warp sums
+  int* scan = reinterpret_cast<int*>(ml + 4);                      // [8] build_extra scratch
+  int* flag = reinterpret_cast<int*>(smem + L::flag);            // split-K: "this job merges"
+  int* scnt = flag + 1;                                            // the unit's block count
+  const uint32_t full0 = sb + L::bar, empty0 = full0 + 8 * kR1Slots;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kR1Slots; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(full0 + 8 * s), "r"(kR1Threads) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(empty0 + 8 * s), "r"(4) : "memory");
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int lbk = 31 - __clz(sh.bk);
+  // QK lanes: key j = lane / 4 of the warp's 8, quarter p = lane % 4 (16-byte chunks p + 4 i, i < 4)
+  const int kj = lane >> 2, kp = lane & 3;
+  uint32_t g = 0;  // ring items issued / consumed by this CTA so far (slot g % 3, parity (g / 3) & 1)
+
+  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int S = kSplit ? sh.splits : 1;
+  JobQueue jq(sh.sched, smem + L::jq);
+  for (int64_t jb = blockIdx.x; jb < units * S; jb = jq.next(jb)) {
+    jq.claim();
+    const int64_t u = kSplit ? jb / S : jb;
+    const int sp = kSplit ? (int)(jb - u * S) : 0;
+    int b, h, q;
+    unit_coords(sh, u, b, h, q);
+    const int hk = h / (sh.Hq / sh.Hkv);
+    const int Tk = seq_len(sh, b);
+    const int64_t lin = mask_lin(sh, b, h, q);
+    const int64_t tpos = (int64_t)q * sh.bq + (Tk - sh.Tq);  // the row's key position (G7)
+    const int nkb = (Tk + sh.bk - 1) / sh.bk;
+    // Prologue, one global round trip: the unit's count, its index row and (paged) the block-table
+    // entries of its sequence are loaded together into ring slot 2 (free between jobs: every item of
+    // the previous job has been consumed), then build_extra and the row staging work from shared
+    // memory — no chain of dependent global loads (count -> indices -> pages) before the first gather.
+    int* sblk = reinterpret_cast<int*>(smem + L::ring + 2 * kR1Item);       // [n] selected blocks
+    int* sbt = sblk + kR1MaxN;                                              // [<= kR1BtStage] pages
+    const int32_t* blk = idx + lin * sh.n;
+    const int npg = kPaged ? (Tk + ks.page_size - 1) / ks.page_size : 0;
+    const bool bt_staged = kPaged && npg <= kR1BtStage;
+    for (int i = tid; i < sh.n; i += kR1Threads) sblk[i] = __ldg(blk + i);
+    if (bt_staged) {
+      const int32_t* btrow = ks.block_table + (int64_t)b * ks.max_pages;
+      for (int i = tid; i < npg; i += kR1Threads) sbt[i] = __ldg(btrow + i);
+    }
+    if (tid == 0) *scnt = __ldg(cnt + lin);
+    __syncthreads();
+    const int c = min(max(*scnt, 0), sh.n);
+    const int nkeys = c * sh.bk;
+    const int ne = kSW ? build_extra<kR1Threads, true>(sblk, c, lbk, Tk, tpos, tpos, sh.causal, sh.sink, sh.window,
+                                                       xlist, scan)
+                       : 0;
+    const int nall = nkeys + ne;
+    const int nit_all = (nall + 31) >> 5;
+    const int i_lo = kSplit ? sp * nit_all / S : 0;
+    const int nit = kSplit ? (sp + 1) * nit_all / S - i_lo : nit_all;
+    const int k_lo = i_lo * 32, nk = min(nit * 32, nall - k_lo);
+
+    // key slots of this job -> physical rows (-1: not a key, or not visible to the row)
+    for (int kk = tid; kk < nit * 32; kk += kR1Threads) {
+      const int k = k_lo + kk;
+      int row = -1;
+      if (kk < nk) {
+        int s;
+        bool ok;
+        if (k < nkeys) {
+          const int j = min(max(sblk[k >> lbk], 0), nkb - 1);
+          s = (j << lbk) + (k & ((1 << lbk) - 1));
+          ok = s < Tk && (!sh.causal || s <= tpos);
+        } else {
+          s = xlist[k - nkeys];
+          ok = extra_visible(s, tpos, sh.causal, sh.sink, sh.window);
+        }
+        if (ok) {
+          if constexpr (kPaged) {
+            const uint32_t us = (uint32_t)s;
+            const uint32_t pi = ks.page_shift >= 0 ? (us >> ks.page_shift) : (us / (uint32_t)ks.page_size);
+            const uint32_t off = us - pi * (uint32_t)ks.page_size;
+            const int64_t page = bt_staged ? (int64_t)sbt[pi] : __ldg(ks.block_table + (int64_t)b * ks.max_pages + pi);
+            row = (int)(page * ks.sp_rows + off);
+          } else {
+            row = s;
+          }
+        }
+      }
+      tok[kk] = row;
+    }
+    // this lane's quarter of q: chunks kp + 4 i, as bf16 pairs
+    uint32_t qv[16];
+    {
+      const char* qr = q_ptr(qsrc, b, h, (int64_t)q * sh.bq);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(qr + (kp + 4 * i) * 16));
+        qv[4 * i] = t.x; qv[4 * i + 1] = t.y; qv[4 * i + 2] = t.z; qv[4 * i + 3] = t.w;
+      }
+    }
+    __syncthreads();  // tok visible
+
+    const char* kbase = ks.base + ((kPaged ? 0 : b * ks.sb) + hk * ks.sh) * (int64_t)ks.esize;
+    const char* vbase = vs.base + ((kPaged ? 0 : b * vs.sb) + hk * vs.sh) * (int64_t)vs.esize;
+    const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
+    // item i of the job -> ring item g0 + i.  Thread t copies pieces p = 128 j + t (j < 8): row p / 16
+    // of the item (< 32: K row of key p / 16, else V row of key p / 16 - 32), 16-byte chunk p % 16.
+    const uint32_t g0 = g;
+    auto issue = [&](int i) {
+      const uint32_t gi = g0 + (uint32_t)i, slot = gi % kR1Slots;
+      if (gi >= (uint32_t)kR1Slots) mbar_wait_u32(empty0 + 8 * slot, ((gi / kR1Slots) - 1) & 1u);
+      const uint32_t dst0 = sb + L::ring + slot * kR1Item;
+      const int cc = tid & 15;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = 8 * j + (tid >> 4);  // 0..63
+        const int key = r & 31;
+        const int row = tok[i * 32 + key];
+        const bool isv = r >= 32;
+        const char* src = (isv ? vbase : kbase) + (uint64_t)(uint32_t)max(row, 0) * (isv ? vrow : krow) + cc * 16;
+        const uint32_t dst = dst0 + (isv ? 8192u : 0u) + key * 256 + ((cc ^ ((key & 1) << 2)) << 4);
+        cp_async16(dst, src, row >= 0 ? 16u : 0u);
+      }
+      cp_async_mbar_arrive_noinc(full0 + 8 * slot);
+    };
+
+    float m = -INFINITY, l = 0.f, ov[4] = {0.f, 0.f, 0.f, 0.f};
+    const int pre = min(nit, kR1Slots);
+    for (int i = 0; i < pre; ++i) issue(i);
+    for (int i = 0; i < nit; ++i) {
+      const uint32_t gi = g0 + (uint32_t)i, slot = gi % kR1Slots;
+      mbar_wait_u32(full0 + 8 * slot, (gi / kR1Slots) & 1u);
+      const char* it = smem + L::ring + slot * kR1Item;
+      // q . k for key 8 warp + kj, quarter kp
+      const int key = 8 * warp + kj;
+      const char* kr = it + key * 256;
+      float dot = 0.f;
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int ch = kp + 4 * c4;
+        const uint4 kv = *reinterpret_cast<const uint4*>(kr + ((ch ^ ((key & 1) << 2)) << 4));
+        const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          dot = fmaf(bf16_lo(qv[4 * c4 + e]), bf16_lo(kw[e]), dot);
+          dot = fmaf(bf16_hi(qv[4 * c4 + e]), bf16_hi(kw[e]), dot);
+        }
+      }
+      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+      const bool valid = tok[i * 32 + key] >= 0;
+      const float x = valid ? dot * scale_log2 : -INFINITY;
+      // warp online softmax over its 8 keys
+      float cm = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 4));
+      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 8));
+      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
+      const float mn = fmaxf(m, cm);
+      if (mn != m) {  // warp-uniform
+        const float cf = m == -INFINITY ? 0.f : ex2_approx(m - mn);
+        l *= cf;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ov[e] *= cf;
+        m = mn;
+      }
+      const float p = x == -INFINITY ? 0.f : ex2_approx(x - m);
+      float ps = p + __shfl_xor_sync(0xffffffffu, p, 4);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+      l += ps;
+      // O[4 lane .. 4 lane + 3] += sum_j p_j V[8 warp + j]
+      const char* vr0 = it + 8192;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float pj = __shfl_sync(0xffffffffu, p, 4 * j);
+        const int vk = 8 * warp + j;
+        const uint2 vv = *reinterpret_cast<const uint2*>(vr0 + vk * 256 + ((((lane >> 1) ^ ((vk & 1) << 2))) << 4) +
+                                                         (lane & 1) * 8);
+        ov[0] = fmaf(pj, bf16_lo(vv.x), ov[0]);
+        ov[1] = fmaf(pj, bf16_hi(vv.x), ov[1]);
+        ov[2] = fmaf(pj, bf16_lo(vv.y), ov[2]);
+        ov[3] = fmaf(pj, bf16_hi(vv.y), ov[3]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+      if (i + kR1Slots < nit) issue(i + kR1Slots);
+    }
+    g = g0 + (uint32_t)nit;
+
+    // merge the four warp states: M = max_w m_w, O = sum_w 2^(m_w - M) O_w, L = sum_w 2^(m_w - M) l_w
+    *reinterpret_cast<float4*>(mo + warp * 128 + 4 * lane) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+    if (lane == 0) {
+      mm[warp] = m;
+      ml[warp] = l;
+    }
+    __syncthreads();
+    const int d = tid;
+    float M = fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3]));
+    float O = 0.f, Ls = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        if (mm[w] == -INFINITY) continue;
+        const float f = ex2_approx(mm[w] - M);
+        O = fmaf(f, mo[w * 128 + d], O);
+        Ls = fmaf(f, ml[w], Ls);
+      }
+    }
+    if constexpr (kSplit) {
+      // publish this split's partial (O unnormalised, M, L), the last split of the unit merges
+      constexpr int PS = kSplitStride;
+      float* my = sh.part + (u * S + sp) * PS;
+      __stcg(my + d, O);
+      if (d == 0) {
+        __stcg(my + 128, M);
+        __stcg(my + 129, Ls);
+      }
+      __threadfence();
+      __syncthreads();
+      if (d == 0) *flag = atomicAdd(sh.arrive + u, 1u) == (unsigned)(S - 1);
+      __syncthreads();
+      if (!*flag) continue;
+      __threadfence();
+      const float* pu = sh.part + u * S * PS;
+      M = -INFINITY;
+      for (int s = 0; s < S; ++s) M = fmaxf(M, __ldcg(pu + s * PS + 128));
+      O = 0.f;
+      Ls = 0.f;
+      if (M != -INFINITY) {
+        for (int s = 0; s < S; ++s) {
+          const float ms = __ldcg(pu + s * PS + 128);
+          if (ms == -INFINITY) continue;
+          const float f = ex2_approx(ms - M);
+          O = fmaf(f, __ldcg(pu + s * PS + d), O);
+          Ls = fmaf(f, __ldcg(pu + s * PS + 129), Ls);
+        }
+      }
+    }
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(o + (b * osb + h * osh + (int64_t)q * sh.bq * ost) * 2);
+    orow[d] = __float2bfloat16_rn(Ls > 0.f ? O / Ls : 0.f);  // a row with no visible key: O = 0 (G13)
+    if (lse && d == 0)
+      lse[((int64_t)b * sh.Hq + h) * sh.Tq + (int64_t)q * sh.bq] = Ls > 0.f ? M * kR1Ln2 + logf(Ls) : -INFINITY;
+    __syncthreads();  // merge scratch and tok are rewritten by the next job
+  }
+}
+
+// Single-row query blocks (every unit one row: b_q = 1 or T_q = 1), bf16, d = 128, up to 512
+// selected keys + 256 sink / window tokens (wider union masks use attn_tc).
+bool attn_row1_supported(const Shape& sh) {
+  return sh.d == 128 && std::min(sh.bq, sh.Tq) == 1 && (int64_t)sh.n * sh.bk + kMaxExtra <= kR1Tok && sh.n <= kR1MaxN &&
+         sh.sink + sh.window <= kMaxExtra;
+}
+
+template <bool kPaged, bool kSW, bool kSplit>
+static cudaError_t launch_r1(const Shape& s2, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
+                             const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
+                             float* lse, cudaStream_t stream, int64_t grid) {
+  auto kern = attn_row1_kernel<kPaged, kSW, kSplit>;
+  int per_sm = 1;
+  cudaError_t e = persistent_ctas(kern, kR1Threads, Row1Smem::total, 0, &per_sm);  // sets the smem attribute
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, kR1Threads, Row1Smem::total, stream>>>(s2, qs, ks, vs, idx, cnt, sm_scale * kR1Log2e, o, osb,
+                                                                osh, ost, lse);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_row1(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
+                             const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
+                             float* lse, cudaStream_t stream, int num_sms) {
+  int per_sm = 1;
+  cudaError_t e = persistent_ctas(attn_row1_kernel<false, false, false>, kR1Threads, Row1Smem::total, 0, &per_sm);
+  if (e != cudaSuccess) return e;
+  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
+  const int64_t slots = (int64_t)num_sms * per_sm;
+  Shape s2 = sh;
+  // split-K only to fill CTA slots the units leave idle (never a second wave)
+  s2.splits = 1;
+  if (sh.part && sh.arrive && units <= kSplitMaxUnits)
+    s2.splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitMax, slots / units));
+#ifdef HIPATTN_TUNING
+  if (const char* e2 = getenv("HIPATTN_SPLITS"))
+    if (sh.part) s2.splits = std::max(1, std::min(kSplitMax, atoi(e2)));
+#endif
+  if (s2.splits > 1) {
+    e = cudaMemsetAsync(s2.arrive, 0, (size_t)units * sizeof(unsigned int), stream);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t jobs = units * s2.splits;
+  const int64_t grid = std::min<int64_t>(jobs, slots);
+  if ((e = setup_queue(s2, jobs, grid, stream)) != cudaSuccess) return e;
+  const bool sw = sh.sink > 0 || sh.window > 0;
+#define HIP_R1(P, W, SP) \
+  return launch_r1<P, W, SP>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid)
+  if (s2.splits > 1) {
+    if (ks.paged) { if (sw) HIP_R1(true, true, true); HIP_R1(true, false, true); }
+    if (sw) HIP_R1(false, true, true);
+    HIP_R1(false, false, true);
+  }
+  if (ks.paged) { if (sw) HIP_R1(true, true, false); HIP_R1(true, false, false); }
+  if (sw) HIP_R1(false, true, false);
+  HIP_R1(false, false, false);
+#undef HIP_R1
+}
+
+}  // namespace hip

@@ -69,55 +69,8 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   return v[0];
 }
 
-// Split-K epilogue of a single-row job (u, sp) of S (128 threads, thread = output column d).  The
-// partial is the job's UNNORMALISED O (fp32, relative to its running max), that max (log2 units) and
-// its two probability sums (bf16-rounded p, which normalises O, and unrounded p, for lse); stored
-// with st.cg, published by a fence + one atomic arrival per job.  The job that arrives last reads
-// the S partials (ld.cg, L2) and merges them exactly like chunks of one softmax:
-//     M = max_s m_s,  O = sum_s 2^(m_s - M) O_s,  L = sum_s 2^(m_s - M) l_s,  o = O / L.
-// An empty split (kHasO = false) contributes max -inf and zero sums.
-template <bool kHasO>
-__device__ __forceinline__ void split_finish(const Shape& sh, int64_t u, int sp, int S, int b, int h, int q,
-                                             float ov, const float* mrun, const float* lrun, const float* lurun,
-                                             char* o, int64_t osb, int64_t osh, int64_t ost, float* lse, int* flag) {
-  constexpr int D = 128, PS = kSplitStride;
-  const int d = threadIdx.x;
-  float* my = sh.part + (u * S + sp) * PS;
-  __stcg(my + d, kHasO ? ov : 0.f);
-  if (d == 0) {
-    __stcg(my + D, kHasO ? mrun[0] : -INFINITY);
-    __stcg(my + D + 1, kHasO ? lrun[0] : 0.f);
-    __stcg(my + D + 2, kHasO ? lurun[0] : 0.f);
-  }
-  __threadfence();
-  __syncthreads();
-  if (d == 0) *flag = atomicAdd(sh.arrive + u, 1u) == (unsigned)(S - 1);
-  __syncthreads();
-  if (!*flag) return;
-  __threadfence();
-  const float* pu = sh.part + u * S * PS;
-  float M = -INFINITY;
-  for (int s = 0; s < S; ++s) M = fmaxf(M, __ldcg(pu + s * PS + D));
-  float O = 0.f, L = 0.f, Lu = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < S; ++s) {
-      const float ms = __ldcg(pu + s * PS + D);
-      if (ms == -INFINITY) continue;
-      const float w = ex2_approx(ms - M);
-      O = fmaf(w, __ldcg(pu + s * PS + d), O);
-      L = fmaf(w, __ldcg(pu + s * PS + D + 1), L);
-      Lu = fmaf(w, __ldcg(pu + s * PS + D + 2), Lu);
-    }
-  }
-  __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(o + (b * osb + h * osh + (int64_t)q * sh.bq * ost) * 2);
-  orow[d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
-  if (lse && d == 0)
-    lse[((int64_t)b * sh.Hq + h) * sh.Tq + (int64_t)q * sh.bq] = Lu > 0.f ? M * kATLn2 + logf(Lu) : -INFINITY;
-}
-
-// kSW: sink / sliding-window tokens enabled; kSplit: split-K jobs of single-row units (separate
-// instantiations, so the plain path pays nothing for either).
-template <bool kPaged, bool kSW, int TOK, bool kSplit>
+// kSW: sink / sliding-window tokens enabled (a separate instantiation, so the plain path pays nothing).
+template <bool kPaged, bool kSW, int TOK>
 __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
                                                                 const int32_t* __restrict__ idx,
                                                                 const int32_t* __restrict__ cnt, float scale_log2,
@@ -158,15 +111,9 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   const int lbk = 31 - __clz(sh.bk);
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  // split-K (single-row units, sh.splits = S > 1): job (u, sp) runs chunks [sp nch / S, (sp + 1) nch / S)
-  // of unit u and leaves an unnormalised partial (O, running max, sums) in the workspace; the last
-  // split to arrive merges the S partials (lse-style rescale) and writes the row.
-  const int S = kSplit ? sh.splits : 1;
   JobQueue jq(sh.sched, base + L::jq);
-  for (int64_t jb = blockIdx.x; jb < units * S; jb = jq.next(jb)) {
+  for (int64_t u = blockIdx.x; u < units; u = jq.next(u)) {
     jq.claim();
-    const int64_t u = kSplit ? jb / S : jb;
-    const int sp = kSplit ? (int)(jb - u * S) : 0;
     int b, h, q;
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
@@ -183,16 +130,9 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
                                                  sh.sink, sh.window, xlist, reinterpret_cast<int*>(red))
                        : 0;
     const int nall = nkeys + ne;
-    const int nch_all = (nall + 127) / 128;
+    const int nch = (nall + 127) / 128;
     const int32_t* blk = idx + lin * sh.n;
-    // this job's chunks [c_lo, c_lo + nch)
-    const int c_lo = kSplit ? sp * nch_all / S : 0;
-    const int nch = kSplit ? (sp + 1) * nch_all / S - c_lo : nch_all;
 
-    if (kSplit && nch == 0) {  // an empty split: a neutral partial (max -inf, sums 0)
-      split_finish<false>(sh, u, sp, S, b, h, q, 0u, mrun, lrun, lurun, o, osb, osh, ost, lse, flag);
-      continue;
-    }
     if (nch == 0) {  // no selected block: O = 0, lse = -inf (G13)
       for (int i = threadIdx.x; i < rows_q * 16; i += kATThreads) {
         const int t = i >> 4, c16 = i & 15;
@@ -213,8 +153,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     // row of every selected key slot (or -1 past T_k / past cnt), staged once per unit: the token
     // index for contiguous K/V, the physical row page * (page stride in rows) + offset for a paged
     // cache (K and V share the block table and strides), so the gathers carry no dependent load
-    for (int kk = threadIdx.x; kk < nch * 128; kk += kATThreads) {
-      const int k = c_lo * 128 + kk;
+    for (int k = threadIdx.x; k < nch * 128; k += kATThreads) {
       int s = -1;
       if (k < nall) {
         if (k < nkeys) {
@@ -236,7 +175,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
           if (k >= nkeys && s >= 0) s |= kExtraBit;  // contiguous: the token itself, extras flagged
         }
       }
-      tok[kk] = s;
+      tok[k] = s;
     }
     if (threadIdx.x < 32) {
       mrun[threadIdx.x] = -INFINITY;
@@ -248,7 +187,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     const char* vbase = vs.base + ((kPaged ? 0 : b * vs.sb) + hk * vs.sh) * (int64_t)vs.esize;
     const uint32_t krow = (uint32_t)(ks.st * ks.esize), vrow = (uint32_t)(vs.st * vs.esize);
 
-    // item i: chunk ch = c_lo + (i >> 2) (tok[] holds this job's chunks from c_lo); (i & 3) = 0, 1: K_ch d-half 0 / 1; 2, 3: V_ch keys [0,64) / [64,128)
+    // item i: chunk ch = i >> 2; (i & 3) = 0, 1: K_ch d-half 0 / 1; 2, 3: V_ch keys [0,64) / [64,128)
     // Thread (c8, r0) moves 16-byte chunk c8 of the 8 keys r0 + 16 j (j = 0..7) of every chunk: for
     // K items those 8 rows (one d-half), for V items keys r0 + 16 j' + 64 (kind - 2) of both d-halves.
     // All eight keys share r0's swizzle phase, so the destinations are one base + immediates, and
@@ -257,7 +196,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     const uint32_t dbase = (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + ((c8 ^ (r0 & 7)) << 4));
     int srow[8];  // this thread's 8 key rows of the current chunk (-1: none)
     auto issue = [&](int i) {
-      const int ch = i >> 2, kind = i & 3;  // job-local chunk
+      const int ch = i >> 2, kind = i & 3;
       const uint32_t dst = sb + L::ring + (i & 1) * kATSlot + dbase;
       if (kind == 0) {
 #pragma unroll
@@ -302,7 +241,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
       // Every MMA up to item it - 1 has completed here (each slot is refilled only after its MMA is
       // waited for, and tcgen05 MMAs of one thread complete in order): S of this chunk is final
       // before its softmax, and the previous chunk's PV is done before P is rewritten.
-      const int ch = it >> 2, kind = it & 3;  // job-local chunk (global c_lo + ch)
+      const int ch = it >> 2, kind = it & 3;
       const uint32_t slot = sb + L::ring + (it & 1) * kATSlot;
       if (kind == 2) {
         // ---- online softmax of chunk ch (S^T_ch complete: its last MMA was item it - 1)
@@ -312,13 +251,13 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         int s;  // token position of this lane's key (-1: none)
         bool extra;  // a sink / window token: row-dependent visibility
         {
-          const int k = (c_lo + ch) * 128 + 32 * warp + lane;
+          const int k = ch * 128 + 32 * warp + lane;
           if constexpr (kPaged) {
             s = -1;
             extra = kSW && k >= nkeys;
             if (k < nkeys) {
               if (!kSW && tail1) {  // one row at the last position: every staged key is visible to it
-                s = tok[k - c_lo * 128] >= 0 ? (int)tpos0 : -1;
+                s = tok[k] >= 0 ? (int)tpos0 : -1;
               } else {
                 const int j = min(max(__ldg(blk + (k >> lbk)), 0), nkb - 1);
                 s = (j << lbk) + (k & ((1 << lbk) - 1));
@@ -328,7 +267,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
               s = xlist[k - nkeys];
             }
           } else {
-            s = tok[k - c_lo * 128];
+            s = tok[k];
             extra = kSW && s >= 0 && (s & kExtraBit);
             if (extra) s &= ~kExtraBit;
           }
@@ -460,14 +399,6 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     }
     wait_slot(0);  // the last MMAs (O^T complete)
     wait_slot(1);
-    if (kSplit) {  // split-K job: publish the partial; the last split of the unit merges
-      tc_fence_after();
-      const float ov = tmem_ld_32x32b_x1(tmem_lane + 32);  // O^T lane d, query column 0
-      split_finish<true>(sh, u, sp, S, b, h, q, ov, mrun, lrun, lurun, o, osb, osh, ost, lse, flag);
-      tc_fence_before();
-      __syncthreads();
-      continue;
-    }
     // ---- epilogue: O^T lanes = d, columns = queries -> normalise, stage [32 q][128 d] bf16 in the
     // (now free) ring, then 16-byte coalesced row stores
     if (threadIdx.x < 32) {
@@ -511,54 +442,24 @@ bool attn_tc_supported(const Shape& sh) {
          (int64_t)sh.n * sh.bk <= 4096 && sh.sink + sh.window + sh.bq - 1 <= kMaxExtra;
 }
 
-template <int TOK, bool kSplit>
-static cudaError_t launch_attn_tc_k(const Shape& s2, const QSrc& qs, const RowSrc& ks, const RowSrc& vs,
-                                    const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb,
-                                    int64_t osh, int64_t ost, float* lse, cudaStream_t stream, int64_t grid) {
-  const size_t smem = AttnTCSmemT<TOK>::total + 1024;
-  const bool sw = s2.sink > 0 || s2.window > 0;
-  auto kern = ks.paged ? (sw ? attn_tc_kernel<true, true, TOK, kSplit> : attn_tc_kernel<true, false, TOK, kSplit>)
-                       : (sw ? attn_tc_kernel<false, true, TOK, kSplit> : attn_tc_kernel<false, false, TOK, kSplit>);
-  int per_sm = 1;
-  cudaError_t e = persistent_ctas(kern, kATThreads, smem, 64, &per_sm);  // sets the smem attribute
-  if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, kATThreads, smem, stream>>>(s2, qs, ks, vs, idx, cnt, sm_scale * kATLog2e, o, osb, osh, ost,
-                                                     lse);
-  return cudaGetLastError();
-}
-
 template <int TOK>
 static cudaError_t launch_attn_tc_t(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs,
                                     const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb,
                                     int64_t osh, int64_t ost, float* lse, cudaStream_t stream, int num_sms) {
+  const size_t smem = AttnTCSmemT<TOK>::total + 1024;
+  const bool sw = sh.sink > 0 || sh.window > 0;
+  auto kern = ks.paged ? (sw ? attn_tc_kernel<true, true, TOK> : attn_tc_kernel<true, false, TOK>)
+                       : (sw ? attn_tc_kernel<false, true, TOK> : attn_tc_kernel<false, false, TOK>);
   int per_sm = 1;
-  cudaError_t e = persistent_ctas(attn_tc_kernel<false, false, TOK, false>, kATThreads, AttnTCSmemT<TOK>::total + 1024,
-                                  64, &per_sm);
+  cudaError_t e = persistent_ctas(kern, kATThreads, smem, 64, &per_sm);
   if (e != cudaSuccess) return e;
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  const int64_t slots = (int64_t)num_sms * per_sm;
+  const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms * per_sm);
   Shape s2 = sh;
-  // Split-K for single-row units (decode) only to fill CTA slots the units leave idle:
-  // S = floor(slots / units) <= kSplitMax jobs per unit, never a second wave (measured on C3, 512
-  // units on 592 slots: splitting into 2-8 jobs per unit costs 15-35 % — every job repeats the
-  // dependent idx -> block-table -> row prologue and the merge adds a round trip).
-  s2.splits = 1;
-  if (sh.part && sh.arrive && std::min(sh.bq, sh.Tq) == 1 && units <= kSplitMaxUnits)
-    s2.splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitMax, slots / units));
-#ifdef HIPATTN_TUNING
-  if (const char* e2 = getenv("HIPATTN_SPLITS"))
-    if (sh.part && std::min(sh.bq, sh.Tq) == 1) s2.splits = std::max(1, std::min(kSplitMax, atoi(e2)));
-#endif
-  if (s2.splits > 1) {
-    e = cudaMemsetAsync(s2.arrive, 0, (size_t)units * sizeof(unsigned int), stream);
-    if (e != cudaSuccess) return e;
-  }
-  const int64_t jobs = units * s2.splits;
-  const int64_t grid = std::min<int64_t>(jobs, slots);
-  if ((e = setup_queue(s2, jobs, grid, stream)) != cudaSuccess) return e;
-  if (s2.splits > 1)
-    return launch_attn_tc_k<TOK, true>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid);
-  return launch_attn_tc_k<TOK, false>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid);
+  if ((e = setup_queue(s2, units, grid, stream)) != cudaSuccess) return e;
+  kern<<<(unsigned)grid, kATThreads, smem, stream>>>(s2, qs, ks, vs, idx, cnt, sm_scale * kATLog2e, o, osb, osh, ost,
+                                                     lse);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,

@@ -48,7 +48,7 @@ inline cudaError_t persistent_ctas(K kernel, int threads, size_t smem, int tmem_
   return cudaSuccess;
 }
 
-// Split-K of single-row attention units (attn_tc): at most kSplitMax splits, only for launches of at
+// Split-K of single-row attention units (attn_row1): at most kSplitMax splits, only for launches of at
 // most kSplitMaxUnits units; partial stride kSplitStride floats (O[128], max, sum, unrounded sum, pad).
 constexpr int kSplitMax = 8, kSplitMaxUnits = 4096, kSplitStride = 132;
 
@@ -92,6 +92,14 @@ bool attn_tc_supported(const Shape& sh);
 cudaError_t launch_attn_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
                            const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                            float* lse, cudaStream_t stream, int num_sms);
+
+// Single-row query blocks (decode, b_q = 1), bf16, d = 128: CUDA-core GEMV attention over a
+// 3-slot cp.async ring with mbarrier completion, warp-owned online softmax, split-K to fill idle
+// CTA slots (attn_row1.cu).
+bool attn_row1_supported(const Shape& sh);
+cudaError_t launch_attn_row1(const Shape& sh, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
+                             const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
+                             float* lse, cudaStream_t stream, int num_sms);
 
 // Ensemble vote (vote.cu).
 cudaError_t launch_vote(int n_e, int64_t units, int n_in, const int32_t* idx, const int32_t* cnt, int theta, int tau,

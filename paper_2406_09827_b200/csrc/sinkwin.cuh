@@ -16,15 +16,22 @@ namespace hip {
 constexpr int kMaxExtra = 256;        // sink + window + b_q - 1 <= 256 (checked on the host)
 constexpr int kExtraBit = 1 << 30;    // marks an extra token in the kernels' staged token lists
 
-// Is key block j among the ascending selected blocks blk[0, c)?
+// Is key block j among the ascending selected blocks blk[0, c)?  (blk in global memory, read
+// through the read-only path, or staged in shared memory: kShared.)
+template <bool kShared = false>
+__device__ __forceinline__ int blk_at(const int32_t* blk, int i) {
+  if constexpr (kShared) return blk[i];
+  else return __ldg(blk + i);
+}
+template <bool kShared = false>
 __device__ __forceinline__ bool blk_selected(const int32_t* blk, int c, int j) {
   int lo = 0, hi = c;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    const int v = __ldg(blk + mid);
+    const int v = blk_at<kShared>(blk, mid);
     if (v < j) lo = mid + 1; else hi = mid;
   }
-  return lo < c && __ldg(blk + lo) == j;
+  return lo < c && blk_at<kShared>(blk, lo) == j;
 }
 
 // Row at position p sees extra token s (s < T_k by construction): a sink token, or inside the
@@ -36,7 +43,7 @@ __device__ __forceinline__ bool extra_visible(int s, int64_t p, int causal, int 
 // The extra tokens of one query block (rows at positions p_first..p_last), ascending, into
 // list[0, return).  Block-wide (all NT threads of the CTA call it); ends with a barrier.  Blocks
 // must be ascending in blk (hip_mask_estimate's output format).
-template <int NT>
+template <int NT, bool kShared = false>
 __device__ int build_extra(const int32_t* blk, int c, int lbk, int Tk, int64_t p_first, int64_t p_last, int causal,
                            int sink, int window, int* list, int* warp_tot) {
   const int tid = threadIdx.x;
@@ -53,7 +60,7 @@ __device__ int build_extra(const int32_t* blk, int c, int lbk, int Tk, int64_t p
     int s = 0, keep = 0;
     if (i < L) {
       s = i < a1 ? i : (int)(r2 + (i - a1));
-      keep = !blk_selected(blk, c, s >> lbk);
+      keep = !blk_selected<kShared>(blk, c, s >> lbk);
     }
     int cnt_round;
     const int pos = block_excl_scan<NT, CtaSync>(keep, warp_tot, cnt_round);

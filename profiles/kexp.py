@@ -6,7 +6,7 @@
 `build` compiles every csrc/*.cu with the extra defines into its own library; `time` runs each
 library in a fresh process on the same seeded inputs (the bench's: per-head `llm` recipe, paged C3
 cache) and prints one JSON line per (variant, config): median CUDA-event ms of the mask and the
-attention launch, one L2 flush (256 MB write) before every timed launch.  "base" = the product
+attention launch, one L2 flush (256 MB read, leaving clean lines) before every timed launch.  "base" = the product
 library paper_2406_09827_b200/libhipattn.so.
 """
 import json
@@ -59,7 +59,7 @@ def _time_one(path, cfgs, reps):
     from paper_2406_09827_b200 import synth
     H._lib = H._open(path)
     dev = torch.device("cuda:0")
-    flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    flush = torch.ones(bench.L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     st = torch.cuda.current_stream(dev)
     out = []
 
@@ -69,7 +69,8 @@ def _time_one(path, cfgs, reps):
             f()
         for _ in range(reps):
             for i, f in enumerate(fns):
-                flush.fill_(1)
+                flush.sum()  # read-flush: L2 left holding clean lines (a write flush leaves ~126 MB of dirty
+                #              lines whose write-back lands inside the next short kernel)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
                 f()

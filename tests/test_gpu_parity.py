@@ -766,15 +766,20 @@ def test_decode_split_k_parity(orc, B, Hq, Hkv, sw):
     assert np.abs(lse.cpu().numpy() - lo).max() <= 1e-3
 
 
-def test_single_row_prefill_split_k_parity(orc):
-    """T_q = 1 through the contiguous prefill entry also takes the split-K path (same kernel)."""
+@pytest.mark.parametrize("Tq,causal,sw", [(1, True, False), (40, True, False), (40, True, True), (40, False, True)])
+def test_single_row_prefill_parity(orc, Tq, causal, sw):
+    """Single-row query blocks through the contiguous prefill entry (the decode kernel): T_q = 1
+    (split-K), and b_q = 1 with T_q = 40 rows at increasing positions, where the token-level causal
+    mask cuts selected blocks and the sink / window sets differ per row."""
     B, Hq, Hkv, Tk, d, k, bk = 3, 4, 2, 2500, 128, 256, 2
-    Q, K, V = synth.gen_qkv(B, Hq, Hkv, 1, Tk, d, "iid", seed=41, dtype=torch.bfloat16)
-    idx, cnt = synth.gen_block_indices(B, Hq, 1, k // bk, torch.full((B, Hq, 1), -(-Tk // bk)), seed=41)
+    Q, K, V = synth.gen_qkv(B, Hq, Hkv, Tq, Tk, d, "iid", seed=41, dtype=torch.bfloat16)
+    hi = torch.tensor([[[_visible(t, 1, bk, Tq, Tk, causal) for t in range(Tq)] for _ in range(Hq)] for _ in range(B)])
+    idx, cnt = synth.gen_block_indices(B, Hq, Tq, k // bk, hi, seed=41)
+    kw = dict(sink=32, window=128) if sw else {}
     o, lse = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx.cuda(), cnt.cuda(), k_budget=k, b_q=1,
-                                        b_k=bk, causal=True, return_lse=True)
+                                        b_k=bk, causal=causal, return_lse=True, **kw)
     torch.cuda.synchronize()
-    Oo, lo = orc.sparse_attention(Q, K, V, k, 1, bk, True, idx.numpy(), cnt.numpy())
+    Oo, lo = orc.sparse_attention(Q, K, V, k, 1, bk, causal, idx.numpy(), cnt.numpy(), **kw)
     assert np.abs(o.float().cpu().numpy() - Oo).max() <= TOL[torch.bfloat16]
     fin = np.isfinite(lo)
     assert np.array_equal(fin, np.isfinite(lse.cpu().numpy()))
