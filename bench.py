@@ -511,42 +511,90 @@ def ncu_traffic(kernel_key: str, config: str):
         return None
 
 
+def read_flush(flush):
+    """Evict L2 by READING a buffer larger than it (256 MB): the lines left behind are clean, so no
+    write-back of a flush lands inside the next (short) timed kernel."""
+    flush.sum()
+
+
+def graph_times_us(fns, flush, reps, device):
+    """Device time (us, median over reps) of each fn captured as a CUDA graph: per rep an untimed L2
+    read-flush, then events around one graph replay on the launching stream.  The flush keeps the
+    GPU busy while the host enqueues the replay, so no host launch gap lands in the interval."""
+    import torch
+    cur = torch.cuda.current_stream(device)
+    graphs = []
+    for fn in fns:
+        side = torch.cuda.Stream(device)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            fn()  # warm-up (kernel attributes, workspace sizes) outside the capture
+        cur.wait_stream(side)
+        torch.cuda.synchronize(device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        graphs.append(g)
+    for g in graphs:
+        g.replay()
+    torch.cuda.synchronize(device)
+    ts = [[] for _ in graphs]
+    for _ in range(reps):
+        for i, g in enumerate(graphs):
+            read_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            g.replay()
+            e1.record(cur)
+            ts[i].append((e0, e1))
+    torch.cuda.synchronize(device)
+    out = [1e3 * statistics.median(a.elapsed_time(b) for a, b in t) for t in ts]
+    del graphs
+    return out
+
+
 def time_hip_decoder(q, kp, vp, bt, c, device, steps=16):
-    """Alg. 2 measured: HipDecoder.step over `steps` consecutive decode steps, at r_m = 1
-    and the paper's default r_m = 8, with the paper's sink / window (32, 128).
-    Step t runs at sequence length T - steps + t + 1 (the cache holds T tokens), so an r_m = 8 run
-    refreshes the mask on every 8th step exactly as the loop would.  Per-step CUDA events on the
-    launching stream; the mean over the steps (one L2 flush before the run)."""
+    """Alg. 2 (P:595-619) measured: HipDecoder.graphed_step (decode.py) over `steps` consecutive
+    decode steps at r_m = 1 and at the paper's default r_m = 8, with the paper's sink /
+    window (32, 128).  Step t runs at sequence length T - steps + t + 1 (the cache holds T
+    tokens; the lengths are written into the static seq_lens buffer before the step, untimed), so an
+    r_m = 8 run refreshes the mask on every 8th step exactly as the loop would.  Per step: untimed
+    L2 read-flush, CUDA events around the step on the launching stream; mean over the steps."""
     import torch
     from paper_2406_09827_b200.decode import HipDecoder
     st = torch.cuda.current_stream(device)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
     out = {}
     T0 = c["T"] - steps
+    lens = [T0 + 1 + t for t in range(steps)]
+    sls = [torch.full((c["B"],), L, dtype=torch.int32, device=device) for L in lens]
+    sl = sls[0].clone()
+    o = torch.empty_like(q)
     for r_m in (1, 8):
         dec = HipDecoder(r_m=r_m, k_budget=c["k"], b_k=c["bk"], b_q=1)
-        lens = [T0 + 1 + t for t in range(steps)]
-        sls = [torch.full((c["B"],), L, dtype=torch.int32, device=device) for L in lens]
-        # warm-up on the first length (then reset so the timed run starts with a refresh)
-        dec.step(q, kp, vp, bt, sls[0], [lens[0]] * c["B"])
-        dec.idx = dec.cnt = None
+        dec.graphed_step(q, kp, vp, bt, sl, [lens[0]] * c["B"], o)  # capture + warm-up
+        dec.idx = dec.cnt = None  # the timed run starts with a refresh
         dec.refreshes = 0
         torch.cuda.synchronize(device)
-        flush.fill_(1)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-        ev[0].record(st)
+        ev = []
         for t in range(steps):
-            dec.step(q, kp, vp, bt, sls[t], [lens[t]] * c["B"])
-            ev[t + 1].record(st)
+            sl.copy_(sls[t])
+            read_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            dec.graphed_step(q, kp, vp, bt, sl, [lens[t]] * c["B"], o)
+            e1.record(st)
+            ev.append((e0, e1))
         torch.cuda.synchronize(device)
-        per = [ev[t].elapsed_time(ev[t + 1]) * 1e3 for t in range(steps)]
+        per = [1e3 * a.elapsed_time(b) for a, b in ev]
+        ref = [p for p, L in zip(per, lens) if r_m == 1 or L % r_m == 0]
+        cached = [p for p, L in zip(per, lens) if r_m > 1 and L % r_m]
         out[f"r_m{r_m}"] = {"us_per_step": round(sum(per) / steps, 2), "refreshes": dec.refreshes, "steps": steps,
-                            "us_refresh_steps": round(statistics.mean(p for p, L in zip(per, lens) if L % r_m == 0 or r_m == 1), 2)
-                            if any(L % r_m == 0 for L in lens) else None,
-                            "us_cached_steps": round(statistics.mean(p for p, L in zip(per, lens) if L % r_m), 2)
-                            if r_m > 1 else None}
-    out["note"] = ("HipDecoder.step (decode.py): mask estimation when the length is divisible by r_m, then the "
-                   "paged sparse attention with sink 32 + window 128; seq lengths T-16+1..T")
+                            "us_refresh_steps": round(statistics.mean(ref), 2) if ref else None,
+                            "us_cached_steps": round(statistics.mean(cached), 2) if cached else None}
+    out["note"] = ("HipDecoder.graphed_step (decode.py, CUDA graphs): mask estimation when the length is divisible by "
+                   "r_m, then the paged sparse attention with sink 32 + window 128; seq lengths T-16+1..T; L2 "
+                   "read-flushed before every step")
     return out
 
 
@@ -613,23 +661,15 @@ def bench_decode(args, device, T=None, options=True):
     idx = torch.empty(c["B"], c["Hq"], 1, n, dtype=torch.int32, device=device)
     cnt = torch.empty(c["B"], c["Hq"], 1, dtype=torch.int32, device=device)
     o = torch.empty_like(q)
-    st = torch.cuda.current_stream(device)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    for _ in range(3):
-        HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(idx, cnt), **kw)
-        HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], idx, cnt, out=o, **kw)
-    torch.cuda.synchronize(device)
-    m_t, a_t = [], []
-    for _ in range(max(args.steps, 5)):
-        ev[0].record(st)
-        HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(idx, cnt), **kw)
-        ev[1].record(st)
-        HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], idx, cnt, out=o, **kw)
-        ev[2].record(st)
-        torch.cuda.synchronize(device)
-        m_t.append(ev[0].elapsed_time(ev[1]))
-        a_t.append(ev[1].elapsed_time(ev[2]))
-    mask_us, attn_us = 1e3 * statistics.median(m_t), 1e3 * statistics.median(a_t)
+    flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    mask_f = lambda: HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(idx, cnt), **kw)  # noqa: E731
+    attn_f = lambda: HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], idx, cnt, out=o, **kw)  # noqa: E731
+
+    def step_f():
+        mask_f()
+        attn_f()
+    reps = max(args.steps, 10)
+    mask_us, attn_us, step_us = graph_times_us([mask_f, attn_f, step_f], flush, reps, device)
     Bq = (c["T"] + c["bk"] - 1) // c["bk"]
     it = math.ceil(math.log2(math.ceil(Bq / n)))
     units = c["B"] * c["Hq"]
@@ -639,8 +679,12 @@ def bench_decode(args, device, T=None, options=True):
     kv_bytes = 2 * c["B"] * c["Hkv"] * c["T"] * c["d"] * 2
     res = {
         "workload": c["workload"], "r_m": 1,
-        "us_per_step": round(mask_us + attn_us, 2), "mask_us": round(mask_us, 2), "attn_us": round(attn_us, 2),
-        "us_per_sequence": round((mask_us + attn_us) / c["B"], 3),
+        "us_per_step": round(step_us, 2), "mask_us": round(mask_us, 2), "attn_us": round(attn_us, 2),
+        "us_per_sequence": round(step_us / c["B"], 3),
+        "timing": "CUDA graphs (mask, attention, and the step = both), L2 read-flushed before each replay, median",
+        "step_roofline": {"bound": "hbm", "achieved": round((mask_bytes + attn_bytes) / (step_us * 1e-6) / 1e9, 1),
+                          "peak": pk["hbm_gbs"], "unit": "GB/s",
+                          "frac": round((mask_bytes + attn_bytes) / (step_us * 1e-6) / 1e9 / pk["hbm_gbs"], 4)},
         "roofline": {"kernel": "mask_estimate (paged, b_q=1)", "bound": "hbm",
                      "achieved": round(mask_bytes / (mask_us * 1e-6) / 1e9, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": round(mask_bytes / (mask_us * 1e-6) / 1e9 / pk["hbm_gbs"], 4),
@@ -662,21 +706,10 @@ def bench_decode(args, device, T=None, options=True):
             ti = torch.empty(c["B"], c["Hkv"], 1, n, dtype=torch.int32, device=device)
             tc = torch.empty(c["B"], c["Hkv"], 1, dtype=torch.int32, device=device)
             akw = dict(kw, gqa_shared=True)
-            for _ in range(3):
-                HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(ti, tc), **kw, **ex)
-                HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], ti, tc, out=o, **akw)
-            torch.cuda.synchronize(device)
-            vm, va = [], []
-            for _ in range(max(args.steps, 5)):
-                ev[0].record(st)
-                HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(ti, tc), **kw, **ex)
-                ev[1].record(st)
-                HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], ti, tc, out=o, **akw)
-                ev[2].record(st)
-                torch.cuda.synchronize(device)
-                vm.append(ev[0].elapsed_time(ev[1]))
-                va.append(ev[1].elapsed_time(ev[2]))
-            vmu, vau = 1e3 * statistics.median(vm), 1e3 * statistics.median(va)
+            vmu, vau = graph_times_us(
+                [lambda: HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(ti, tc), **kw, **ex),  # noqa: B023
+                 lambda: HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], ti, tc, out=o, **akw)],  # noqa: B023
+                flush, reps, device)
             variants[name] = {"mask_us": round(vmu, 2), "attn_us": round(vau, 2), "us_per_step": round(vmu + vau, 2),
                               "mask_bytes": mask_bytes // (c["Hq"] // c["Hkv"]),
                               "mask_gbs": round(mask_bytes / (c["Hq"] // c["Hkv"]) / (vmu * 1e-6) / 1e9, 1)}

@@ -42,6 +42,7 @@ class HipDecoder:
         self.idx = None
         self.cnt = None
         self.refreshes = 0  # number of steps that ran the mask estimation (for tests / stats)
+        self._graphs = None  # graphed_step state: (buffers key, refresh graph, cached graph)
 
     def refresh_rows(self, seq_lens_host) -> list:
         """Per-sequence refresh decision for this step (Alg. 2 line 8)."""
@@ -68,3 +69,57 @@ class HipDecoder:
                                          k_budget=self.k_budget, b_q=self.b_q, b_k=self.b_k, causal=self.causal,
                                          sm_scale=self.sm_scale, sink=self.sink, window=self.window,
                                          return_lse=return_lse, gqa_shared=self.gqa_shared, stream=stream)
+
+    def graphed_step(self, q, k_pages, v_pages, block_table, seq_lens, seq_lens_host, out):
+        """The same Alg. 2 step replayed from CUDA graphs (how a serving loop launches it: one graph
+        launch per step instead of a chain of host calls).  q, seq_lens, out (and the cache) are
+        STATIC buffers the caller updates in place between steps.  Two graphs are captured on the
+        first call for a set of buffers: refresh (mask estimation into the cached idx / cnt, then the
+        sparse attention) and cached (the attention only).  The kernels take each sequence's length
+        from seq_lens, so the graphs are captured once with max_seq_len = the cache capacity
+        (block_table columns x page size).  Per step (Alg. 2 line 8, from seq_lens_host): every
+        sequence refreshes -> the refresh graph; none -> the cached graph; a mix -> the mask is
+        estimated eagerly for the batch, the refreshing rows are merged into the cached buffers,
+        then the cached graph runs.  Returns out."""
+        cap = int(block_table.shape[1]) * int(k_pages.shape[2])
+        key = tuple(int(t.data_ptr()) for t in (q, k_pages, v_pages, block_table, seq_lens, out)) + (
+            tuple(q.shape), tuple(k_pages.shape), tuple(block_table.shape))
+        if self._graphs is None or self._graphs[0] != key:
+            mkw = dict(k_budget=self.k_budget, b_q=self.b_q, b_k=self.b_k, causal=self.causal,
+                       gqa_shared=self.gqa_shared, chunks=self.chunks)
+            akw = dict(k_budget=self.k_budget, b_q=self.b_q, b_k=self.b_k, causal=self.causal, sm_scale=self.sm_scale,
+                       sink=self.sink, window=self.window, gqa_shared=self.gqa_shared)
+            idx, cnt = H.mask_estimate_paged(q, k_pages, block_table, seq_lens, cap, **mkw)  # buffers + warm-up
+            if self.idx is not None and self.idx.shape == idx.shape:
+                idx.copy_(self.idx)
+                cnt.copy_(self.cnt)
+            H.sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, cap, idx, cnt, out=out, **akw)
+            torch.cuda.synchronize(q.device)
+            g_ref, g_att = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_ref):
+                H.mask_estimate_paged(q, k_pages, block_table, seq_lens, cap, out=(idx, cnt), **mkw)
+                H.sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, cap, idx, cnt, out=out, **akw)
+            with torch.cuda.graph(g_att):
+                H.sparse_attention_decode(q, k_pages, v_pages, block_table, seq_lens, cap, idx, cnt, out=out, **akw)
+            self._graphs = (key, g_ref, g_att, idx, cnt, cap, mkw)
+            had_mask = self.idx is not None
+            self.idx, self.cnt = idx, cnt
+            if not had_mask:
+                self.idx = None  # nothing cached yet: the first step refreshes
+        _, g_ref, g_att, idx, cnt, cap, mkw = self._graphs
+        rows = self.refresh_rows(seq_lens_host)
+        if all(rows):
+            g_ref.replay()
+            self.refreshes += 1
+        elif not any(rows):
+            g_att.replay()
+        else:
+            ni, nc = H.mask_estimate_paged(q, k_pages, block_table, seq_lens, cap, **mkw)
+            sel = torch.tensor(rows, device=idx.device)
+            idx.copy_(torch.where(sel.view(-1, 1, 1, 1), ni, idx))
+            cnt.copy_(torch.where(sel.view(-1, 1, 1), nc, cnt))
+            self.refreshes += 1
+            g_att.replay()
+        self.idx, self.cnt = idx, cnt
+        return out
+

@@ -29,6 +29,7 @@ def main():
     lib_path = build() if "--build" in sys.argv else os.path.join(ROOT, "paper_2406_09827_b200", "libhipattn_phases.so")
     H._lib = None
     lib = H.load(lib_path)
+    H._lib = lib  # route the binding through the phase-timer build
     fn = lib.hip_debug_phase_cycles
     fn.argtypes = [ctypes.c_void_p]
     T, Hh = int(os.environ.get("PT_T", 32768)), int(os.environ.get("PT_H", 32))

@@ -454,6 +454,32 @@ def test_decoder_rm_cache_schedule(orc, shared, chunks):
     assert 1 < dec.refreshes < 8
 
 
+@pytest.mark.parametrize("lens", [[690, 893], [692, 896]])
+def test_decoder_graphed_step_equals_eager(lens):
+    """HipDecoder.graphed_step (CUDA graphs: refresh graph = mask + attention, cached graph =
+    attention; mixed-refresh steps merge an eager mask) gives the eager step's indices and outputs
+    bit-for-bit over an r_m = 4 schedule.  lens[0] % 4 != lens[1] % 4 exercises the mixed case, the
+    second set (both divisible by 4 together) the all / none cases.  Static buffers updated in place."""
+    from paper_2406_09827_b200.decode import HipDecoder
+    B, Hq, Hkv, d, k, bk, ps, r_m = 2, 4, 2, 128, 128, 2, 16, 4
+    kp, vp, bt, _ = (x.cuda() for x in synth.gen_paged_direct(B, Hkv, [1000, 1000], d, ps, seed=32))
+    eager = HipDecoder(r_m=r_m, k_budget=k, b_k=bk, b_q=1, sink=4, window=16)
+    graphed = HipDecoder(r_m=r_m, k_budget=k, b_k=bk, b_q=1, sink=4, window=16)
+    q = torch.empty(B, Hq, 1, d, dtype=torch.bfloat16, device="cuda")
+    sl = torch.empty(B, dtype=torch.int32, device="cuda")
+    out = torch.empty_like(q)
+    for step in range(9):
+        cur = [lens[0] + step, lens[1] + step]
+        q.copy_(synth.gen_decode_q(B, Hq, d, seed=200 + step))
+        sl.copy_(torch.tensor(cur, dtype=torch.int32))
+        oe = eager.step(q, kp, vp, bt, sl, cur)
+        graphed.graphed_step(q, kp, vp, bt, sl, cur, out)
+        torch.cuda.synchronize()
+        assert torch.equal(graphed.idx, eager.idx) and torch.equal(graphed.cnt, eager.cnt), step
+        assert torch.equal(out, oe), step
+    assert graphed.refreshes == eager.refreshes
+
+
 def test_decoder_non_refresh_step_attends_current_token(orc):
     """with a cached mask (r_m = 8, the paper's default) a step between refreshes must still
     attend the token just generated — the default sliding window (128) covers it.  Changing
