@@ -492,10 +492,13 @@ def tensor_util(cfg, heads, mask_ms, attn_ms, pk, cfg_name):
     p = latest_ncu_summary(cfg_name)
     if p:
         import re
-        pct = re.findall(r"sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active\s+([0-9.]+)", open(p).read())
-        if len(pct) >= 2:
-            res["ncu_tensor_pipe_active_pct"] = {"mask": float(pct[0]), "attention": float(pct[1]),
-                                                 "source": os.path.relpath(p, ROOT)}
+        got = {}
+        for block in open(p).read().split("== ")[1:]:  # one block per kernel (ncu_summary.py format)
+            m = re.search(r"sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active\s+([0-9.]+)", block)
+            if m:
+                got["mask" if block.startswith("void mask") else "attention"] = float(m.group(1))
+        if len(got) == 2:
+            res["ncu_tensor_pipe_active_pct"] = dict(got, source=os.path.relpath(p, ROOT))
     return res
 
 

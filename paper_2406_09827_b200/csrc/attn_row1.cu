@@ -8,7 +8,7 @@
 // tcgen05), the math here runs on the CUDA cores straight from shared memory:
 //   * items of 32 keys = 32 K rows + 32 V rows (16 KB) stream through a 3-slot ring of cp.async
 //     gathers (16 lanes per 256-byte row: whole sectors, no L1); completion is tracked on mbarriers
-//     (cp.async.mbarrier.arrive.noinc -> "full", one arrival per warp -> "empty"), so no CTA-wide
+//     (cp.async.mbarrier.arrive.noinc -> "full", one arrival per reading thread -> "empty"), so no CTA-wide
 //     barrier sits between items and a slot is refilled as soon as the four warps have read it;
 //   * warp w owns keys 8w..8w+7 of every item: 4 lanes per key each dot a quarter of d (q in
 //     registers), two shuffles complete q.k; the warp keeps its own online softmax state (max, sum,
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
   if (tid == 0) {
     for (int s = 0; s < kR1Slots; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(full0 + 8 * s), "r"(kR1Threads) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(empty0 + 8 * s), "r"(4) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(empty0 + 8 * s), "r"(kR1Threads) : "memory");
     }
     fence_mbar_init();
   }
@@ -246,8 +246,7 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
         ov[2] = fmaf(pj, bf16_lo(vv.y), ov[2]);
         ov[3] = fmaf(pj, bf16_hi(vv.y), ov[3]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+      mbar_arrive(empty0 + 8 * slot);  // every reader releases its own reads of the slot
       if (i + kR1Slots < nit) issue(i + kR1Slots);
     }
     g = g0 + (uint32_t)nit;

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   float* lurun = red + 448;                                // running sum of unrounded p (lse)
   float* corr = red + 480;                                 // rescale factor of this chunk
   float* invl = red + 512;
+  float* thr = red + 544;                                  // mrun + kATRescale: the lazy-rescale thresholds
   int* flag = reinterpret_cast<int*>(red + 576);
   int* tok = reinterpret_cast<int*>(base + L::tok);
   int* xlist = reinterpret_cast<int*>(base + L::xlist);
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     }
     if (threadIdx.x < 32) {
       mrun[threadIdx.x] = -INFINITY;
+      thr[threadIdx.x] = -INFINITY;
       lrun[threadIdx.x] = 0.f;
       lurun[threadIdx.x] = 0.f;
     }
@@ -294,6 +296,19 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         float x[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) x[j] = v[j];
+        // The running max moves only when some query's chunk max exceeds it by more than kATRescale
+        // (lazy rule below).  Every thread first checks its own 32 scores against the thresholds
+        // thr[j] = mrun[j] + kATRescale; only if any score in the CTA exceeds one (always on a unit's
+        // first chunk) is the chunk max reduced and the running max updated — otherwise that whole
+        // step would leave mrun, corr and the sums' scale unchanged, so skipping it is exact.
+        bool grow = false;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(thr + j);
+          grow |= (v[j] > t.x) | (v[j + 1] > t.y) | (v[j + 2] > t.z) | (v[j + 3] > t.w);
+        }
+        bool resc = false;
+        if (__syncthreads_or(grow)) {
         red[warp * 32 + lane] = reduce_scatter32<true>(v, lane);
         __syncthreads();
         if (threadIdx.x < 32) {  // new running max per query (lazy), rescale factor, rescale flag
@@ -304,12 +319,15 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
           const float cf = (mn == mo) ? 1.f : (mo == -INFINITY ? 0.f : ex2_approx(mo - mn));
           corr[j] = cf;
           mrun[j] = mn;
+          thr[j] = mn + kATRescale;
           lrun[j] *= cf;
           lurun[j] *= cf;
           const unsigned any = __ballot_sync(0xffffffffu, cf != 1.f);
           if (j == 0) *flag = (any != 0u) && ch > 0;
         }
         __syncthreads();
+        resc = *flag;
+        }
         float lq = 0.f, lu = 0.f;
         {
           uint32_t pk[16];
@@ -343,7 +361,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
         }
         red[128 + warp * 32 + lane] = lq;
         red[256 + warp * 32 + lane] = lu;
-        if (*flag) {  // rescale O^T columns (queries) whose running max moved; all PV MMAs retired
+        if (resc) {  // rescale O^T columns (queries) whose running max moved; all PV MMAs retired
           float ov[32];
           tmem_ld_32x32b_x32(tmem_lane + 32, ov);
 #pragma unroll
