@@ -31,6 +31,7 @@ constexpr uint32_t kR1Item = 16384;            // 32 K rows + 32 V rows of 256 b
 constexpr int kR1Tok = 768;                    // <= 512 selected keys + <= 256 sink / window tokens
 constexpr int kR1MaxN = 512;                   // n = k / b_k <= kR1MaxN (the index row staged in the prologue)
 constexpr int kR1BtStage = (int)(kR1Item / 4) - kR1MaxN;  // block-table entries staged with it (3584)
+constexpr int kR1ChunkItems = 4;               // a softmax chunk: 4 items = 128 keys (<= 6 chunks per unit)
 constexpr float kR1Log2e = 1.4426950408889634f;
 constexpr float kR1Ln2 = 0.6931471805599453f;
 
@@ -50,6 +51,23 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar) : "memory");
+}
+
+// acc <- acc (+) part: two softmax states over disjoint key sets merged at their common max.  The
+// unit's result is the merge of its chunk states in chunk order, whichever jobs computed the chunks
+// (one job, or split-K jobs whose chunk states pass through the workspace): the same operations in
+// the same order, so the output does not depend on the split factor, i.e. on batch composition.
+__device__ __forceinline__ void r1_merge(float& Ma, float& La, float& Oa, float Mc, float Lc, float Oc) {
+  if (Mc == -INFINITY) return;  // no visible key in the part
+  if (Ma == -INFINITY) {
+    Ma = Mc; La = Lc; Oa = Oc;
+    return;
+  }
+  const float Mn = fmaxf(Ma, Mc);
+  const float fa = ex2_approx(Ma - Mn), fc = ex2_approx(Mc - Mn);
+  Oa = fmaf(Oc, fc, Oa * fa);
+  La = fmaf(Lc, fc, La * fa);
+  Ma = Mn;
 }
 
 template <bool kPaged, bool kSW, bool kSplit>
@@ -121,9 +139,12 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
                        : 0;
     const int nall = nkeys + ne;
     const int nit_all = (nall + 31) >> 5;
-    const int i_lo = kSplit ? sp * nit_all / S : 0;
-    const int nit = kSplit ? (sp + 1) * nit_all / S - i_lo : nit_all;
-    const int k_lo = i_lo * 32, nk = min(nit * 32, nall - k_lo);
+    const int nch_all = (nit_all + kR1ChunkItems - 1) / kR1ChunkItems;
+    // this job's chunks [c_lo, c_hi) and items [i_lo, i_lo + nit)
+    const int c_lo = kSplit ? sp * nch_all / S : 0, c_hi = kSplit ? (sp + 1) * nch_all / S : nch_all;
+    const int i_lo = c_lo * kR1ChunkItems;
+    const int nit = max(0, min(c_hi * kR1ChunkItems, nit_all) - i_lo);
+    const int k_lo = i_lo * 32, nk = max(0, min(nit * 32, nall - k_lo));
 
     // key slots of this job -> physical rows (-1: not a key, or not visible to the row)
     for (int kk = tid; kk < nit * 32; kk += kR1Threads) {
@@ -190,7 +211,9 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
       cp_async_mbar_arrive_noinc(full0 + 8 * slot);
     };
 
-    float m = -INFINITY, l = 0.f, ov[4] = {0.f, 0.f, 0.f, 0.f};
+    float m = -INFINITY, l = 0.f, ov[4] = {0.f, 0.f, 0.f, 0.f};  // this warp's state of the current chunk
+    float Ma = -INFINITY, La = 0.f, Oa = 0.f;                     // thread d: merge of the chunks so far
+    const int d = tid;
     const int pre = min(nit, kR1Slots);
     for (int i = 0; i < pre; ++i) issue(i);
     for (int i = 0; i < nit; ++i) {
@@ -248,58 +271,58 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
       }
       mbar_arrive(empty0 + 8 * slot);  // every reader releases its own reads of the slot
       if (i + kR1Slots < nit) issue(i + kR1Slots);
+      if ((i + 1) % kR1ChunkItems == 0 || i == nit - 1) {
+        // chunk end: merge the four warp states (fixed order) into the chunk state of column d
+        *reinterpret_cast<float4*>(mo + warp * 128 + 4 * lane) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+        if (lane == 0) {
+          mm[warp] = m;
+          ml[warp] = l;
+        }
+        __syncthreads();
+        const float Mc = fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3]));
+        float Oc = 0.f, Lc = 0.f;
+        if (Mc != -INFINITY) {
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            if (mm[w] == -INFINITY) continue;
+            const float f = ex2_approx(mm[w] - Mc);
+            Oc = fmaf(f, mo[w * 128 + d], Oc);
+            Lc = fmaf(f, ml[w], Lc);
+          }
+        }
+        if constexpr (kSplit) {  // the chunk state goes to the workspace; the unit's last job merges
+          float* my = sh.part + (u * kSplitMax + (i_lo + i) / kR1ChunkItems) * kSplitStride;
+          __stcg(my + d, Oc);
+          if (d == 0) {
+            __stcg(my + 128, Mc);
+            __stcg(my + 129, Lc);
+          }
+        } else {
+          r1_merge(Ma, La, Oa, Mc, Lc, Oc);
+        }
+        m = -INFINITY;
+        l = 0.f;
+        ov[0] = ov[1] = ov[2] = ov[3] = 0.f;
+        __syncthreads();  // mo / mm / ml are rewritten at the next chunk end
+      }
     }
     g = g0 + (uint32_t)nit;
 
-    // merge the four warp states: M = max_w m_w, O = sum_w 2^(m_w - M) O_w, L = sum_w 2^(m_w - M) l_w
-    *reinterpret_cast<float4*>(mo + warp * 128 + 4 * lane) = make_float4(ov[0], ov[1], ov[2], ov[3]);
-    if (lane == 0) {
-      mm[warp] = m;
-      ml[warp] = l;
-    }
-    __syncthreads();
-    const int d = tid;
-    float M = fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3]));
-    float O = 0.f, Ls = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        if (mm[w] == -INFINITY) continue;
-        const float f = ex2_approx(mm[w] - M);
-        O = fmaf(f, mo[w * 128 + d], O);
-        Ls = fmaf(f, ml[w], Ls);
-      }
-    }
     if constexpr (kSplit) {
-      // publish this split's partial (O unnormalised, M, L), the last split of the unit merges
-      constexpr int PS = kSplitStride;
-      float* my = sh.part + (u * S + sp) * PS;
-      __stcg(my + d, O);
-      if (d == 0) {
-        __stcg(my + 128, M);
-        __stcg(my + 129, Ls);
-      }
+      // publish this job's chunk states; the job that arrives last merges all chunks of the unit in
+      // chunk order with r1_merge, exactly as one unsplit job would
       __threadfence();
       __syncthreads();
       if (d == 0) *flag = atomicAdd(sh.arrive + u, 1u) == (unsigned)(S - 1);
       __syncthreads();
       if (!*flag) continue;
       __threadfence();
-      const float* pu = sh.part + u * S * PS;
-      M = -INFINITY;
-      for (int s = 0; s < S; ++s) M = fmaxf(M, __ldcg(pu + s * PS + 128));
-      O = 0.f;
-      Ls = 0.f;
-      if (M != -INFINITY) {
-        for (int s = 0; s < S; ++s) {
-          const float ms = __ldcg(pu + s * PS + 128);
-          if (ms == -INFINITY) continue;
-          const float f = ex2_approx(ms - M);
-          O = fmaf(f, __ldcg(pu + s * PS + d), O);
-          Ls = fmaf(f, __ldcg(pu + s * PS + 129), Ls);
-        }
-      }
+      const float* pu = sh.part + u * kSplitMax * kSplitStride;
+      for (int c = 0; c < nch_all; ++c)
+        r1_merge(Ma, La, Oa, __ldcg(pu + c * kSplitStride + 128), __ldcg(pu + c * kSplitStride + 129),
+                 __ldcg(pu + c * kSplitStride + d));
     }
+    const float M = Ma, Ls = La, O = Oa;
     __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(o + (b * osb + h * osh + (int64_t)q * sh.bq * ost) * 2);
     orow[d] = __float2bfloat16_rn(Ls > 0.f ? O / Ls : 0.f);  // a row with no visible key: O = 0 (G13)
     if (lse && d == 0)
@@ -337,10 +360,13 @@ cudaError_t launch_attn_row1(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
   const int64_t slots = (int64_t)num_sms * per_sm;
   Shape s2 = sh;
-  // split-K only to fill CTA slots the units leave idle (never a second wave)
+  // split-K only to fill CTA slots the units leave idle (never a second wave), and never into more
+  // jobs than a unit has 128-key chunks (the split granularity)
+  const int64_t max_keys = (int64_t)sh.n * sh.bk + ((sh.sink > 0 || sh.window > 0) ? sh.sink + sh.window : 0);
+  const int64_t max_chunks = std::max<int64_t>(1, (max_keys + 32 * kR1ChunkItems - 1) / (32 * kR1ChunkItems));
   s2.splits = 1;
   if (sh.part && sh.arrive && units <= kSplitMaxUnits)
-    s2.splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitMax, slots / units));
+    s2.splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(kSplitMax, max_chunks), slots / units));
 #ifdef HIPATTN_TUNING
   if (const char* e2 = getenv("HIPATTN_SPLITS"))
     if (sh.part) s2.splits = std::max(1, std::min(kSplitMax, atoi(e2)));

@@ -839,3 +839,22 @@ def test_concurrent_streams_own_workspaces():
         torch.cuda.synchronize()
         assert torch.equal(i1, ref_i) and torch.equal(o1, ref_o)
         assert torch.equal(pi, ref_pi) and torch.equal(po, ref_po)
+
+
+def test_decode_attention_batch_composition_invariant():
+    """Split-K is chosen from the unit count (S = min(8, CTA slots / units)), but the output of a unit
+    does not depend on it: every path merges the same 128-key chunk states in chunk order.  One
+    sequence alone (32 units: split 8) and inside a batch of 20 (640 units: no split) give the same
+    bits, lse included; so do sequence subsets (the decode batch shard of dist.py)."""
+    B, Hq, Hkv, d, k, bk, ps = 20, 32, 8, 128, 512, 2, 16
+    seq = [3000 - 37 * b for b in range(B)]
+    q = synth.gen_decode_q(B, Hq, d, seed=71).cuda()
+    kp, vp, bt, sl = (x.cuda() for x in synth.gen_paged_direct(B, Hkv, seq, d, ps, seed=71))
+    kw = dict(k_budget=k, b_q=1, b_k=bk, causal=True, sink=32, window=128, return_lse=True)
+    idx, cnt = H.mask_estimate_paged(q, kp, bt, sl, max(seq), k_budget=k, b_q=1, b_k=bk)
+    o_all, l_all = H.sparse_attention_decode(q, kp, vp, bt, sl, max(seq), idx, cnt, **kw)
+    for lo, hi in ((0, 1), (5, 6), (3, 7), (10, 20)):
+        o, l = H.sparse_attention_decode(q[lo:hi].contiguous(), kp, vp, bt[lo:hi].contiguous(), sl[lo:hi].contiguous(),
+                                         max(seq[lo:hi]), idx[lo:hi].contiguous(), cnt[lo:hi].contiguous(), **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(o, o_all[lo:hi]) and torch.equal(l, l_all[lo:hi]), (lo, hi)
