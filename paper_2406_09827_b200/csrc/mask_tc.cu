@@ -474,10 +474,17 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                            cudaStream_t stream, int num_sms) {
   const int ext = (sh.jitter > 0 ? 1 : 0) | (sh.top_r > 0 ? 2 : 0) | (sh.group > 1 ? 4 : 0);
+  const int64_t jobs = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb * std::max(sh.chunks, 1);
   switch (ext) {
     case 0:
       if (sh.bk == 2) {
-        if (sh.bq == 1) return launch_v<2, 4, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);  // decode
+        if (sh.bq == 1) {  // decode
+          // Small batches leave SMs idle: give each unit a deeper ring instead (one unit per SM: 8
+          // slots, a whole iteration's 8 items in flight; two per SM: 4 slots).  Same arithmetic.
+          if (jobs <= num_sms) return launch_v<8, 4, 1, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
+          if (jobs <= 2 * (int64_t)num_sms) return launch_v<4, 4, 2, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
+          return launch_v<2, 4, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
+        }
         return launch_v<2, 4, 4, 16>(sh, qs, ks, idx, cnt, stream, num_sms);
       }
       if (sh.bq == 1) return launch_v<2, 4, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);
