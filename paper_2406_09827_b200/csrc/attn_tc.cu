@@ -31,12 +31,15 @@ constexpr uint32_t kIdescPV = idesc_bf16(128, 32, 1, 1);
 constexpr float kATLog2e = 1.4426950408889634f;
 constexpr float kATLn2 = 0.6931471805599453f;
 constexpr float kATRescale = 8.f;                     // lazy rescale threshold (log2 units)
+// Ring slots of 16 KB items.  Two slots at 4 CTAs per SM beat three at 3 CTAs per SM (C4 attention
+// 5.20 vs 6.57 ms, profiles/r02/notes.md): more concurrent units matter more than a deeper ring.
+constexpr int kATRing = 2;
 
 template <int kTokN>
 struct AttnTCSmemT {
   static constexpr uint32_t q = 0;
-  static constexpr uint32_t ring = kATQTile;                      // 2 slots
-  static constexpr uint32_t p = ring + 2 * kATSlot;               // one P chunk
+  static constexpr uint32_t ring = kATQTile;                      // kATRing slots
+  static constexpr uint32_t p = ring + kATRing * kATSlot;         // one P chunk
   static constexpr uint32_t red = p + kATPChunk;                  // floats, see below
   static constexpr int kRedFloats = 3 * 4 * 32 + 6 * 32 + 32;     // [3][4][32] + m, l, lu, corr, invl, pad + flag
   static constexpr int kTok = kTokN;                              // selected + extra (<= 256) key slots
@@ -93,12 +96,11 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
   int* tok = reinterpret_cast<int*>(base + L::tok);
   int* xlist = reinterpret_cast<int*>(base + L::xlist);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * kATRing);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(mbar, 1);  // one MMA-completion barrier per ring slot
-    mbar_init(mbar + 1, 1);
+    for (int r = 0; r < kATRing; ++r) mbar_init(mbar + r, 1);  // one MMA-completion barrier per ring slot
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<64>(tmem_slot);
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     int srow[8];  // this thread's 8 key rows of the current chunk (-1: none)
     auto issue = [&](int i) {
       const int ch = i >> 2, kind = i & 3;
-      const uint32_t dst = sb + L::ring + (i & 1) * kATSlot + dbase;
+      const uint32_t dst = sb + L::ring + (i % kATRing) * kATSlot + dbase;
       if (kind == 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -232,19 +234,21 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
     };
 
     const int nitems = 4 * nch;
-    issue(0);
-    cp_async_commit();
-    issue(1);  // nitems >= 4
-    cp_async_commit();
+#pragma unroll
+    for (int r = 0; r < kATRing; ++r) {  // nitems >= 4 >= kATRing
+      issue(r);
+      cp_async_commit();
+    }
     for (int it = 0; it < nitems; ++it) {
-      cp_async_wait<1>();  // item it landed (item it + 1 may still be in flight)
+      cp_async_wait<kATRing - 1>();  // item it landed (items it + 1 .. may still be in flight)
       fence_proxy_async_smem();
       __syncthreads();
       // Every MMA up to item it - 1 has completed here (each slot is refilled only after its MMA is
       // waited for, and tcgen05 MMAs of one thread complete in order): S of this chunk is final
       // before its softmax, and the previous chunk's PV is done before P is rewritten.
       const int ch = it >> 2, kind = it & 3;
-      const uint32_t slot = sb + L::ring + (it & 1) * kATSlot;
+      const uint32_t slot = sb + L::ring + (it % kATRing) * kATSlot;
+      if (kATRing > 2 && kind == 2) wait_slot((it - 1) % kATRing);  // the tail does not refill: S, PV done
       if (kind == 2) {
         // ---- online softmax of chunk ch (S^T_ch complete: its last MMA was item it - 1)
         tc_fence_after();
@@ -405,18 +409,18 @@ __global__ void __launch_bounds__(kATThreads, 4) attn_tc_kernel(Shape sh, QSrc q
             umma_bf16(tmem + 32, a, bp, kIdescPV, (ch > 0 || hk2 > 0 || s > 0) ? 1u : 0u);
           }
         }
-        umma_commit_u32(mbar_a + 8u * (it & 1));
+        umma_commit_u32(mbar_a + 8u * (it % kATRing));
       }
-      pend |= 1u << (it & 1);
-      // refill this slot with item it + 2 as soon as MMA(it) has read it (two items in flight)
-      if (it + 2 < nitems) {
-        wait_slot(it & 1);
-        issue(it + 2);
+      pend |= 1u << (it % kATRing);
+      // refill this slot with item it + kATRing as soon as MMA(it) has read it
+      if (it + kATRing < nitems) {
+        wait_slot(it % kATRing);
+        issue(it + kATRing);
       }
       cp_async_commit();
     }
-    wait_slot(0);  // the last MMAs (O^T complete)
-    wait_slot(1);
+#pragma unroll
+    for (int r = 0; r < kATRing; ++r) wait_slot(r);  // the last MMAs (O^T complete)
     // ---- epilogue: O^T lanes = d, columns = queries -> normalise, stage [32 q][128 d] bf16 in the
     // (now free) ring, then 16-byte coalesced row stores
     if (threadIdx.x < 32) {
