@@ -646,9 +646,10 @@ def bench_decode_sharded(args, device, world, rank):
             "sharding": f"batch/{world} ({Bl} sequences per rank)", "gather": "NCCL all-gather of O along batch"}
 
 
-def bench_decode(args, device, T=None, options=True):
+def bench_decode(args, device, T=None, options=True, batch=None, decoder=True):
     """C3: one decode step (r_m = 1): paged mask estimation + paged sparse attention (T = 128k, or
-    the given context length, e.g. 32k — BASELINE's decode metric is quoted at both)."""
+    the given context length, e.g. 32k — BASELINE's decode metric is quoted at both; `batch`
+    overrides the batch, e.g. 1 for single-sequence latency)."""
     import torch
     from paper_2406_09827_b200 import hipattn as HA
     from paper_2406_09827_b200 import synth
@@ -656,6 +657,9 @@ def bench_decode(args, device, T=None, options=True):
     if T is not None:
         c["T"] = int(T)
         c["workload"] = c["workload"].replace("T=128k", f"T={T // 1024}k")
+    if batch is not None:
+        c["B"] = int(batch)
+        c["workload"] = c["workload"].replace("batch 16", f"batch {batch}")
     seq = [c["T"]] * c["B"]
     q = synth.gen_decode_q(c["B"], c["Hq"], c["d"], seed=args.seed, device=device)
     kp, vp, bt, sl = synth.gen_paged_direct(c["B"], c["Hkv"], seq, c["d"], c["page"], seed=args.seed, device=device)
@@ -699,23 +703,23 @@ def bench_decode(args, device, T=None, options=True):
         "dense_decode_us": dense_decode_us(kp, vp, bt, q, c),
         "step_bytes": mask_bytes + attn_bytes,
     }
-    res["hip_decoder"] = time_hip_decoder(q, kp, vp, bt, c, device, steps=max(16, args.steps))
-    # appendix / NEXT options of the same step (different masks, not Alg. 1's per-head mask):
-    # GQA-shared masks (reading G25) alone and with the stridden partial top-k (S = 4, G21)
+    if decoder:
+        res["hip_decoder"] = time_hip_decoder(q, kp, vp, bt, c, device, steps=max(16, args.steps))
+    # appendix / NEXT options of the same step (different masks, not Alg. 1's per-head mask): the
+    # stridden partial top-k (S = 4 chunks, G21), GQA-shared masks (reading G25), and both
     variants = {}
-    for name, ex in ((("gqa_shared", dict(gqa_shared=True)), ("gqa_shared_chunks4", dict(gqa_shared=True, chunks=4)))
-                     if options else ()):
+    for name, ex in ((("chunks4", dict(chunks=4)), ("gqa_shared", dict(gqa_shared=True)),
+                      ("gqa_shared_chunks4", dict(gqa_shared=True, chunks=4))) if options else ()):
         try:
-            ti = torch.empty(c["B"], c["Hkv"], 1, n, dtype=torch.int32, device=device)
-            tc = torch.empty(c["B"], c["Hkv"], 1, dtype=torch.int32, device=device)
-            akw = dict(kw, gqa_shared=True)
+            hm = c["Hkv"] if ex.get("gqa_shared") else c["Hq"]
+            ti = torch.empty(c["B"], hm, 1, n, dtype=torch.int32, device=device)
+            tc = torch.empty(c["B"], hm, 1, dtype=torch.int32, device=device)
+            akw = dict(kw, gqa_shared=bool(ex.get("gqa_shared")))
             vmu, vau = graph_times_us(
                 [lambda: HA.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(ti, tc), **kw, **ex),  # noqa: B023
                  lambda: HA.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], ti, tc, out=o, **akw)],  # noqa: B023
                 flush, reps, device)
-            variants[name] = {"mask_us": round(vmu, 2), "attn_us": round(vau, 2), "us_per_step": round(vmu + vau, 2),
-                              "mask_bytes": mask_bytes // (c["Hq"] // c["Hkv"]),
-                              "mask_gbs": round(mask_bytes / (c["Hq"] // c["Hkv"]) / (vmu * 1e-6) / 1e9, 1)}
+            variants[name] = {"mask_us": round(vmu, 2), "attn_us": round(vau, 2), "us_per_step": round(vmu + vau, 2)}
         except Exception as e:  # noqa: BLE001 - an option failing must not hide the headline
             variants[name] = {"error": repr(e)}
     if options:
@@ -878,6 +882,7 @@ def main():
         try:
             extras["decode"] = bench_decode(args, device)
             extras["decode_32k"] = bench_decode(args, device, T=32768, options=False)
+            extras["decode_batch1"] = bench_decode(args, device, options=True, batch=1, decoder=False)
         except Exception as e:  # noqa: BLE001 - report, do not hide the headline
             extras["decode"] = {"error": repr(e)}
         torch.cuda.empty_cache()
