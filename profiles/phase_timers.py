@@ -33,12 +33,19 @@ def main():
     fn = lib.hip_debug_phase_cycles
     fn.argtypes = [ctypes.c_void_p]
     T, Hh = int(os.environ.get("PT_T", 32768)), int(os.environ.get("PT_H", 32))
-    Q, K, _ = synth.gen_qkv(1, Hh, Hh, T, T, 128, "llm", seed=0, device="cuda", make_v=False)
-    H.mask_estimate(Q, K)
+    if os.environ.get("PT_DECODE"):  # paged decode mask, batch PT_DECODE, 32 q / 8 kv heads (C3 shape)
+        B = int(os.environ["PT_DECODE"])
+        q = synth.gen_decode_q(B, 32, 128, seed=0, device="cuda")
+        kp, vp, bt, sl = synth.gen_paged_direct(B, 8, [T] * B, 128, 64, seed=0, device="cuda")
+        run = lambda: H.mask_estimate_paged(q, kp, bt, sl, T, k_budget=512, b_q=1, b_k=2)  # noqa: E731
+    else:
+        Q, K, _ = synth.gen_qkv(1, Hh, Hh, T, T, 128, "llm", seed=0, device="cuda", make_v=False)
+        run = lambda: H.mask_estimate(Q, K)  # noqa: E731
+    run()
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 16)()
     fn(buf)
-    H.mask_estimate(Q, K)
+    run()
     fn(buf)
     tot = sum(buf[i] for i in range(9))
     for i, nm in enumerate(PHASES):

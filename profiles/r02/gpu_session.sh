@@ -1,1 +1,2 @@
-timeout 600 python profiles/kexp.py time tpriv --cfg c2 --reps 5
+PT_T=131072 PT_DECODE=1 python profiles/phase_timers.py
+PT_T=131072 PT_DECODE=16 python profiles/phase_timers.py
