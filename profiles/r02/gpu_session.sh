@@ -1,5 +1,2 @@
-# round-2 final validation: full GPU suite, smoke, default bench
-python -m pytest tests -m gpu -q 2>&1 | tail -4 > gpurun_out/pytest_final.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final.log 2>&1
-python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
-cat gpurun_out/pytest_final.log gpurun_out/smoke_final.log
+timeout 900 python profiles/kexp.py time prev,base --cfg c3,c3_32k,c3b4 --reps 7 --rounds 2
+timeout 1200 python -m pytest tests -m gpu -x -q -k "decode or decoder or paged or composition or dist_gpu or concurrent" 2>&1 | tail -5
