@@ -5,7 +5,8 @@ compute-sanitizer; no checking here — the parity tests do that):
 
 Cases (kernel, instantiation): mask_tc prefill b_k = 2 / b_k = 4, paged decode b_k = 2 / 4, ensemble
 jitter, top-r, GQA-shared; mask_cc (fp32, exact bf16); mask_decode (fp32 GEMV); attn_tc prefill
-plain / sink + window / wide (union masks), paged decode split-K and unsplit; attn_cc (fp32);
+plain / sink + window / wide (union masks), paged decode split-K and unsplit; the small-batch decode
+mask rings (8 and 4 slots); attn_cc (fp32);
 attn_decode (fp32 GEMV); the ensemble vote.  Sizes span several tiles and ragged tails and stay
 small enough for racecheck.
 """
@@ -54,7 +55,7 @@ def main():
     run("vote", lambda: H.mask_vote(I, C, theta=2, tau=1))
     run("attn_tc wide", lambda: H.sparse_attention_prefill(Q, K, V, vi, vc, k_budget=vi.shape[-1] * 2, b_q=32, b_k=2))
     # paged decode: split-K (few units) and unsplit (>= the CTA slots)
-    for B, Hq, Hkv, Tmax, tag in ((3, 8, 2, T, "split-K"), (20, 32, 8, 400, "unsplit")):
+    for B, Hq, Hkv, Tmax, tag in ((3, 8, 2, T, "split-K"), (20, 32, 8, 400, "unsplit"), (1, 32, 8, T, "batch-1")):
         seq = [max(1, Tmax - 97 * b) for b in range(B)]
         q = synth.gen_decode_q(B, Hq, 128, seed=2, dtype=bf, device=dev)
         kp, vp, bt, sl = (x.to(dev) for x in synth.gen_paged_direct(B, Hkv, seq, 128, 16, seed=2, dtype=bf))
@@ -71,6 +72,10 @@ def main():
             run("mask_decode fp32", lambda: H.mask_estimate_paged(qf, kpf, bt, sl, Tmax, **dk))
             run("attn_decode fp32", lambda: H.sparse_attention_decode(qf, kpf, vpf, bt, sl, Tmax, di, dc, **dk))
             run("mask_tc decode gqa-shared", lambda: H.mask_estimate_paged(q, kp, bt, sl, Tmax, gqa_shared=True, **dk))
+    # decode mask, 2 units per SM or fewer: the 4-slot ring instantiation
+    q4 = synth.gen_decode_q(8, 32, 128, seed=3, dtype=bf, device=dev)
+    kp4, vp4, bt4, sl4 = (x.to(dev) for x in synth.gen_paged_direct(8, 8, [T] * 8, 128, 16, seed=3, dtype=bf))
+    run("mask_tc decode 4-slot ring", lambda: H.mask_estimate_paged(q4, kp4, bt4, sl4, T, k_budget=256, b_q=1, b_k=2))
     print("[sanitize] all cases ran", flush=True)
 
 
