@@ -64,7 +64,8 @@ struct MaskTCSmemLayout {
   static constexpr uint32_t total = jq + 16;
 };
 
-template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kGrp = false, bool kRow1 = false, bool kBk2 = false>
+template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kGrp = false, bool kRow1 = false, bool kBk2 = false,
+          int CL = 1>
 struct TCScorer {
   static_assert(SLOTS >= 2 && SLOTS <= 8, "ring of 2..8 slots");
   static constexpr int RPP = NT / 8;        // rows per pass (8 threads per 128-byte half row)
@@ -86,6 +87,7 @@ struct TCScorer {
   // the second row is the first plus one row stride)
   const char* rp[kBk2 ? 4 : RJ];
   uint32_t rok;          // bit j: rp[j] is a real row (< T_k, block < n_rep)
+  int crank = 0;         // CL > 1: this CTA's rank in the unit's cluster; it scores tiles crank + CL j
   uint32_t ckeep = 3u;   // top-r: bit h = this thread's chunk of d-half h has a kept component
                          // (else the chunk is zero-filled without a global read, topr.cuh)
   HIP_PT_MEMBER
@@ -93,6 +95,7 @@ struct TCScorer {
   __device__ __forceinline__ void mark(int p) { HIP_MARK(p); (void)p; }
 
   __device__ __forceinline__ const char* row(int s) const { return kh + (uint64_t)(uint32_t)s * row_bytes; }
+  __device__ __forceinline__ int gtile(int lt) const { return CL == 1 ? lt : crank + lt * CL; }  // local -> call tile
   // Paged: key row s of a block whose page was looked up once per call (pg).
   __device__ __forceinline__ const char* paged_row(int page, int s) const {
     const uint32_t off = ks.page_shift >= 0 ? ((uint32_t)s & ((1u << ks.page_shift) - 1u))
@@ -103,7 +106,7 @@ struct TCScorer {
   // Item i of a round = (tile c0 + i / 2, d-half i % 2) into slot i % SLOTS.  The row pointers are
   // computed once per tile (at its first half).
   __device__ __forceinline__ void issue(const int* rep, int n_rep, int c0, int i) {
-    const int c = c0 + (i >> 1), h = i & 1;
+    const int c = gtile(c0 + (i >> 1)), h = i & 1;
     const int tid = Sync::tid(), c8 = tid & 7, r0 = tid >> 3;
     if constexpr (kBk2) {  // b_k = 2 (the paper's setting): thread (c8, g) owns the 8 consecutive rows 8g..8g+7
       issue_bk2(rep, n_rep, c, h, c8, r0, i);
@@ -175,7 +178,7 @@ struct TCScorer {
     const int warp = Sync::tid() >> 5, lane = threadIdx.x & 31;
     const int r = 32 * warp + lane, bm = (1 << lbk) - 1;
     for (int cc = 0; cc < nt; ++cc) {
-      const int c = c0 + cc;
+      const int c = gtile(c0 + cc);
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int lb = r >> lbk;
       float best = -INFINITY;
@@ -189,6 +192,8 @@ struct TCScorer {
         if (lb < nblk && (r & bm) == 0) {
           HIP_DBG_STORE(rep[blk0 + lb], best);
           out[blk0 + lb] = best;
+          if constexpr (CL > 1)  // every CTA of the cluster selects on all the scores
+            for (int rr = 1; rr < CL; ++rr) st_cluster_f32(smem_u32(out + blk0 + lb), (crank + rr) % CL, best);
         }
         continue;
       }
@@ -219,12 +224,20 @@ struct TCScorer {
       if (lb < nblk && (r & bm) == 0) {
         HIP_DBG_STORE(rep[blk0 + lb], best);
         out[blk0 + lb] = best;
+        if constexpr (CL > 1)
+          for (int rr = 1; rr < CL; ++rr) st_cluster_f32(smem_u32(out + blk0 + lb), (crank + rr) % CL, best);
       }
     }
   }
 
   __device__ void score(const int* rep, int n_rep, float* out) {
-    const int ntiles = (n_rep + bpt - 1) / bpt;
+    const int ntiles_all = (n_rep + bpt - 1) / bpt;
+    // CL > 1: the cluster's CTAs hold identical search states; CTA `crank` gathers and scores tiles
+    // crank, crank + CL, ... and stores each score into every CTA's score array (DSMEM).  A cluster
+    // barrier first (every CTA has read its nodes for this iteration: the scores alias the node
+    // arrays) and last (every score everywhere before the selections).
+    if constexpr (CL > 1) cluster_sync();
+    const int ntiles = CL == 1 ? ntiles_all : (ntiles_all > crank ? (ntiles_all - crank + CL - 1) / CL : 0);
     if constexpr (kPaged) {
       // one block-table lookup per representative block for the whole call (a block never straddles
       // a page), so the gathers below carry no dependent global load.  pg[i] is read only before
@@ -232,6 +245,7 @@ struct TCScorer {
       int* pgw = reinterpret_cast<int*>(out);
       const int32_t* bt = ks.block_table + (int64_t)b * ks.max_pages;
       for (int i = Sync::tid(); i < n_rep; i += NT) {
+        if (CL > 1 && ((i / bpt) % CL) != crank) continue;  // another CTA's tile (its score may land here)
         const uint32_t s0 = (uint32_t)rep[i] << lbk;
         const uint32_t pi = ks.page_shift >= 0 ? (s0 >> ks.page_shift) : (s0 / (uint32_t)ks.page_size);
         pgw[i] = bt16 ? (int)bt16[pi] : __ldg(bt + pi);  // staged row: no global round trip
@@ -281,6 +295,7 @@ struct TCScorer {
       Sync::sync();  // scores visible; TMEM reads done before the next round's MMAs
       mark(3);  // epilogue
     }
+    if constexpr (CL > 1) cluster_sync();
   }
 };
 
@@ -289,7 +304,7 @@ struct TCScorer {
 // carries none of their code or registers: bit 0 ensemble split jitter (G23), bit 1 top-r (G22),
 // bit 2 GQA-shared rows (G25); bit 3 = one query row per unit (decode), whose epilogue reads a single
 // TMEM column per key; bit 4 = b_k = 2, the gather mapping with 4 blocks per thread.
-template <int SLOTS, int TT, bool kPaged, int MINB, int EXT>
+template <int SLOTS, int TT, bool kPaged, int MINB, int EXT, int CL = 1>
 __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc, RowSrc ks,
                                                                    int32_t* __restrict__ idx,
                                                                    int32_t* __restrict__ cnt) {
@@ -329,8 +344,10 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
 
   const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb;
   const int S = max(sh.chunks, 1);
+  // CL > 1: one unit per cluster of CL CTAs (grid = units x CL; the launcher guarantees a single wave)
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   JobQueue jq(sh.sched, base + L::jq);
-  for (int64_t jb = blockIdx.x; jb < units * S; jb = jq.next(jb)) {
+  for (int64_t jb = CL > 1 ? blockIdx.x / CL : blockIdx.x; jb < units * S; jb = jq.next(jb)) {
     jq.claim();
     const int64_t u = jb / S;
     const int cs = (int)(jb - u * S);
@@ -398,7 +415,8 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
       }
       cp_async_commit();
     }
-    TCScorer<NT, SLOTS, TT, kPaged, Sync, kGrp, kRow1, kBk2> sc;
+    TCScorer<NT, SLOTS, TT, kPaged, Sync, kGrp, kRow1, kBk2, CL> sc;
+    sc.crank = crank;
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = smem_u32(mbar);
@@ -431,7 +449,7 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
     tree_search<kMTNmax, NT, decltype(sc), Sync>(st, nn, lo, len, sc, idx + lin * sh.n + slot0, nullptr,
                                                  kJit ? make_jitter(sh.jitter, sh.seed, lin) : SplitJitter());
     phase = sc.phase;
-    if (cs == 0 && Sync::tid() == 0) cnt[lin] = min(Bq, sh.n);
+    if (cs == 0 && Sync::tid() == 0 && crank == 0) cnt[lin] = min(Bq, sh.n);
     Sync::sync();
   }
   tc_fence_before();
@@ -468,6 +486,35 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
   return cudaGetLastError();
 }
 
+// One unit per cluster of CL CTAs on CL SMs (small decode batches: the units would leave SMs idle,
+// and one SM's memory-level parallelism bounds a unit's gathers).  Grid = units x CL, one wave.
+template <int SLOTS, int TT, int EXT, int CL>
+static cudaError_t launch_cluster(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
+                                  cudaStream_t stream) {
+  const size_t smem = (ks.paged ? MaskTCSmemLayout<SLOTS, true>::total : MaskTCSmemLayout<SLOTS, false>::total) + 1024;
+  auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, true, 1, EXT, CL> : mask_tc_kernel<SLOTS, TT, false, 1, EXT, CL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb * std::max(sh.chunks, 1);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(units * CL));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  Shape s2 = sh;
+  s2.sched = nullptr;  // one unit per cluster, no claiming
+  e = cudaLaunchKernelEx(&cfg, kern, s2, qs, ks, idx, cnt);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // One instantiation per mask option (EXT bits above), so none inflates another's registers; the
 // b_k = 2 gather mapping (bit 4) and the single-row decode epilogue (bit 3) are specialisations of
 // Alg. 1 itself.  Dispatch depends on the arguments only.
@@ -479,8 +526,13 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
     case 0:
       if (sh.bk == 2) {
         if (sh.bq == 1) {  // decode
-          // Small batches leave SMs idle: give each unit a deeper ring instead (one unit per SM: 8
-          // slots, a whole iteration's 8 items in flight; two per SM: 4 slots).  Same arithmetic.
+          // Small batches leave SMs idle: spread each unit over a cluster of 4 or 2 CTAs (SMs) when the
+          // units fit, else give each unit a deeper ring (one unit per SM: 8 slots, a whole
+          // iteration's 8 items in flight; two per SM: 4 slots).  Same arithmetic.
+          if (sh.chunks <= 1 && 4 * jobs <= num_sms)
+            return launch_cluster<4, 4, 8 | 16, 4>(sh, qs, ks, idx, cnt, stream);
+          if (sh.chunks <= 1 && 2 * jobs <= num_sms)
+            return launch_cluster<4, 4, 8 | 16, 2>(sh, qs, ks, idx, cnt, stream);
           if (jobs <= num_sms) return launch_v<8, 4, 1, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
           if (jobs <= 2 * (int64_t)num_sms) return launch_v<4, 4, 2, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
           return launch_v<2, 4, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
