@@ -537,6 +537,9 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
           if (jobs <= 2 * (int64_t)num_sms) return launch_v<4, 4, 2, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
           return launch_v<2, 4, 4, 8 | 16>(sh, qs, ks, idx, cnt, stream, num_sms);
         }
+        // few units (short prompts, small batches): a cluster of CTAs per unit, as for decode
+        if (sh.chunks <= 1 && 4 * jobs <= num_sms) return launch_cluster<4, 4, 16, 4>(sh, qs, ks, idx, cnt, stream);
+        if (sh.chunks <= 1 && 2 * jobs <= num_sms) return launch_cluster<4, 4, 16, 2>(sh, qs, ks, idx, cnt, stream);
         return launch_v<2, 4, 4, 16>(sh, qs, ks, idx, cnt, stream, num_sms);
       }
       if (sh.bq == 1) return launch_v<2, 4, 4, 8>(sh, qs, ks, idx, cnt, stream, num_sms);

@@ -1,2 +1,4 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -k "decode or decoder or paged or composition or dist_gpu or concurrent or replay" 2>&1 | tail -5
-timeout 600 python profiles/kexp.py time base --cfg c3b1,c3b4,c3 --reps 9
+python -m pytest tests -m gpu -q 2>&1 | tail -4 > gpurun_out/pytest_final2.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final2.log 2>&1
+python bench.py > gpurun_out/bench_final2.json 2> gpurun_out/bench_final2.err
+cat gpurun_out/pytest_final2.log gpurun_out/smoke_final2.log
