@@ -495,7 +495,7 @@ static cudaError_t launch_cluster(const Shape& sh, const QSrc& qs, const RowSrc&
   auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, true, 1, EXT, CL> : mask_tc_kernel<SLOTS, TT, false, 1, EXT, CL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb * std::max(sh.chunks, 1);
+  const int64_t units = (int64_t)sh.B * (sh.group > 1 ? sh.Hkv : sh.Hq) * sh.nqb * std::max(sh.chunks, 1);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(units * CL));
   cfg.blockDim = dim3(128);
@@ -546,7 +546,10 @@ cudaError_t launch_mask_tc(const Shape& sh, const QSrc& qs, const RowSrc& ks, in
       return launch_v<2, 4, 4, 0>(sh, qs, ks, idx, cnt, stream, num_sms);
     case 1: return launch_v<2, 4, 4, 1>(sh, qs, ks, idx, cnt, stream, num_sms);
     case 2: return launch_v<2, 4, 4, 2>(sh, qs, ks, idx, cnt, stream, num_sms);
-    case 4: return launch_v<2, 4, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
+    case 4:  // GQA-shared masks: one unit per kv head, so few units at small batch -> clusters
+      if (sh.chunks <= 1 && 8 * jobs <= num_sms) return launch_cluster<4, 4, 4, 8>(sh, qs, ks, idx, cnt, stream);
+      if (sh.chunks <= 1 && 4 * jobs <= num_sms) return launch_cluster<4, 4, 4, 4>(sh, qs, ks, idx, cnt, stream);
+      return launch_v<2, 4, 4, 4>(sh, qs, ks, idx, cnt, stream, num_sms);
     default: return launch_v<2, 4, 4, 7>(sh, qs, ks, idx, cnt, stream, num_sms);
   }
 }
