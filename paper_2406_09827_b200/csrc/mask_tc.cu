@@ -23,10 +23,13 @@
 // be in flight per SM for the ~15 TB/s L2 gather ceiling) and by the selection's serial chain.
 //
 // Launch shape: one unit (b, h, query block) per 128-thread CTA with a private 2-slot ring, 4 CTAs
-// per SM.  Round 1 measured and rejected deeper rings with fewer units (3 slots x 3 CTAs), two units
-// sharing one ring ("ping-pong") and five units per SM under a 96-register cap; TMA was measured and
-// rejected for these gathers as well: one {64 x b_k} box per block (the only box shape that lands
-// in a UMMA layout) runs at ~half the cp.async rate (profiles/r01/notes.md).
+// per SM, units claimed in order from a per-launch counter (common.cuh JobQueue).  When the units
+// would leave SMs idle (decode at small batch, short prompts) a unit instead runs on a cluster of
+// 2-8 CTAs on separate SMs (each scores a share of the tiles, scores exchanged through DSMEM) or on
+// a deeper ring.  Measured and rejected (profiles/r01/notes.md, profiles/r02/notes.md): deeper rings
+// with fewer units, rings shared between units (a lock in round 1, a slot allocator in round 2), five
+// units per SM under a 96-register cap, one CTA per GQA group with collective scoring, TMA boxes
+// ({64 x b_k} per block: ~half the cp.async rate).
 #include "kernels.h"
 #include "select.cuh"
 #include "topr.cuh"
