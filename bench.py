@@ -775,8 +775,8 @@ def config_obj(cfg, world, chunks=1):
             "b_q": cfg["bq"], "b_k": cfg["bk"], "causal": True, "dist": cfg["dist"],
             "parallelism": (f"heads/{world}, {chunks} head chunks per rank, all-gather per chunk overlapped"
                             if world > 1 else "single GPU"),
-            "l2": "L2 flushed (256 MB write, untimed) before every timed step; inputs larger than L2 (Q,K,V,O = "
-                  "%.2f GB)" % (4 * cfg["B"] * cfg["H"] * cfg["T"] * cfg["d"] * (4 if cfg["dtype"] == "f32" else 2) / 1e9)}
+            "l2": "L2 flushed (256 MB write, untimed) before every timed step (Q,K,V,O = %.2f GB)"
+                  % (4 * cfg["B"] * cfg["H"] * cfg["T"] * cfg["d"] * (4 if cfg["dtype"] == "f32" else 2) / 1e9)}
 
 
 def reference_arm(args, cfg):
