@@ -46,12 +46,6 @@ struct Row1Smem {
   static constexpr uint32_t total = flag + 16;
 };
 
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar) : "memory");
-}
 
 // acc <- acc (+) part: two softmax states over disjoint key sets merged at their common max.  The
 // unit's result is the merge of its chunk states in chunk order, whichever jobs computed the chunks

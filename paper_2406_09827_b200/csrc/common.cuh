@@ -236,6 +236,14 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Arrive on `bar` once all of this thread's earlier cp.async copies have landed (no pending-count
+// increment: the barrier's expected count includes this arrival).
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void umma_commit_u32(uint32_t addr) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(addr)
                : "memory");
