@@ -267,6 +267,7 @@ struct TCScorer {
         cp_async_wait<SLOTS - 1>();  // item i landed
         fence_proxy_async_smem();
         Sync::sync();
+        mark(11);  // (profiling builds) landing wait + barrier
         const int slot = i % SLOTS;
         if (Sync::tid() == 0) {
           tc_fence_after();
@@ -281,12 +282,15 @@ struct TCScorer {
           umma_commit_u32(mbar + 8u * slot);
         }
         pend |= 1u << slot;
+        mark(12);  // MMA issue
         // refill this slot with item i + SLOTS as soon as MMA(i) has read it
         if (i + SLOTS < nitems) {
           wait_slot(slot);
+          mark(13);  // MMA completion wait
           issue(rep, n_rep, c0, i + SLOTS);
         }
         cp_async_commit();
+        mark(14);  // refill issue
       }
       mark(1);  // gathers + MMA issue
 #pragma unroll

@@ -47,8 +47,14 @@ def main():
     fn(buf)
     run()
     fn(buf)
-    tot = sum(buf[i] for i in range(9))
+    tot = sum(buf[i] for i in range(9)) + sum(buf[i] for i in range(11, 15))
     for i, nm in enumerate(PHASES):
+        print(f"{nm:22s} {100 * buf[i] / tot:5.1f}%   {buf[i] / 1e9:8.3f} Gcyc")
+    # per-item split of the gather loop (mask_tc.cu marks 11-14).  The clock read after BAR.SYNC sees the
+    # barrier's ISSUE, not its release (the block is deferred to the next dependent instruction), so
+    # the barrier wait lands in the "MMA issue" slice: read 11 + 12 together as landing + barrier + issue.
+    sub = {11: "  landing wait+barrier", 12: "  MMA issue", 13: "  MMA completion wait", 14: "  refill issue"}
+    for i, nm in sub.items():
         print(f"{nm:22s} {100 * buf[i] / tot:5.1f}%   {buf[i] / 1e9:8.3f} Gcyc")
     if buf[10]:
         print(f"radix passes per select: {buf[9] / buf[10]:.2f} over {buf[10]} selections")
