@@ -1,0 +1,146 @@
+"""Randomised GPU-vs-oracle parity over the shape space the C ABI accepts (seeded, -m gpu).
+
+Each case draws (B, H_q, H_kv, T_q, T_k, d, k, b_q, b_k, causal, dtype, contiguous or paged) from a
+fixed generator, so the run is reproducible, and crosses the combinations the hand-written cases in
+test_gpu_parity.py do not enumerate: every kernel the dispatch in csrc/api.cu can pick (tcgen05 mask
+and attention, the CUDA-core fp32 / exact kernels, the decode GEMV, the single-row attention, d = 64),
+ragged tails, T_q < T_k, b_q > T_q, b_k > T_k, n = 1, GQA ratios, non-causal, sink + sliding window.
+
+Bars:
+  * mask: bit-exact with the oracle in the order the dispatched kernel computes in — integer-valued
+    bf16 inputs (every fp32 sum exact, any order) on the tcgen05 / CUDA-core kernels; fp32 with
+    HIP_FLAG_EXACT_SCORES == oracle F32C; fp32 without it == F32L where the decode GEMV runs
+    (min(b_q, T_q) <= 4 rows, b_k <= 16, power of two), F32C otherwise.
+  * attention on the ORACLE's mask (no GPU output ever feeds the oracle): max-abs <= 1e-4 (fp32) /
+    2e-2 (bf16), lse <= 1e-3 where finite, identical -inf pattern.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2406_09827_b200 import hipattn as H
+from paper_2406_09827_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+N_CASES = 96
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    H.load()
+
+
+def _case(i):
+    """Case i of the fixed stream: a dict of shape / option parameters, always a valid ABI call."""
+    r = np.random.default_rng(20261018 + 7919 * i)
+    dt = torch.bfloat16 if r.random() < 0.6 else torch.float32
+    d = 128 if r.random() < 0.8 else 64
+    Hkv = int(r.choice([1, 2]))
+    Hq = Hkv * int(r.choice([1, 2, 4]))
+    B = int(r.choice([1, 2]))
+    bk = int(r.choice([1, 2, 2, 4, 8, 16]))
+    bq = int(r.choice([1, 4, 16, 32, 32, 64]))
+    n = int(r.choice([1, 8, 32, 64, 128, 256]))
+    k = n * bk
+    Tk = int(r.integers(1, 2600))
+    causal = bool(r.random() < 0.75)
+    Tq = int(r.integers(1, Tk + 1)) if r.random() < 0.4 else Tk
+    if not causal and r.random() < 0.3:
+        Tq = int(r.integers(1, 700))  # non-causal: any T_q
+    paged = bool(r.random() < 0.25)
+    if paged:  # decode / speculative-decode regime over a paged cache
+        Tq = min(Tq, int(r.choice([1, 1, 4, 16, 64])))
+    ps = int(r.choice([p for p in (16, 32, 64) if p % bk == 0] or [bk]))
+    sink = window = 0
+    if r.random() < 0.3:  # attention sink + sliding window, sink + window + b_q - 1 <= 256
+        sink, window = int(r.choice([0, 4, 32])), int(r.choice([0, 16, 128]))
+        if sink + window + bq - 1 > 256:
+            sink, window = 4, 16
+    return dict(dt=dt, d=d, B=B, Hq=Hq, Hkv=Hkv, Tq=Tq, Tk=Tk, bq=bq, bk=bk, k=k, causal=causal, paged=paged,
+                ps=ps, sink=sink, window=window)
+
+
+def _decode_gemv(c):
+    """Mirror of csrc/mask_decode.cu mask_decode_supported for the plain mask (group = 1)."""
+    rows = min(c["bq"], c["Tq"])
+    return rows <= 4 and c["bk"] <= 16 and (c["bk"] & (c["bk"] - 1)) == 0 and c["d"] in (64, 128)
+
+
+def _to_paged(K, V, ps, seed):
+    """Contiguous [B, H_kv, T, d] -> ([pages, H_kv, ps, d] x 2, block table, seq lens), pages in a seeded
+    permuted order (the oracle reads the same pages through the same table)."""
+    B, Hkv, T, d = K.shape
+    npg = -(-T // ps)
+    perm = torch.randperm(B * npg, generator=torch.Generator().manual_seed(seed))
+    kp = torch.zeros(B * npg, Hkv, ps, d, dtype=K.dtype)
+    vp = torch.zeros_like(kp)
+    bt = torch.zeros(B, npg, dtype=torch.int32)
+    for b in range(B):
+        for j in range(npg):
+            p = int(perm[b * npg + j])
+            bt[b, j] = p
+            t0, t1 = j * ps, min((j + 1) * ps, T)
+            kp[p, :, : t1 - t0] = K[b, :, t0:t1]
+            vp[p, :, : t1 - t0] = V[b, :, t0:t1]
+    return kp, vp, bt, torch.full((B,), T, dtype=torch.int32)
+
+
+@pytest.mark.parametrize("i", range(N_CASES))
+def test_fuzz_mask_and_attention(orc, i):
+    c = _case(i)
+    dt, causal, k, bq, bk = c["dt"], c["causal"], c["k"], c["bq"], c["bk"]
+    dist = "int" if dt == torch.bfloat16 else ("llm" if i % 2 else "iid")
+    Q, K, V = synth.gen_qkv(c["B"], c["Hq"], c["Hkv"], c["Tq"], c["Tk"], c["d"], dist, seed=100 + i, dtype=dt)
+    if c["paged"]:
+        kp, vp, bt, sl = _to_paged(K, V, c["ps"], seed=100 + i)
+        T = c["Tk"]
+        run_mask = lambda exact: H.mask_estimate_paged(  # noqa: E731
+            Q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=bq, b_k=bk, causal=causal, exact=exact)
+        oracle_mask = lambda mode: orc.mask_paged(Q, kp, bt, sl, k, bq, bk, causal, mode=mode)  # noqa: E731
+    else:
+        run_mask = lambda exact: H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk,  # noqa: E731
+                                                 causal=causal, exact=exact)
+        oracle_mask = lambda mode: orc.mask(Q, K, k, bq, bk, causal, mode=mode)  # noqa: E731
+
+    # mask: the dispatched kernel's own order
+    oi, oc = oracle_mask(orc.F32C)
+    gi, gc = run_mask(False)
+    torch.cuda.synchronize()
+    if dt == torch.float32 and _decode_gemv(c):
+        oi_l, oc_l = oracle_mask(orc.F32L)
+        ref_i, ref_c = oi_l, oc_l
+    else:
+        ref_i, ref_c = oi, oc
+    gi, gc = gi.cpu().numpy(), gc.cpu().numpy()
+    assert np.array_equal(gc, ref_c), f"case {c}: cnt differs"
+    bad = np.argwhere((gi != ref_i).any(-1))
+    assert len(bad) == 0, f"case {c}: {len(bad)} query blocks differ, first {bad[:3].tolist()}"
+    if dt == torch.float32:  # HIP_FLAG_EXACT_SCORES: the sequential chain == F32C
+        ei, ec = run_mask(True)
+        torch.cuda.synchronize()
+        assert np.array_equal(ei.cpu().numpy(), oi) and np.array_equal(ec.cpu().numpy(), oc), f"case {c}: exact"
+
+    # attention on the oracle's selection (with the case's sink / sliding window, if any)
+    sw = (c["sink"], c["window"])
+    idx, cnt = torch.from_numpy(oi).cuda(), torch.from_numpy(oc).cuda()
+    if c["paged"]:
+        o, lse = H.sparse_attention_decode(Q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T, idx, cnt,
+                                           k_budget=k, b_q=bq, b_k=bk, causal=causal, sink=sw[0], window=sw[1],
+                                           return_lse=True)
+        Oo, lo = orc.sparse_attention_paged(Q, kp, vp, bt, sl, k, bq, bk, causal, oi, oc, sink=sw[0], window=sw[1])
+    else:
+        o, lse = H.sparse_attention_prefill(Q.cuda(), K.cuda(), V.cuda(), idx, cnt, k_budget=k, b_q=bq, b_k=bk,
+                                            causal=causal, sink=sw[0], window=sw[1], return_lse=True)
+        Oo, lo = orc.sparse_attention(Q, K, V, k, bq, bk, causal, oi, oc, sink=sw[0], window=sw[1])
+    torch.cuda.synchronize()
+    err = float(np.abs(o.float().cpu().numpy() - Oo).max())
+    assert err <= TOL[dt], f"case {c}: attention max-abs {err}"
+    lg = lse.cpu().numpy()
+    fin = np.isfinite(lo)
+    assert np.array_equal(np.isfinite(lg), fin), f"case {c}: lse -inf pattern"
+    if fin.any():
+        assert float(np.abs(lg[fin] - lo[fin]).max()) <= 1e-3, f"case {c}: lse"
