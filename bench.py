@@ -211,7 +211,7 @@ def bench_prefill(cfg, args, rank, world, device, pg):
     idx = torch.empty(cfg["B"], len(hs), nqb, n, dtype=torch.int32, device=device)
     cnt = torch.empty(cfg["B"], len(hs), nqb, dtype=torch.int32, device=device)
     stream = torch.cuda.current_stream(device)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
     hc = hpr // nch
     Ofull = torch.empty(cfg["B"], cfg["H"], cfg["T"], cfg["d"], dtype=Q.dtype, device=device) if world > 1 else None
 
@@ -250,12 +250,16 @@ def bench_prefill(cfg, args, rank, world, device, pg):
     torch.cuda.synchronize(device)
     with ClockSampler(device.index) as clk:
         for e in evs:
-            flush.fill_(1)
+            if os.environ.get("BENCH_WRITE_FLUSH"):
+                flush.fill_(1)
+            else:
+                read_flush(flush)
             step(e)
         torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     total_ms = sum(e[0].elapsed_time(e[2]) for e in evs)
+    print("[bench] prefill step ms: " + " ".join(f"{e[0].elapsed_time(e[2]):.3f}" for e in evs), file=sys.stderr)
     if world == 1:
         mask_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
         attn_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
