@@ -10,7 +10,7 @@ k=512, b_q=32, b_k=2, bf16, causal) that north_star's ">= 5x dense" target is st
 synthetic "llm"-structured inputs.  `--config c2` selects configs[1].
 
   value        ms per layer: sum over the K timed steps of CUDA-event device time on the launching
-               stream, max over ranks; the L2 is flushed (256 MB write) before every timed step
+               stream, max over ranks; the L2 is flushed (256 MB read) before every timed step
   dense        the same layer as dense causal flash attention (torch SDPA) and the speedup
   e2e          the same through the public API with pinned HOST buffers: H2D of Q/K/V + the layer
                + D2H of O inside the timed region
@@ -779,7 +779,7 @@ def config_obj(cfg, world, chunks=1):
             "b_q": cfg["bq"], "b_k": cfg["bk"], "causal": True, "dist": cfg["dist"],
             "parallelism": (f"heads/{world}, {chunks} head chunks per rank, all-gather per chunk overlapped"
                             if world > 1 else "single GPU"),
-            "l2": "L2 flushed (256 MB write, untimed) before every timed step (Q,K,V,O = %.2f GB)"
+            "l2": "L2 flushed (256 MB read, untimed) before every timed step (Q,K,V,O = %.2f GB)"
                   % (4 * cfg["B"] * cfg["H"] * cfg["T"] * cfg["d"] * (4 if cfg["dtype"] == "f32" else 2) / 1e9)}
 
 
