@@ -52,6 +52,7 @@ DECODE = dict(workload="C3 Llama-3-8B-shaped GQA decode, paged KV T=128k, batch 
               d=128, k=512, bk=2, page=64, dtype="bf16")
 DEFAULT_CONFIG = "c4"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+HOST_COVER_CYCLES = 400_000  # ~200 us of device-side spin before a timed launch whose host call is slow
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
 
 
@@ -583,22 +584,33 @@ def time_hip_decoder(q, kp, vp, bt, c, device, steps=16):
         dec.idx = dec.cnt = None  # the timed run starts with a refresh
         dec.refreshes = 0
         torch.cuda.synchronize(device)
-        ev = []
+        ev, refreshed = [], []
         for t in range(steps):
             sl.copy_(sls[t])
             read_flush(flush)
+            # keep the device busy (untimed) while the host runs graphed_step's Python preamble, so the
+            # interval between the events is the step's device time, not the host's launch latency
+            torch.cuda._sleep(HOST_COVER_CYCLES)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
+            r0 = dec.refreshes
             dec.graphed_step(q, kp, vp, bt, sl, [lens[t]] * c["B"], o)
             e1.record(st)
             ev.append((e0, e1))
+            refreshed.append(dec.refreshes > r0)
         torch.cuda.synchronize(device)
         per = [1e3 * a.elapsed_time(b) for a, b in ev]
-        ref = [p for p, L in zip(per, lens) if r_m == 1 or L % r_m == 0]
-        cached = [p for p, L in zip(per, lens) if r_m > 1 and L % r_m]
+        # classified by what the step ran (the first step refreshes: nothing is cached yet)
+        ref = [p for p, f in zip(per, refreshed) if f]
+        cached = [p for p, f in zip(per, refreshed) if not f]
+        mr = statistics.mean(ref) if ref else None
+        mc = statistics.mean(cached) if cached else None
         out[f"r_m{r_m}"] = {"us_per_step": round(sum(per) / steps, 2), "refreshes": dec.refreshes, "steps": steps,
-                            "us_refresh_steps": round(statistics.mean(ref), 2) if ref else None,
-                            "us_cached_steps": round(statistics.mean(cached), 2) if cached else None}
+                            "us_refresh_steps": round(mr, 2) if mr is not None else None,
+                            "us_cached_steps": round(mc, 2) if mc is not None else None,
+                            # one refresh every r_m steps, as the loop runs once warm
+                            "us_per_step_steady": round((mr + (r_m - 1) * mc) / r_m, 2) if r_m > 1 and ref and cached
+                            else (round(mr, 2) if mr is not None else None)}
     out["note"] = ("HipDecoder.graphed_step (decode.py, CUDA graphs): mask estimation when the length is divisible by "
                    "r_m, then the paged sparse attention with sink 32 + window 128; seq lengths T-16+1..T; L2 "
                    "read-flushed before every step")

@@ -82,10 +82,16 @@ def _time_one(path, cfgs, reps):
     for cn in cfgs:
         if cn.startswith("c3"):  # c3, c3_32k, c3b1 / c3b4 (batch 1 / 4)
             c = dict(bench.DECODE)
-            if cn == "c3_32k":
+            if cn.startswith("c3_32k"):
                 c["T"] = 32768
-            if cn.startswith("c3b"):
-                c["B"] = int(cn[3:])
+            sw = {}
+            if cn.endswith("sw"):  # attention with the paper's sink 32 + window 128 (Alg. 2 cached steps)
+                sw = dict(sink=32, window=128)
+                cn0 = cn[:-2]
+            else:
+                cn0 = cn
+            if cn0.startswith("c3b"):
+                c["B"] = int(cn0[3:])
             seq = [c["T"]] * c["B"]
             q = synth.gen_decode_q(c["B"], c["Hq"], c["d"], seed=0, device=dev)
             kp, vp, bt, sl = synth.gen_paged_direct(c["B"], c["Hkv"], seq, c["d"], c["page"], seed=0, device=dev)
@@ -95,7 +101,7 @@ def _time_one(path, cfgs, reps):
             cnt = torch.empty(c["B"], c["Hq"], 1, dtype=torch.int32, device=dev)
             o = torch.empty_like(q)
             m, a = timed([lambda: H.mask_estimate_paged(q, kp, bt, sl, c["T"], out=(idx, cnt), **kw),
-                          lambda: H.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], idx, cnt, out=o, **kw)])
+                          lambda: H.sparse_attention_decode(q, kp, vp, bt, sl, c["T"], idx, cnt, out=o, **kw, **sw)])
             out.append({"cfg": cn, "mask_us": round(m * 1e3, 2), "attn_us": round(a * 1e3, 2),
                         "step_us": round((m + a) * 1e3, 2), "chk": checksum(idx, o)})
             del kp, vp
