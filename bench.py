@@ -898,7 +898,7 @@ def main():
         try:
             extras["decode"] = bench_decode(args, device)
             extras["decode_32k"] = bench_decode(args, device, T=32768, options=False)
-            extras["decode_batch1"] = bench_decode(args, device, options=True, batch=1, decoder=False)
+            extras["decode_batch1"] = bench_decode(args, device, options=True, batch=1, decoder=True)
         except Exception as e:  # noqa: BLE001 - report, do not hide the headline
             extras["decode"] = {"error": repr(e)}
         torch.cuda.empty_cache()
