@@ -34,8 +34,11 @@
  *                             s % page_size; gathered with plain loops.
  *
  * Arithmetic.  Inputs are float32 arrays (bf16 inputs are widened exactly by the caller).  Mask
- * scores come in two modes: ORC_F32C — `acc = fmaf(q[c], k[c], acc)` for c = 0..d-1 (the canonical
- * fp32 order, reading G9), and ORC_F64 — the dot product in double.  Attention is fp64 throughout.
+ * scores come in three modes: ORC_F32C — `acc = fmaf(q[c], k[c], acc)` for c = 0..d-1 (the canonical
+ * fp32 order, reading G9); ORC_F32L — 16 sequential fmaf segments of d/16 terms combined by the
+ * xor tree o = 8, 4, 2, 1 (the decode GEMV's order, reading G9b); and ORC_F64 — the dot product in
+ * double.  Both fp32 orders are pinned by exact rational recomputation in the pin suite (one
+ * rounding per fmaf / tree addition).  Attention is fp64 throughout.
  * Compile with -ffp-contract=off and without -ffast-math so that the written order is the order run.
  *
  * Pins (tests/test_oracle_pins.py): PIN-1 k >= T => dense causal attention (vs torch SDPA fp64);
