@@ -250,6 +250,7 @@ def bench_prefill(cfg, args, rank, world, device, pg):
         dist.barrier()
     torch.cuda.synchronize(device)
     with ClockSampler(device.index) as clk:
+        step()  # untimed: the GPU sat idle while the sampler started; bring the clocks back up first
         for e in evs:
             if os.environ.get("BENCH_WRITE_FLUSH"):
                 flush.fill_(1)
