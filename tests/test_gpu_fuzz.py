@@ -144,3 +144,45 @@ def test_fuzz_mask_and_attention(orc, i):
     assert np.array_equal(np.isfinite(lg), fin), f"case {c}: lse -inf pattern"
     if fin.any():
         assert float(np.abs(lg[fin] - lo[fin]).max()) <= 1e-3, f"case {c}: lse"
+
+
+def _option_case(i):
+    """Case i of the mask-option stream: shape plus a random combination of the SURVEY §8(f) options
+    (stridden partial top-k S, top-r, ensemble jitter R / seed, GQA-shared masks)."""
+    r = np.random.default_rng(9001 + 104729 * i)
+    dt = torch.bfloat16 if r.random() < 0.5 else torch.float32
+    Hkv = int(r.choice([1, 2]))
+    Hq = Hkv * int(r.choice([1, 2, 4]))
+    bk = int(r.choice([1, 2, 2, 4]))
+    n = int(r.choice([16, 64, 128, 256]))
+    Tk = int(r.integers(64, 3000))
+    Tq = Tk if r.random() < 0.6 else int(r.integers(1, Tk + 1))
+    bq = int(r.choice([1, 8, 16, 32]))
+    gqa = bool(r.random() < 0.3)
+    if gqa:
+        bq = min(bq, 32 // (Hq // Hkv))  # the group's rows share one <= 32-row tile
+    return dict(dt=dt, B=int(r.choice([1, 2])), Hq=Hq, Hkv=Hkv, Tq=Tq, Tk=Tk, bq=bq, bk=bk, k=n * bk,
+                causal=bool(r.random() < 0.8), chunks=int(r.choice([1, 1, 2, 4])), top_r=int(r.choice([0, 0, 16, 40])),
+                jitter=int(r.choice([0, 0, 3])), seed=int(r.integers(0, 1000)), gqa=gqa)
+
+
+@pytest.mark.parametrize("i", range(48))
+def test_fuzz_mask_options(orc, i):
+    """Every option combination against the oracle, bit-exact in the dispatched kernel's order."""
+    c = _option_case(i)
+    dt = c["dt"]
+    dist = "int" if dt == torch.bfloat16 else "llm"
+    Q, K, _ = synth.gen_qkv(c["B"], c["Hq"], c["Hkv"], c["Tq"], c["Tk"], 128, dist, seed=300 + i, dtype=dt,
+                            make_v=False)
+    opt = dict(chunks=c["chunks"], top_r=c["top_r"], jitter=c["jitter"], seed=c["seed"])
+    gi, gc = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=c["k"], b_q=c["bq"], b_k=c["bk"], causal=c["causal"],
+                             gqa_shared=c["gqa"], **opt)
+    torch.cuda.synchronize()
+    group = c["Hq"] // c["Hkv"] if c["gqa"] else 1
+    gemv = min(c["bq"], c["Tq"]) * group <= 4 and c["bk"] <= 16
+    mode = orc.F32L if (dt == torch.float32 and gemv) else orc.F32C
+    oi, oc = orc.mask(Q, K, c["k"], c["bq"], c["bk"], c["causal"], mode=mode, gqa_shared=c["gqa"], **opt)
+    gi, gc = gi.cpu().numpy(), gc.cpu().numpy()
+    assert np.array_equal(gc, oc), f"case {c}: cnt differs"
+    bad = np.argwhere((gi != oi).any(-1))
+    assert len(bad) == 0, f"case {c}: {len(bad)} query blocks differ, first {bad[:3].tolist()}"
