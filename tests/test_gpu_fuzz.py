@@ -186,3 +186,63 @@ def test_fuzz_mask_options(orc, i):
     assert np.array_equal(gc, oc), f"case {c}: cnt differs"
     bad = np.argwhere((gi != oi).any(-1))
     assert len(bad) == 0, f"case {c}: {len(bad)} query blocks differ, first {bad[:3].tolist()}"
+
+
+def _decode_case(i):
+    """Case i of the decode stream: a batch of sequences of mixed lengths on a paged cache."""
+    r = np.random.default_rng(424242 + 7727 * i)
+    dt = torch.bfloat16 if r.random() < 0.6 else torch.float32
+    B = int(r.integers(1, 7))
+    Hkv = int(r.choice([1, 2, 4]))
+    Hq = Hkv * int(r.choice([1, 2, 4]))
+    bk = int(r.choice([1, 2, 2, 4]))
+    ps = int(r.choice([p for p in (16, 32, 64) if p % bk == 0]))
+    n = int(r.choice([8, 64, 256]))
+    seq = [int(x) for x in r.integers(1, 6000, size=B)]
+    Tq = int(r.choice([1, 1, 1, 4]))
+    seq = [max(s, Tq) for s in seq]
+    gqa = bool(r.random() < 0.25)
+    sw = (32, 128) if r.random() < 0.4 else (0, 0)
+    return dict(dt=dt, B=B, Hq=Hq, Hkv=Hkv, bk=bk, ps=ps, k=n * bk, seq=seq, Tq=Tq, gqa=gqa, sink=sw[0], window=sw[1],
+                chunks=int(r.choice([1, 1, 2])), top_r=int(r.choice([0, 0, 32])), jitter=int(r.choice([0, 0, 2])),
+                seed=int(r.integers(0, 100)))
+
+
+@pytest.mark.parametrize("i", range(32))
+def test_fuzz_decode_mixed_lengths(orc, i):
+    """Paged decode over a batch of different lengths (and T_q = 4 speculative rows), with random
+    mask options and sink / window: mask bit-exact, attention within tolerance of the oracle."""
+    c = _decode_case(i)
+    dt, bk, k, Tq = c["dt"], c["bk"], c["k"], c["Tq"]
+    dist = "int" if dt == torch.bfloat16 else "iid"
+    q = synth.gen_decode_q(c["B"], c["Hq"], 128, seed=500 + i, dtype=dt, dist=dist, Tq=Tq)
+    kp, vp, bt, sl = synth.gen_paged_direct(c["B"], c["Hkv"], c["seq"], 128, c["ps"], seed=500 + i, dtype=dt,
+                                            dist=dist)
+    T = max(c["seq"])
+    bq = 32 // (c["Hq"] // c["Hkv"]) if c["gqa"] else 32
+    opt = dict(chunks=c["chunks"], top_r=c["top_r"], jitter=c["jitter"], seed=c["seed"])
+    gi, gc = H.mask_estimate_paged(q.cuda(), kp.cuda(), bt.cuda(), sl.cuda(), T, k_budget=k, b_q=bq, b_k=bk,
+                                   causal=True, gqa_shared=c["gqa"], **opt)
+    torch.cuda.synchronize()
+    group = c["Hq"] // c["Hkv"] if c["gqa"] else 1
+    gemv = min(bq, Tq) * group <= 4 and bk <= 16
+    mode = orc.F32L if (dt == torch.float32 and gemv) else orc.F32C
+    oi, oc = orc.mask_paged(q, kp, bt, sl, k, bq, bk, True, mode=mode, gqa_shared=c["gqa"], **opt)
+    gi, gc = gi.cpu().numpy(), gc.cpu().numpy()
+    assert np.array_equal(gc, oc), f"case {c}: cnt differs"
+    bad = np.argwhere((gi != oi).any(-1))
+    assert len(bad) == 0, f"case {c}: {len(bad)} units differ, first {bad[:3].tolist()}"
+    o, lse = H.sparse_attention_decode(q.cuda(), kp.cuda(), vp.cuda(), bt.cuda(), sl.cuda(), T,
+                                       torch.from_numpy(oi).cuda(), torch.from_numpy(oc).cuda(), k_budget=k, b_q=bq,
+                                       b_k=bk, causal=True, sink=c["sink"], window=c["window"], return_lse=True,
+                                       gqa_shared=c["gqa"])
+    torch.cuda.synchronize()
+    ei, ec = orc.expand_gqa(oi, oc, c["Hq"]) if c["gqa"] else (oi, oc)  # the group's mask for each head
+    Oo, lo = orc.sparse_attention_paged(q, kp, vp, bt, sl, k, bq, bk, True, ei, ec, sink=c["sink"],
+                                        window=c["window"])
+    err = float(np.abs(o.float().cpu().numpy() - Oo).max())
+    assert err <= TOL[dt], f"case {c}: attention max-abs {err}"
+    fin = np.isfinite(lo)
+    assert np.array_equal(np.isfinite(lse.cpu().numpy()), fin), f"case {c}: lse -inf pattern"
+    if fin.any():
+        assert float(np.abs(lse.cpu().numpy()[fin] - lo[fin]).max()) <= 1e-3, f"case {c}: lse"
