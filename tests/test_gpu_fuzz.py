@@ -246,3 +246,39 @@ def test_fuzz_decode_mixed_lengths(orc, i):
     assert np.array_equal(np.isfinite(lse.cpu().numpy()), fin), f"case {c}: lse -inf pattern"
     if fin.any():
         assert float(np.abs(lse.cpu().numpy()[fin] - lo[fin]).max()) <= 1e-3, f"case {c}: lse"
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_fuzz_tcgen05_gaussian_replay(orc, i):
+    """The tcgen05 mask on Gaussian bf16 inputs over random shapes (b_q, b_k, n, T, causal, GQA):
+    sampled units checked as in test_gpu_replay — every dumped score within the fp32 error bound of
+    fp64, the oracle's selection replayed on the GPU's scores equals the GPU mask, and any difference
+    from the fp64 mask is certified at its first divergent iteration."""
+    from test_gpu_replay import _slot_map, _stats, check_unit
+    r = np.random.default_rng(77 + 31337 * i)
+    Hkv = int(r.choice([1, 2]))
+    Hq = Hkv * int(r.choice([1, 2]))
+    bq = int(r.choice([1, 4, 16, 32]))
+    bk = int(r.choice([1, 2, 4, 8, 16, 32]))
+    n = int(r.choice([8, 64, 256]))
+    k = n * bk
+    Tk = int(r.integers(2 * n * bk // 2 + 1, 3000)) if n * bk < 3000 else 3000
+    causal = bool(r.random() < 0.75)
+    Tq = Tk if r.random() < 0.6 else int(r.integers(1, Tk + 1))
+    d = 128
+    Q, K, _ = synth.gen_qkv(1, Hq, Hkv, Tq, Tk, d, "iid" if i % 2 else "llm", seed=700 + i, dtype=torch.bfloat16,
+                            make_v=False)
+    nqb, nkb = -(-Tq // bq), -(-Tk // bk)
+    units = sorted(set(int(u) for u in r.integers(0, Hq * nqb, size=min(48, Hq * nqb))))
+    dump = torch.full((len(units), nkb), float("nan"), dtype=torch.float32, device="cuda")
+    with H.debug_score_dump(_slot_map(units, Hq * nqb, "cuda"), dump):
+        idx, _ = H.mask_estimate(Q.cuda(), K.cuda(), k_budget=k, b_q=bq, b_k=bk, causal=causal)
+    torch.cuda.synchronize()
+    gi, gs = idx.cpu().numpy(), dump.cpu().numpy()
+    st = _stats()
+    g = Hq // Hkv
+    for s, u in enumerate(units):
+        h, q = divmod(u, nqb)
+        check_unit(orc, Q[:, h:h + 1], K[:, h // g:h // g + 1], k, bq, bk, causal, q, gi[0, h, q], gs[s], d, st)
+    print(f"\n[fuzz replay] case {i} (bq={bq} bk={bk} n={n} Tq={Tq} Tk={Tk} causal={causal}): {st}")
+    assert st["unexplained"] == 0
