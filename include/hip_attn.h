@@ -141,11 +141,10 @@ int32_t hip_num_blocks(const hip_params_t* params);
  * run concurrently (different streams without ordering), exactly like the outputs.
  *   - every op: 256 bytes for the launch's job counter (persistent CTAs claim (b, h, query block)
  *     jobs in order, which balances uneven query blocks and keeps the running jobs within one or
- *     two heads, so that head's K stays L2-resident);
- *   - HIP_OP_PREFILL / HIP_OP_DECODE with single-row units (min(b_q, T_q) = 1), d = 128 and at most
- *     4096 units (B * H_q * T_q): + the split-K region, units * (4 + 8 * 132 * 4) bytes rounded up
- *     (per-unit arrival counters and up to 8 partial softmax states of d + 4 floats), used when the
- *     units do not fill the GPU (decode).
+ *     two heads, so that head's K stays L2-resident).
+ *   (Single-row attention units split over idle CTA slots run each unit on a thread-block cluster
+ *   and merge the partial softmax states in shared memory, so they need nothing more; ABI 2.0
+ *   callers that size the workspace with this function are unaffected.)
  * Returns 0 for invalid arguments. */
 size_t hip_workspace_bytes(hip_op_t op, hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,
                            int32_t T_k, int32_t d, const hip_params_t* params);
@@ -220,7 +219,7 @@ hip_status_t hip_sparse_attention_prefill(hip_dtype_t dtype, int32_t B, int32_t 
  *   q            [B, H_q, T_q, d]; the rows sit at positions seq_lens[b] - T_q + t
  *   paged        the cache (k_pages and v_pages required)
  *   block_idx / block_cnt / o / lse as for prefill, with N_qb = ceil(T_q / b_q)
- *   workspace    device scratch of at least hip_workspace_bytes(HIP_OP_DECODE, ...) bytes (split-K)
+ *   workspace    device scratch of at least hip_workspace_bytes(HIP_OP_DECODE, ...) bytes
  *   Errors: as hip_mask_estimate.
  */
 hip_status_t hip_sparse_attention_decode(hip_dtype_t dtype, int32_t B, int32_t H_q, int32_t H_kv, int32_t T_q,

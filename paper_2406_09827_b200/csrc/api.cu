@@ -122,29 +122,12 @@ hip_status_t check_paged(const hip_paged_kv_t* pg, int esz, bool need_v, int bk)
   return HIP_SUCCESS;
 }
 
-// Workspace layout (bytes): [0, 256) the JobQueue counter of the launch; attention launches of
-// single-row units (T_q = 1 or b_q = 1, at most kSplitMaxUnits units) add the split-K region:
-// arrivals [units] uint32 (256-aligned), then partials [units][kSplitMax][kSplitStride] fp32.
+// Workspace layout (bytes): [0, 256) the JobQueue counter of the launch.  (Split single-row
+// attention units merge their chunk states through a thread-block cluster's shared memory, so no
+// call needs more.)
 constexpr size_t kWsQueue = 256;
 
-size_t split_region_bytes(int64_t units) {
-  return hip::align_up((size_t)units * 4, 256) + (size_t)units * hip::kSplitMax * hip::kSplitStride * 4;
-}
-
-int64_t attn_units(int32_t B, int32_t Hq, int32_t Tq, const hip_params_t* p) {
-  const int32_t bq = std::min(p->b_q, Tq);
-  return (int64_t)B * Hq * ((Tq + bq - 1) / bq);
-}
-
-bool split_eligible(int32_t B, int32_t Hq, int32_t Tq, int32_t d, const hip_params_t* p) {
-  return d == 128 && std::min(p->b_q, Tq) == 1 && attn_units(B, Hq, Tq, p) <= hip::kSplitMaxUnits;
-}
-
-size_t workspace_bytes_for(hip_op_t op, int32_t B, int32_t Hq, int32_t Tq, int32_t d, const hip_params_t* p) {
-  if (op == HIP_OP_MASK) return kWsQueue;
-  if (split_eligible(B, Hq, Tq, d, p)) return kWsQueue + split_region_bytes(attn_units(B, Hq, Tq, p));
-  return kWsQueue;
-}
+size_t workspace_bytes_for(hip_op_t, int32_t, int32_t, int32_t, int32_t, const hip_params_t*) { return kWsQueue; }
 
 hip_status_t check_workspace(void* ws, size_t have, size_t need) {
   if (need == 0) return HIP_SUCCESS;
@@ -154,16 +137,9 @@ hip_status_t check_workspace(void* ws, size_t have, size_t need) {
   return HIP_SUCCESS;
 }
 
-// Point the launch's scheduling / split-K state at the caller's workspace.
-void bind_workspace(hip::Shape& sh, void* ws, bool attn, int32_t B, int32_t Hq, int32_t Tq, int32_t d,
-                    const hip_params_t* p) {
-  char* w = static_cast<char*>(ws);
-  sh.sched = reinterpret_cast<unsigned int*>(w);
-  if (attn && split_eligible(B, Hq, Tq, d, p)) {
-    const int64_t units = attn_units(B, Hq, Tq, p);
-    sh.arrive = reinterpret_cast<unsigned int*>(w + kWsQueue);
-    sh.part = reinterpret_cast<float*>(w + kWsQueue + hip::align_up((size_t)units * 4, 256));
-  }
+// Point the launch's job counter at the caller's workspace.
+void bind_workspace(hip::Shape& sh, void* ws, bool, int32_t, int32_t, int32_t, int32_t, const hip_params_t*) {
+  sh.sched = reinterpret_cast<unsigned int*>(ws);
 }
 
 hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk, int32_t d, const hip_params_t* p,
@@ -181,8 +157,6 @@ hip::Shape make_shape(int32_t B, int32_t Hq, int32_t Hkv, int32_t Tq, int32_t Tk
   s.seq_lens = seq_lens;
   s.sched = nullptr;
   s.splits = 1;
-  s.part = nullptr;
-  s.arrive = nullptr;
   return s;
 }
 

@@ -17,9 +17,10 @@
 //   * probabilities stay fp32 (no bf16 rounding of P as in the tensor-core kernel).
 // Rows are staged in shared memory with the 16-byte chunk index XOR 4 * (key & 1), which makes the
 // QK reads (lanes of two keys x four quarters) bank-conflict-free per quarter warp.
-// Split-K (jobs = units x S when the units leave CTA slots idle): job (u, sp) takes items
-// [sp n / S, (sp + 1) n / S) of its unit and leaves an unnormalised partial state in the workspace;
-// the last split to arrive merges them (max-rescaled, like the warp states).
+// Split-K (when the units leave CTA slots idle): a unit runs on a thread-block cluster of S CTAs, CTA
+// sp takes the unit's 128-key chunks [sp nch / S, (sp + 1) nch / S) and keeps their states in its
+// shared memory; rank 0 merges all chunk states in chunk order through DSMEM (max-rescaled, like the
+// warp states) — the unsplit kernel's operations, so the output does not depend on S.
 #include "kernels.h"
 #include "sinkwin.cuh"
 
@@ -42,8 +43,9 @@ struct Row1Smem {
   static constexpr uint32_t merge = xlist + kMaxExtra * 4;         // [4][128] O + [4] max + [4] sum, scan scratch
   static constexpr uint32_t bar = merge + (4 * 128 + 8 + 8) * 4;   // full[3], empty[3]
   static constexpr uint32_t jq = bar + 2 * kR1Slots * 8;           // JobQueue slots
-  static constexpr uint32_t flag = jq + 16;
-  static constexpr uint32_t total = flag + 16;
+  static constexpr uint32_t flag = jq + 16;                        // the unit's block count
+  static constexpr uint32_t cstate = flag + 16;                    // cluster split: [3][132] chunk states
+  static constexpr uint32_t total = cstate + 3 * kSplitStride * 4;
 };
 
 
@@ -64,7 +66,10 @@ __device__ __forceinline__ void r1_merge(float& Ma, float& La, float& Oa, float 
   Ma = Mn;
 }
 
-template <bool kPaged, bool kSW, bool kSplit>
+// kClu: split-K on a thread-block cluster (one unit per cluster, one split per CTA): the chunk states
+// stay in each CTA's shared memory and rank 0 merges them in chunk order through DSMEM — the same
+// operations as the unsplit kernel, with no workspace, atomics or global round trip.
+template <bool kPaged, bool kSW, bool kClu>
 __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc qsrc, RowSrc ks, RowSrc vs,
                                                                    const int32_t* __restrict__ idx,
                                                                    const int32_t* __restrict__ cnt, float scale_log2,
@@ -79,8 +84,7 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
   float* mm = mo + 4 * 128;                                        // [4] warp maxima
   float* ml = mm + 4;                                              // [4] warp sums
   int* scan = reinterpret_cast<int*>(ml + 4);                      // [8] build_extra scratch
-  int* flag = reinterpret_cast<int*>(smem + L::flag);            // split-K: "this job merges"
-  int* scnt = flag + 1;                                            // the unit's block count
+  int* scnt = reinterpret_cast<int*>(smem + L::flag);             // the unit's block count
   const uint32_t full0 = sb + L::bar, empty0 = full0 + 8 * kR1Slots;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -97,12 +101,13 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
   uint32_t g = 0;  // ring items issued / consumed by this CTA so far (slot g % 3, parity (g / 3) & 1)
 
   const int64_t units = (int64_t)sh.B * sh.Hq * sh.nqb;
-  const int S = kSplit ? sh.splits : 1;
+  const int S = kClu ? sh.splits : 1;
+  float* cst = reinterpret_cast<float*>(smem + L::cstate);         // kClu: this CTA's chunk states
   JobQueue jq(sh.sched, smem + L::jq);
   for (int64_t jb = blockIdx.x; jb < units * S; jb = jq.next(jb)) {
     jq.claim();
-    const int64_t u = kSplit ? jb / S : jb;
-    const int sp = kSplit ? (int)(jb - u * S) : 0;
+    const int64_t u = kClu ? jb / S : jb;
+    const int sp = kClu ? (int)(jb - u * S) : 0;
     int b, h, q;
     unit_coords(sh, u, b, h, q);
     const int hk = h / (sh.Hq / sh.Hkv);
@@ -135,7 +140,8 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
     const int nit_all = (nall + 31) >> 5;
     const int nch_all = (nit_all + kR1ChunkItems - 1) / kR1ChunkItems;
     // this job's chunks [c_lo, c_hi) and items [i_lo, i_lo + nit)
-    const int c_lo = kSplit ? sp * nch_all / S : 0, c_hi = kSplit ? (sp + 1) * nch_all / S : nch_all;
+    const int c_lo = kClu ? sp * nch_all / S : 0;
+    const int c_hi = kClu ? (sp + 1) * nch_all / S : nch_all;
     const int i_lo = c_lo * kR1ChunkItems;
     const int nit = max(0, min(c_hi * kR1ChunkItems, nit_all) - i_lo);
     const int k_lo = i_lo * 32, nk = max(0, min(nit * 32, nall - k_lo));
@@ -284,12 +290,12 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
             Lc = fmaf(f, ml[w], Lc);
           }
         }
-        if constexpr (kSplit) {  // the chunk state goes to the workspace; the unit's last job merges
-          float* my = sh.part + (u * kSplitMax + (i_lo + i) / kR1ChunkItems) * kSplitStride;
-          __stcg(my + d, Oc);
+        if constexpr (kClu) {  // the chunk state stays in shared memory for rank 0's merge
+          float* my = cst + ((i_lo + i) / kR1ChunkItems - c_lo) * kSplitStride;
+          my[d] = Oc;
           if (d == 0) {
-            __stcg(my + 128, Mc);
-            __stcg(my + 129, Lc);
+            my[128] = Mc;
+            my[129] = Lc;
           }
         } else {
           r1_merge(Ma, La, Oa, Mc, Lc, Oc);
@@ -302,19 +308,22 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
     }
     g = g0 + (uint32_t)nit;
 
-    if constexpr (kSplit) {
-      // publish this job's chunk states; the job that arrives last merges all chunks of the unit in
-      // chunk order with r1_merge, exactly as one unsplit job would
-      __threadfence();
-      __syncthreads();
-      if (d == 0) *flag = atomicAdd(sh.arrive + u, 1u) == (unsigned)(S - 1);
-      __syncthreads();
-      if (!*flag) continue;
-      __threadfence();
-      const float* pu = sh.part + u * kSplitMax * kSplitStride;
-      for (int c = 0; c < nch_all; ++c)
-        r1_merge(Ma, La, Oa, __ldcg(pu + c * kSplitStride + 128), __ldcg(pu + c * kSplitStride + 129),
-                 __ldcg(pu + c * kSplitStride + d));
+    if constexpr (kClu) {
+      // every CTA's chunk states are in its shared memory; rank 0 merges them in chunk order (the
+      // owner of chunk c is the split whose range [r nch / S, (r + 1) nch / S) holds it), then a second
+      // cluster barrier keeps the other CTAs' shared memory alive until it has been read
+      cluster_sync();
+      if (sp == 0) {
+        int r = 0;
+        for (int c = 0; c < nch_all; ++c) {
+          while ((r + 1) * nch_all / S <= c) ++r;
+          const uint32_t a = smem_u32(cst + (c - r * nch_all / S) * kSplitStride);
+          r1_merge(Ma, La, Oa, ld_cluster_f32(a + 128 * 4, r), ld_cluster_f32(a + 129 * 4, r),
+                   ld_cluster_f32(a + d * 4, r));
+        }
+      }
+      cluster_sync();
+      if (sp != 0) continue;
     }
     const float M = Ma, Ls = La, O = Oa;
     __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(o + (b * osb + h * osh + (int64_t)q * sh.bq * ost) * 2);
@@ -332,11 +341,35 @@ bool attn_row1_supported(const Shape& sh) {
          sh.sink + sh.window <= kMaxExtra;
 }
 
-template <bool kPaged, bool kSW, bool kSplit>
+template <bool kPaged, bool kSW>
+static cudaError_t launch_r1_cluster(const Shape& s2, const QSrc& qs, const RowSrc& ks, const RowSrc& vs,
+                                     const int32_t* idx, const int32_t* cnt, float sm_scale, char* o, int64_t osb,
+                                     int64_t osh, int64_t ost, float* lse, cudaStream_t stream, int64_t grid) {
+  auto kern = attn_row1_kernel<kPaged, kSW, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Row1Smem::total);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kR1Threads);
+  cfg.dynamicSmemBytes = Row1Smem::total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)s2.splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, s2, qs, ks, vs, idx, cnt, sm_scale * kR1Log2e, o, osb, osh, ost, lse);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <bool kPaged, bool kSW>
 static cudaError_t launch_r1(const Shape& s2, const QSrc& qs, const RowSrc& ks, const RowSrc& vs, const int32_t* idx,
                              const int32_t* cnt, float sm_scale, char* o, int64_t osb, int64_t osh, int64_t ost,
                              float* lse, cudaStream_t stream, int64_t grid) {
-  auto kern = attn_row1_kernel<kPaged, kSW, kSplit>;
+  auto kern = attn_row1_kernel<kPaged, kSW, false>;
   int per_sm = 1;
   cudaError_t e = persistent_ctas(kern, kR1Threads, Row1Smem::total, 0, &per_sm);  // sets the smem attribute
   if (e != cudaSuccess) return e;
@@ -355,35 +388,30 @@ cudaError_t launch_attn_row1(const Shape& sh, const QSrc& qs, const RowSrc& ks, 
   const int64_t slots = (int64_t)num_sms * per_sm;
   Shape s2 = sh;
   // split-K only to fill CTA slots the units leave idle (never a second wave), and never into more
-  // jobs than a unit has 128-key chunks (the split granularity)
+  // jobs than a unit has 128-key chunks (the split granularity); a split unit runs on a cluster
   const int64_t max_keys = (int64_t)sh.n * sh.bk + ((sh.sink > 0 || sh.window > 0) ? sh.sink + sh.window : 0);
   const int64_t max_chunks = std::max<int64_t>(1, (max_keys + 32 * kR1ChunkItems - 1) / (32 * kR1ChunkItems));
   s2.splits = 1;
-  if (sh.part && sh.arrive && units <= kSplitMaxUnits)
+  if (units <= kSplitMaxUnits)
     s2.splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(kSplitMax, max_chunks), slots / units));
 #ifdef HIPATTN_TUNING
-  if (const char* e2 = getenv("HIPATTN_SPLITS"))
-    if (sh.part) s2.splits = std::max(1, std::min(kSplitMax, atoi(e2)));
+  if (const char* e2 = getenv("HIPATTN_SPLITS")) s2.splits = std::max(1, std::min(kSplitMax, atoi(e2)));
 #endif
-  if (s2.splits > 1) {
-    e = cudaMemsetAsync(s2.arrive, 0, (size_t)units * sizeof(unsigned int), stream);
-    if (e != cudaSuccess) return e;
-  }
-  const int64_t jobs = units * s2.splits;
-  const int64_t grid = std::min<int64_t>(jobs, slots);
-  if ((e = setup_queue(s2, jobs, grid, stream)) != cudaSuccess) return e;
   const bool sw = sh.sink > 0 || sh.window > 0;
-#define HIP_R1(P, W, SP) \
-  return launch_r1<P, W, SP>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid)
-  if (s2.splits > 1) {
-    if (ks.paged) { if (sw) HIP_R1(true, true, true); HIP_R1(true, false, true); }
-    if (sw) HIP_R1(false, true, true);
-    HIP_R1(false, false, true);
+  if (s2.splits > 1) {  // one cluster of `splits` CTAs per unit, chunk states merged through DSMEM (one wave)
+    s2.sched = nullptr;
+    const int64_t grid = units * s2.splits;
+    if (ks.paged) return sw ? launch_r1_cluster<true, true>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid)
+                            : launch_r1_cluster<true, false>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid);
+    return sw ? launch_r1_cluster<false, true>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid)
+              : launch_r1_cluster<false, false>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid);
   }
-  if (ks.paged) { if (sw) HIP_R1(true, true, false); HIP_R1(true, false, false); }
-  if (sw) HIP_R1(false, true, false);
-  HIP_R1(false, false, false);
-#undef HIP_R1
+  const int64_t grid = std::min<int64_t>(units, slots);
+  if ((e = setup_queue(s2, units, grid, stream)) != cudaSuccess) return e;
+  if (ks.paged) return sw ? launch_r1<true, true>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid)
+                          : launch_r1<true, false>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid);
+  return sw ? launch_r1<false, true>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid)
+            : launch_r1<false, false>(s2, qs, ks, vs, idx, cnt, sm_scale, o, osb, osh, ost, lse, stream, grid);
 }
 
 }  // namespace hip

@@ -73,9 +73,7 @@ struct Shape {
   int group;         // query heads per mask: H_q / H_kv for GQA-shared masks (reading G25), else 1
   const int32_t* seq_lens;
   unsigned int* sched;  // dynamic job counter (JobQueue), zeroed before the launch; nullptr = static
-  int splits;           // attention: split-K factor S (jobs = units x S, partials merged in-kernel), 1 = off
-  float* part;          // attention split-K: partials [units][S][d + 2] (workspace)
-  unsigned int* arrive; // attention split-K: arrivals per unit (workspace, zeroed before the launch)
+  int splits;           // single-row attention: split-K factor S (a cluster of S CTAs per unit), 1 = off
 };
 
 __device__ __forceinline__ int seq_len(const Shape& sh, int b) {
@@ -258,6 +256,13 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 }
 __device__ __forceinline__ void cluster_sync() {  // every thread of every CTA of the cluster
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t local_saddr, uint32_t rank) {
+  uint32_t ra;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(local_saddr), "r"(rank));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(ra) : "memory");
+  return v;
 }
 __device__ __forceinline__ void st_cluster_f32(uint32_t local_saddr, uint32_t rank, float v) {
   uint32_t ra;

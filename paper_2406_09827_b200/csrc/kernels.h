@@ -48,8 +48,9 @@ inline cudaError_t persistent_ctas(K kernel, int threads, size_t smem, int tmem_
   return cudaSuccess;
 }
 
-// Split-K of single-row attention units (attn_row1): at most kSplitMax splits, only for launches of at
-// most kSplitMaxUnits units; partial stride kSplitStride floats (O[128], max, sum, unrounded sum, pad).
+// Split-K of single-row attention units (attn_row1): at most kSplitMax splits (= the cluster size), only
+// for launches of at most kSplitMaxUnits units; a chunk state is kSplitStride floats (O[128], max, sum,
+// pad) in the CTA's shared memory.
 constexpr int kSplitMax = 8, kSplitMaxUnits = 4096, kSplitStride = 132;
 
 // Dynamic job claiming (common.cuh JobQueue) only pays when there are more jobs than resident
