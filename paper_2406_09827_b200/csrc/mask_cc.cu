@@ -21,6 +21,8 @@ constexpr int kCCStages = 4;  // cp.async ring depth: 3 chunks in flight while o
 
 template <typename T>
 struct CCScorer {
+  template <class ST>
+  __device__ __forceinline__ float* score_buf(ST& st, int) { return st.scores(); }
   const float* qs;   // [rows_q][qpitch] fp32
   int qpitch;        // floats
   char* stage0;      // kCCStages staged chunks of key rows

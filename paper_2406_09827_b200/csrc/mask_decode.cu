@@ -24,6 +24,8 @@ constexpr int kMDU = 16;     // rows per half-warp per batch (128 rows = 32 KB i
 
 template <typename T, int D, int RM, bool kPaged>
 struct LaneScorer {
+  template <class ST>
+  __device__ __forceinline__ float* score_buf(ST& st, int) { return st.scores(); }
   static constexpr int E = D / 16;                 // elements per lane
   static constexpr int NV = (E * (int)sizeof(T) + 15) / 16;  // 16-byte vectors per lane (1 or 2)
   const float* qs;   // [rows_q][D] fp32 (smem)

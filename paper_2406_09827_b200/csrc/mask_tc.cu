@@ -55,7 +55,7 @@ __device__ int64_t g_dbg_stride = 0;
 #define HIP_DBG_STORE(blk, v) do { } while (0)
 #endif
 
-template <int SLOTS, bool PAGED = false>
+template <int SLOTS, bool PAGED = false, bool CLU = false>
 struct MaskTCSmemLayout {
   static constexpr uint32_t k0 = 0;                                        // ring (1024-aligned)
   static constexpr uint32_t q = k0 + SLOTS * kMTSlot;                      // Q tile
@@ -64,7 +64,8 @@ struct MaskTCSmemLayout {
   static constexpr uint32_t bt_bytes = PAGED ? (uint32_t)align_up(kBt16Max * 2, 128) : 0u;  // uint16 row
   static constexpr uint32_t misc = bt + bt_bytes;                          // mbarriers, TMEM address
   static constexpr uint32_t jq = misc + (uint32_t)align_up(8 * SLOTS + 4, 16); // JobQueue slots (2 x int64)
-  static constexpr uint32_t total = jq + 16;
+  static constexpr uint32_t dsc = jq + 16;                                  // CLU: 2 score arrays
+  static constexpr uint32_t total = dsc + (CLU ? 2u * 4u * (uint32_t)SelState<kMTNmax, 4>::kRep : 0u);
 };
 
 template <int NT, int SLOTS, int TT, bool kPaged, class Sync, bool kGrp = false, bool kRow1 = false, bool kBk2 = false,
@@ -86,6 +87,7 @@ struct TCScorer {
   int64_t tpos0;
   const int* pg;         // paged: page of each representative block (aliases the score output)
   const uint16_t* bt16 = nullptr;  // paged: the sequence's block-table row staged in shared memory
+  float* dsc = nullptr;  // CL > 1: two score arrays, alternating by iteration (select.cuh score_buf)
   // this thread's source rows of the tile being issued (kBk2: the first row of each of its 4 blocks;
   // the second row is the first plus one row stride)
   const char* rp[kBk2 ? 4 : RJ];
@@ -169,6 +171,12 @@ struct TCScorer {
                   ((rok >> j) & (ckeep >> h) & 1u) ? 16u : 0u);
   }
 
+  template <class ST>
+  __device__ __forceinline__ float* score_buf(ST& st, int iter) {
+    if constexpr (CL > 1) return dsc + (iter & 1) * ST::kRep;
+    else return st.scores();
+  }
+
   __device__ __forceinline__ void wait_slot(int slot) {
     if (pend & (1u << slot)) {
       mbar_wait_u32(mbar + 8u * slot, (phase >> slot) & 1u);
@@ -236,10 +244,9 @@ struct TCScorer {
   __device__ void score(const int* rep, int n_rep, float* out) {
     const int ntiles_all = (n_rep + bpt - 1) / bpt;
     // CL > 1: the cluster's CTAs hold identical search states; CTA `crank` gathers and scores tiles
-    // crank, crank + CL, ... and stores each score into every CTA's score array (DSMEM).  A cluster
-    // barrier first (every CTA has read its nodes for this iteration: the scores alias the node
-    // arrays) and last (every score everywhere before the selections).
-    if constexpr (CL > 1) cluster_sync();
+    // crank, crank + CL, ... and stores each score into every CTA's score array of this iteration's
+    // parity (DSMEM).  One cluster barrier at the end (every score everywhere before the
+    // selections); a peer already writing the next iteration's scores uses the other array.
     const int ntiles = CL == 1 ? ntiles_all : (ntiles_all > crank ? (ntiles_all - crank + CL - 1) / CL : 0);
     if constexpr (kPaged) {
       // one block-table lookup per representative block for the whole call (a block never straddles
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   char* base = smem_raw + pad;
   const uint32_t sbase = raw + pad;
-  using L = MaskTCSmemLayout<SLOTS, kPaged>;
+  using L = MaskTCSmemLayout<SLOTS, kPaged, (CL > 1)>;
   SelState<kMTNmax, 4>& st = *reinterpret_cast<SelState<kMTNmax, 4>*>(base + L::sel);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L::misc);  // one MMA-completion barrier per slot
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::misc + 8 * SLOTS);
@@ -424,6 +431,7 @@ __global__ void __launch_bounds__(128, MINB) mask_tc_kernel(Shape sh, QSrc qsrc,
     }
     TCScorer<NT, SLOTS, TT, kPaged, Sync, kGrp, kRow1, kBk2, CL> sc;
     sc.crank = crank;
+    if constexpr (CL > 1) sc.dsc = reinterpret_cast<float*>(base + L::dsc);
     sc.q_s = q_s;
     sc.k_s0 = sbase + L::k0;
     sc.mbar = smem_u32(mbar);
@@ -498,7 +506,7 @@ static cudaError_t launch_v(const Shape& sh, const QSrc& qs, const RowSrc& ks, i
 template <int SLOTS, int TT, int EXT, int CL>
 static cudaError_t launch_cluster(const Shape& sh, const QSrc& qs, const RowSrc& ks, int32_t* idx, int32_t* cnt,
                                   cudaStream_t stream) {
-  const size_t smem = (ks.paged ? MaskTCSmemLayout<SLOTS, true>::total : MaskTCSmemLayout<SLOTS, false>::total) + 1024;
+  const size_t smem = (ks.paged ? MaskTCSmemLayout<SLOTS, true, true>::total : MaskTCSmemLayout<SLOTS, false, true>::total) + 1024;
   auto kern = ks.paged ? mask_tc_kernel<SLOTS, TT, true, 1, EXT, CL> : mask_tc_kernel<SLOTS, TT, false, 1, EXT, CL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -234,6 +234,10 @@ __device__ __forceinline__ bool chunk_job(int Bq, int n, int S, int s, int& lo, 
   return true;
 }
 
+// Scorer::score_buf(st, iter) names the array the scores of iteration `iter` go to: st.scores() (the
+// node arrays, dead while scoring) for the single-CTA scorers; a cluster scorer alternates two
+// arrays of its own by iteration parity, so a peer CTA may already write the next iteration's scores
+// while this CTA still reads this iteration's (one cluster barrier per iteration instead of two).
 // Runs the tree search of one query block over the L key blocks [lo, lo + L) (lo = 0, L = B_q:
 // Alg. 1; one chunk of the stridden partial top-k otherwise, reading G21) and writes the n
 // selected blocks (ascending, -1 padded) to out_idx and, if out_cnt, the count.  All NT threads
@@ -328,12 +332,13 @@ __device__ void tree_search(SelState<NMAX, NW>& st, int n, int lo, int Bq, Score
     Sync::sync();
     scorer.mark(0);  // split + scan
     // --- representative scores (Alg. 1 lines 10-13)
-    scorer.score(st.rep, first ? C : nB, st.scores());
+    float* const sbuf = scorer.score_buf(st, iter);  // the scores array of this iteration
+    scorer.score(st.rep, first ? C : nB, sbuf);
     // --- top-n (Alg. 1 lines 14-15)
     uint64_t key[EC];
 #pragma unroll
     for (int k = 0; k < EC; ++k)
-      key[k] = make_key(kr[k] >= 0 ? ord_score(st.scores()[kr[k]]) : ks[k], kf[k]);
+      key[k] = make_key(kr[k] >= 0 ? ord_score(sbuf[kr[k]]) : ks[k], kf[k]);
     uint64_t prefix, mask;
     scorer.mark(8);  // keys
     uint32_t live = valid;
