@@ -195,18 +195,27 @@ __global__ void __launch_bounds__(kR1Threads, 4) attn_row1_kernel(Shape sh, QSrc
     const uint32_t g0 = g;
     auto issue = [&](int i) {
       const uint32_t gi = g0 + (uint32_t)i, slot = gi % kR1Slots;
+      const int cc = tid & 15;
+      // the thread's 4 keys (8 jj + tid / 16; K and V rows of each) and their source rows are read
+      // and addressed before waiting for the slot, so its 8 copies go out as soon as it is free
+      const char* ksrc[4];
+      const char* vsrc[4];
+      uint32_t okm = 0;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int row = tok[i * 32 + 8 * jj + (tid >> 4)];
+        ksrc[jj] = kbase + (uint64_t)(uint32_t)max(row, 0) * krow + cc * 16;
+        vsrc[jj] = vbase + (uint64_t)(uint32_t)max(row, 0) * vrow + cc * 16;
+        okm |= (uint32_t)(row >= 0) << jj;
+      }
       if (gi >= (uint32_t)kR1Slots) mbar_wait_u32(empty0 + 8 * slot, ((gi / kR1Slots) - 1) & 1u);
       const uint32_t dst0 = sb + L::ring + slot * kR1Item;
-      const int cc = tid & 15;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int r = 8 * j + (tid >> 4);  // 0..63
-        const int key = r & 31;
-        const int row = tok[i * 32 + key];
-        const bool isv = r >= 32;
-        const char* src = (isv ? vbase : kbase) + (uint64_t)(uint32_t)max(row, 0) * (isv ? vrow : krow) + cc * 16;
+        const int jj = j & 3, key = 8 * jj + (tid >> 4);
+        const bool isv = j >= 4;
         const uint32_t dst = dst0 + (isv ? 8192u : 0u) + key * 256 + ((cc ^ ((key & 1) << 2)) << 4);
-        cp_async16(dst, src, row >= 0 ? 16u : 0u);
+        cp_async16(dst, isv ? vsrc[jj] : ksrc[jj], ((okm >> jj) & 1u) ? 16u : 0u);
       }
       cp_async_mbar_arrive_noinc(full0 + 8 * slot);
     };
