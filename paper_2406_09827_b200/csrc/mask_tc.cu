@@ -143,6 +143,11 @@ struct TCScorer {
   // row stride (a block never straddles a page).  A warp instruction j still moves 4 whole 128-byte
   // half rows (rows 8g + j, g = 4w..4w+3).
   __device__ __forceinline__ void issue_bk2(const int* rep, int n_rep, int c, int h, int c8, int g, int i) {
+    prep_bk2(rep, n_rep, c, h, g, c8);
+    fire_bk2(h, c8, g, i);
+  }
+  // the row pointers of a tile, at its first half (before the slot it goes to is free)
+  __device__ __forceinline__ void prep_bk2(const int* rep, int n_rep, int c, int h, int g, int c8) {
     if (h == 0) {
       const int blk0 = c * bpt, nblk = min(bpt, n_rep - blk0);
       const int4 rv = *reinterpret_cast<const int4*>(rep + blk0 + 4 * g);
@@ -163,6 +168,8 @@ struct TCScorer {
         rok |= ((uint32_t)ok0 << (2 * b2)) | ((uint32_t)ok1 << (2 * b2 + 1));
       }
     }
+  }
+  __device__ __forceinline__ void fire_bk2(int h, int c8, int g, int i) {
     const uint32_t dst = k_s0 + (uint32_t)(i % SLOTS) * kMTSlot + g * 1024;
     const uint32_t x = (uint32_t)c8;
 #pragma unroll
@@ -292,9 +299,17 @@ struct TCScorer {
         mark(12);  // MMA issue
         // refill this slot with item i + SLOTS as soon as MMA(i) has read it
         if (i + SLOTS < nitems) {
+          if constexpr (kBk2) {  // the refill's addresses first, then wait for the slot
+            const int ii = i + SLOTS, tid = Sync::tid();
+            prep_bk2(rep, n_rep, gtile(c0 + (ii >> 1)), ii & 1, tid >> 3, tid & 7);
+            wait_slot(slot);
+            mark(13);  // MMA completion wait
+            fire_bk2(ii & 1, tid & 7, tid >> 3, ii);
+          } else {
           wait_slot(slot);
           mark(13);  // MMA completion wait
           issue(rep, n_rep, c0, i + SLOTS);
+          }
         }
         cp_async_commit();
         mark(14);  // refill issue
