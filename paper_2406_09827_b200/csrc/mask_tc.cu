@@ -6,7 +6,7 @@
 // a CTA of 128 threads gathers the (up to 2n, then n) representative key blocks of its query block,
 // 128 key rows per tile, straight from L2/HBM into 128-byte-swizzled K-major shared memory
 // (coalesced 16-byte cp.async, 8 threads per 128-byte half row, so every warp instruction moves
-// whole 32-byte sectors), and one thread issues
+// whole 32-byte sectors), and one elected lane of warp 0 issues
 //     S^T_c [128 keys x 32 queries] = K_tile_c [128 x 128] . Q_block^T   (tcgen05.mma, M=128, N=32)
 // into TMEM columns [32c, 32c+32) as two d-halves ("items", 4 x K16 each).  Items stream through a
 // ring of SLOTS 16 KB shared slots: the MMA of an item is issued as soon as its bytes land and the
