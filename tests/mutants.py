@@ -60,6 +60,7 @@ MUTANTS = {
 
 def main():
     src = open(SRC).read()
+    os.makedirs("/tmp/mut", exist_ok=True)
     survived = []
     for name, (a, b) in MUTANTS.items():
         assert a in src, name
