@@ -40,7 +40,9 @@
 extern "C" {
 #endif
 
-#define HIP_ATTN_VERSION 200 /* 2.0.0: every compute call takes a workspace (prefill gained the two
+#define HIP_ATTN_VERSION 201 /* 2.0.1: hip_workspace_bytes is 256 for every call (split single-row
+                                 attention merges on thread-block clusters; 2.0 callers unaffected);
+                                 2.0.0: every compute call takes a workspace (prefill gained the two
                                  arguments); 1.2.0: + HIP_FLAG_GQA_SHARED_MASK (1.1.0: top_r,
                                  split_jitter, sample_seed, hip_mask_vote) */
 

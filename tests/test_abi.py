@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     lib = H.load()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.hip_version() == 200
+    assert lib.hip_version() == 201
 
 
 def test_nm_dynamic_symbols():
